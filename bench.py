@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: fp64 CG matvec dF -> G(K4 : dF^T).
+
+Workload (BASELINE.json config 2): 256^3 voxels, St. Venant-Kirchhoff,
+Bernoulli(0.3) two-phase microstructure from mt19937_64(seed 2), stiffness
+contrast 10, tangent K4 evaluated at F_bar = I + 0.1 e_x (x) e_y.  One step =
+one application of the projected tangent (the CG matvec) over all 256^3
+voxels, inputs resident in HBM (12 GB of K4 + dF: far larger than L2, so no
+flush is needed between steps).
+
+  value  : matvec voxels/s, device-resident (whole job, all ranks)
+  e2e    : the same metric through the C ABI with host buffers: a full
+           Newton solve of config 2 (fm_solve_increment) with F uploaded from
+           pinned host memory and F, P read back inside the timed region;
+           value = (matvecs issued) * n / wall time.
+  roofline: the dominant kernel (pass 1: K4 contraction + z r2c FFT) and the
+           whole matvec against MEASURED_PEAKS.json hbm_gbs.
+
+--impl reference times the CPU oracle (restatement of the reference
+apply_projected_tangent; the reference itself needs FFTW3/Eigen3, absent on
+the box) on a bounded 128^3 sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic bytes per voxel: every pass reads and writes
+# one 9-component fp64 field (72 + 72 B); pass 1 also reads K4 (648 B).
+PASS_BYTES = [648 + 72 + 72, 144, 144, 144, 144]  # z-fwd(+K4), y-fwd, x+ghat, y-inv, z-inv
+MATVEC_BYTES = sum(PASS_BYTES)  # 1368 = B_mv
+PASS_NAMES = ["z_fwd_k4", "y_fwd", "x_ghat", "y_inv", "z_inv"]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and not s[2 + i].startswith("Not")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
+
+
+def config2_inputs(N, seed=2):
+    from paper_1603_08893_b200 import microstructure as M
+    pg = M.bernoulli((N, N, N), 0.3, seed)
+    lam, mu, _, _ = M.bind_parameters(pg, [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)])
+    return lam, mu
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_run(args, world, rank):
+    """`--impl reference`: the CPU oracle (restated reference) on host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    N = args.cpu_grid
+    n = N ** 3
+    lam, mu = config2_inputs(N)
+    F = np.zeros(9 * n)
+    for i in range(3):
+        F[(i * 3 + i) * n:(i * 3 + i + 1) * n] = 1.0
+    F[1 * n:2 * n] = 0.1
+    _, K, st, _ = O.hyper_evaluate(F, lam, mu, 3)
+    dF = 2.0 * np.random.default_rng(0).random(9 * n) - 1.0
+    for _ in range(args.warmup):
+        O.time_projected_tangent((N, N, N), K, dF, reps=1)
+    t = [O.time_projected_tangent((N, N, N), K, dF, reps=1) for _ in range(args.steps)]
+    sec = float(np.mean(t))
+    v = n / sec
+    line = {
+        "metric": "fp64 CG matvec voxels/s (G:K4:dF)", "value": v, "unit": "voxel/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"config2 sample: {N}^3 SVK Bernoulli(0.3) contrast 10, one G:K4:dF matvec per step"},
+        "cpu_baseline": {"value": v, "unit": "voxel/s", "cores": 1, "kind": "port",
+                         "sample": f"{N}^3 apply_projected_tangent per step (reference is single-threaded; "
+                                   f"FFTW3/Eigen3 absent so the oracle restatement is timed)"},
+        "e2e": {"value": v, "unit": "voxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline_sample(N):
+    """Bounded oracle sample (10-30 s of single-core CPU work)."""
+    from oracle import oracle as O
+    n = N ** 3
+    lam, mu = config2_inputs(N)
+    F = np.zeros(9 * n)
+    for i in range(3):
+        F[(i * 3 + i) * n:(i * 3 + i + 1) * n] = 1.0
+    F[1 * n:2 * n] = 0.1
+    _, K, _, _ = O.hyper_evaluate(F, lam, mu, 3)
+    dF = 2.0 * np.random.default_rng(0).random(9 * n) - 1.0
+    sec = O.time_projected_tangent((N, N, N), K, dF, reps=1)
+    return {"value": n / sec, "unit": "voxel/s", "cores": 1, "kind": "port",
+            "sample": f"one {N}^3 G:K4:dF apply_projected_tangent (oracle restatement, 1 thread; "
+                      f"reference needs FFTW3/Eigen3, absent on the box)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--grid", type=int, default=256)
+    ap.add_argument("--cpu-grid", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        cpu_reference_run(args, world, rank)
+        return
+
+    import torch
+    from paper_1603_08893_b200 import abi
+
+    N = args.grid
+    n = N ** 3
+    lam, mu = config2_inputs(N)
+    ctx = abi.Context((N, N, N), 3, device=local)
+    model = abi.Model(ctx, "hyper", lam, mu)
+    fbar = np.eye(3)
+    fbar[0, 1] = 0.1
+    F0 = abi.identity_field((N, N, N), 3)
+    F0[1 * n:2 * n] = 0.1
+    F = ctx.field(9, F0)
+    P = ctx.field(9)
+    model.evaluate(F, P)  # K4 at F_bar
+    dF = ctx.field(9, 2.0 * np.random.default_rng(0).random(9 * n) - 1.0)
+    out = ctx.field(9)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+
+    for _ in range(args.warmup):
+        model.apply(dF, out)
+    ctx.sync()
+    barrier(world)
+    ctx.sync()
+    ctx.profile(True)
+    l0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            model.apply(dF, out)
+        ev1.record(stream)
+        ev1.synchronize()
+    launches = (ctx.launches - l0)
+    pass_ms, calls = ctx.profile_read()
+    ctx.profile(False)
+    ms_total = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_total, world)
+    barrier(world)
+    ms_step = ms_total / args.steps
+    value = world * n / (ms_step * 1e-3)
+
+    hbm, src = peaks()
+    per_pass = pass_ms / max(calls, 1)
+    dom = int(np.argmax(per_pass))  # the dominant kernel of the step
+    achieved = PASS_BYTES[dom] * n / (per_pass[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": PASS_NAMES[dom], "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_source": src,
+                "algorithmic_bytes_per_voxel": PASS_BYTES[dom],
+                "passes_ms": {k: float(v) for k, v in zip(PASS_NAMES, per_pass)},
+                "matvec": {"bytes_per_voxel": MATVEC_BYTES,
+                           "achieved": MATVEC_BYTES * n / (ms_step * 1e-3) / 1e9,
+                           "frac": MATVEC_BYTES * n / (ms_step * 1e-3) / 1e9 / hbm}}
+
+    # ---- e2e: full config-2 Newton solve through the C ABI with host buffers
+    e2e = None
+    newton = None
+    if not args.no_e2e:
+        hostF = torch.from_numpy(abi.identity_field((N, N, N), 3)).pin_memory().numpy()
+        hostP = torch.empty(9 * n, dtype=torch.float64).pin_memory().numpy()
+        model2 = abi.Model(ctx, "hyper", lam, mu)
+        Fd = ctx.field(9)
+        Pd = ctx.field(9)
+        barrier(world)
+        t0 = time.perf_counter()
+        Fd.upload(hostF)
+        rep = model2.solve_increment(Fd, fbar, P_out=Pd)
+        Fres = Fd.download()
+        Pres = Pd.download()
+        wall = time.perf_counter() - t0
+        wall = max_over_ranks(wall, world)
+        e2e = {"value": world * rep["matvecs"] * n / wall, "unit": "voxel/s",
+               "h2d_bytes_per_step": int(hostF.nbytes), "d2h_bytes_per_step": int(Fres.nbytes + Pres.nbytes),
+               "what": "fm_solve_increment of config 2 from host F (upload + device Newton/CG + F,P download)"}
+        newton = {"solve_s": wall, "passes": rep["passes"], "cg_iterations": rep["cg_it"],
+                  "matvecs": rep["matvecs"], "rel_update": rep["rel_update"]}
+        model2.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample(args.cpu_grid)
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": "fp64 CG matvec voxels/s (G:K4:dF)", "value": value, "unit": "voxel/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config2: {N}^3 SVK Bernoulli(0.3) seed 2, contrast 10, "
+                                   "G:K4:dF matvec (K4 at F_bar)",
+                       "grid": [N, N, N], "parallelism": f"replicas x{world}",
+                       "l2": "inputs 12 GB > 126 MB L2, no flush"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "newton_solve": newton,
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    barrier(world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,233 @@
+// BLAS-1 and reductions over component-major fields (fields.cpp:14-67,
+// tensor_ops.cpp:276-294).  Reductions are deterministic: a fixed number of
+// blocks (fixed per context) accumulate grid-strided chunks in a fixed order,
+// reduce with warp shuffles, and one block sums the partials in a fixed
+// order -- byte-identical reruns, as the reference requires
+// (test_config_io.cpp:203-229).
+#include "fm_internal.cuh"
+
+namespace fm {
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double wsum[kRedThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) wsum[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < kRedThreads / 32; ++w) s += wsum[w];
+  }
+  return s;  // valid in thread 0
+}
+
+// Scalar slots in ctx->d_scal used by the CG driver (solver.cu).
+enum Slot { S_RR = 0, S_PAP = 1, S_RRNEW = 2, S_ALPHA = 3, S_BETA = 4, S_FLAG = 5, S_OUT = 8 };
+
+__global__ void __launch_bounds__(kRedThreads) k_dot_partial(const double* __restrict__ a,
+                                                             const double* __restrict__ b,
+                                                             int64_t count, double* partial) {
+  double s = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t c2 = count / 2;
+  const double2* a2 = reinterpret_cast<const double2*>(a);
+  const double2* b2 = reinterpret_cast<const double2*>(b);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < c2; i += stride) {
+    const double2 x = __ldg(a2 + i), y = __ldg(b2 + i);
+    s += x.x * y.x;
+    s += x.y * y.y;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (count & 1)) s += a[count - 1] * b[count - 1];
+  s = block_sum(s);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// per-component sums: grid (blocks, ncomp)
+__global__ void __launch_bounds__(kRedThreads) k_sum_comp_partial(const double* __restrict__ a,
+                                                                  int64_t n, double* partial) {
+  const double* slab = a + int64_t(blockIdx.y) * n;
+  double s = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    s += __ldg(slab + i);
+  s = block_sum(s);
+  if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+}
+
+// op: 0 -> out[slot + comp] = sum;  1 -> CG pAp step;  2 -> CG rr_new step
+__global__ void __launch_bounds__(kRedThreads) k_finalize(const double* __restrict__ partial,
+                                                          int nb, double* scal, int op, int slot) {
+  const double* p = partial + blockIdx.x * nb;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) s += p[i];
+  s = block_sum(s);
+  if (threadIdx.x != 0) return;
+  if (op == 0) {
+    scal[slot + blockIdx.x] = s;
+  } else if (op == 1) {  // solver.cpp:37-45
+    scal[S_PAP] = s;
+    const bool bad = !(s > 0.0);
+    scal[S_FLAG] = bad ? 1.0 : 0.0;
+    scal[S_ALPHA] = bad ? 0.0 : scal[S_RR] / s;
+  } else {  // solver.cpp:48-53
+    if (scal[S_FLAG] != 0.0) return;
+    scal[S_RRNEW] = s;
+    scal[S_BETA] = s / scal[S_RR];
+    scal[S_RR] = s;
+  }
+}
+
+// x += alpha p; r -= alpha Ap; partial <r,r>   (solver.cpp:46-48)
+__global__ void __launch_bounds__(kRedThreads) k_cg_update(double* __restrict__ x,
+                                                           double* __restrict__ r,
+                                                           const double* __restrict__ p,
+                                                           const double* __restrict__ Ap,
+                                                           int64_t count, const double* scal,
+                                                           double* partial) {
+  if (scal[S_FLAG] != 0.0) return;
+  const double alpha = scal[S_ALPHA];
+  double s = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double ri = __dadd_rn(r[i], __dmul_rn(-alpha, Ap[i]));
+    r[i] = ri;
+    s += ri * ri;
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// p = beta p + r   (solver.cpp:51-55, p *= beta; p += r)
+__global__ void k_cg_direction(double* __restrict__ p, const double* __restrict__ r,
+                               int64_t count, const double* scal) {
+  const double beta = scal[S_BETA];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride)
+    p[i] = __dadd_rn(__dmul_rn(p[i], beta), r[i]);
+}
+
+__global__ void k_axpy(double a, const double* __restrict__ x, double* __restrict__ y, int64_t count) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride)
+    y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
+}
+
+__global__ void k_scale(double* x, double s, int64_t count) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride)
+    x[i] *= s;
+}
+
+__global__ void k_add(double* __restrict__ y, const double* __restrict__ x, double sign, int64_t count) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride)
+    y[i] = sign > 0 ? y[i] + x[i] : y[i] - x[i];
+}
+
+struct Uni {
+  double t[9];
+};
+
+__global__ void k_uniform(double* f, Uni u, int ncomp, int64_t n, int add) {
+  const int64_t count = n * ncomp;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride) {
+    const double v = u.t[i / n];
+    f[i] = add ? f[i] + v : 0.0 + v;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static int ew_blocks(int64_t count) {
+  const int64_t b = (count + 255) / 256;
+  return int(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+int dot_async(fm_ctx* ctx, const double* a, const double* b, int64_t count, double* d_out) {
+  k_dot_partial<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(a, b, count, ctx->d_partial);
+  FM_LAUNCHED(ctx);
+  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, ctx->red_blocks, d_out, 0, 0);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+int sum_comp_async(fm_ctx* ctx, const double* a, int ncomp, int64_t n, double* d_out) {
+  const int nb = ctx->red_blocks / 16 > 0 ? ctx->red_blocks / 16 : 1;
+  k_sum_comp_partial<<<dim3(nb, ncomp), kRedThreads, 0, ctx->stream>>>(a, n, ctx->d_partial);
+  FM_LAUNCHED(ctx);
+  k_finalize<<<ncomp, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, nb, d_out, 0, 0);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+int axpy_async(fm_ctx* ctx, double a, const double* x, double* y, int64_t count) {
+  k_axpy<<<ew_blocks(count), 256, 0, ctx->stream>>>(a, x, y, count);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+int scale_async(fm_ctx* ctx, double* x, double s, int64_t count) {
+  k_scale<<<ew_blocks(count), 256, 0, ctx->stream>>>(x, s, count);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+int add_async(fm_ctx* ctx, double* y, const double* x, double sign, int64_t count) {
+  k_add<<<ew_blocks(count), 256, 0, ctx->stream>>>(y, x, sign, count);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+static int uniform_async(fm_ctx* ctx, double* f, const double* t, int ncomp, int64_t n, int add) {
+  Uni u{};
+  for (int c = 0; c < ncomp && c < 9; ++c) u.t[c] = t[c];
+  k_uniform<<<ew_blocks(n * ncomp), 256, 0, ctx->stream>>>(f, u, ncomp, n, add);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+int add_uniform_async(fm_ctx* ctx, double* f, const double* t, int ncomp, int64_t n) {
+  return uniform_async(ctx, f, t, ncomp, n, 1);
+}
+int fill_uniform_async(fm_ctx* ctx, double* f, const double* t, int ncomp, int64_t n) {
+  return uniform_async(ctx, f, t, ncomp, n, 0);
+}
+
+int fetch_scalars(fm_ctx* ctx, int count) {
+  FM_CUDA(ctx, cudaMemcpyAsync(ctx->h_scal, ctx->d_scal, sizeof(double) * count,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+  FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FM_OK;
+}
+
+int cg_update_async(fm_ctx* ctx, double* x, double* r, const double* p, const double* Ap,
+                    int64_t count) {
+  k_cg_update<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(x, r, p, Ap, count, ctx->d_scal,
+                                                                ctx->d_partial);
+  FM_LAUNCHED(ctx);
+  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, ctx->red_blocks, ctx->d_scal, 2, 0);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count) {
+  k_cg_direction<<<ew_blocks(count), 256, 0, ctx->stream>>>(p, r, count, ctx->d_scal);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+// pAp finalisation used by the CG driver
+int cg_pap_async(fm_ctx* ctx, const double* p, const double* Ap, int64_t count) {
+  k_dot_partial<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(p, Ap, count, ctx->d_partial);
+  FM_LAUNCHED(ctx);
+  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, ctx->red_blocks, ctx->d_scal, 1, 0);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+}  // namespace fm

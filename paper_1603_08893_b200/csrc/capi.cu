@@ -1,0 +1,477 @@
+// extern "C" boundary of libfftmech_b200.so (include/fftmech_b200.h).
+// Every entry point validates its arguments the way the reference does
+// (std::invalid_argument -> FM_E_INVALID) and returns an fm_status; there
+// is no CPU fallback anywhere behind it.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "fm_internal.cuh"
+
+namespace fm {
+
+int set_error(fm_ctx* ctx, int status, const std::string& msg) {
+  if (ctx) {
+    ctx->last_error = msg;
+    ctx->last_info = fm_error_info{status, 0, -1, 0.0};
+  }
+  return status;
+}
+
+int check_cuda(fm_ctx* ctx, cudaError_t e, const char* what) {
+  const int st = e == cudaErrorMemoryAllocation ? FM_E_OOM : FM_E_CUDA;
+  return set_error(ctx, st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int ensure_field(fm_ctx* ctx, fm_field& f, int ncomp) {
+  if (f.d && f.ncomp == ncomp) return FM_OK;
+  if (f.d) cudaFree(f.d);
+  f.d = nullptr;
+  f.ncomp = ncomp;
+  f.n = ctx->n;
+  FM_CUDA(ctx, cudaMalloc(&f.d, sizeof(double) * size_t(ncomp) * size_t(ctx->n)));
+  return FM_OK;
+}
+
+void release_field(fm_field& f) {
+  if (f.d) cudaFree(f.d);
+  f = fm_field{};
+}
+
+// Radix plan: 4s, then 2, then odd primes ascending (any leftover prime is
+// one direct stage) -- the generic Stockham engine takes any radix.
+static void make_plan(AxisPlan& p, int N) {
+  p.N = N;
+  p.nst = 0;
+  int m = N;
+  while (m % 4 == 0 && p.nst < kMaxStages) { p.radix[p.nst++] = 4; m /= 4; }
+  while (m % 2 == 0 && p.nst < kMaxStages) { p.radix[p.nst++] = 2; m /= 2; }
+  for (int f = 3; f * f <= m; f += 2)
+    while (m % f == 0 && p.nst < kMaxStages) { p.radix[p.nst++] = f; m /= f; }
+  if (m > 1) p.radix[p.nst++] = m;
+}
+
+static void twiddles(std::vector<double2>& all, int N, size_t& off) {
+  off = all.size();
+  const long double tau = 6.283185307179586476925286766559005768L;
+  for (int k = 0; k < N; ++k) {
+    const long double a = -tau * (long double)k / (long double)N;
+    all.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+  }
+}
+
+}  // namespace fm
+
+using namespace fm;
+
+extern "C" {
+
+int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdim,
+                  int nyquist_mode, int device, fm_ctx** out) {
+  if (!out || !points || !lengths) return FM_E_INVALID;
+  *out = nullptr;
+  if (dim != 2 && dim != 3) return FM_E_INVALID;
+  for (int a = 0; a < dim; ++a)
+    if (points[a] < 1 || !(lengths[a] > 0.0)) return FM_E_INVALID;
+  if (tdim < dim || tdim > 3) return FM_E_INVALID;
+  if (nyquist_mode != 0 && nyquist_mode != 1) return FM_E_INVALID;
+  fm_ctx* ctx = new (std::nothrow) fm_ctx;
+  if (!ctx) return FM_E_OOM;
+  ctx->dim = dim;
+  for (int a = 0; a < 3; ++a) {
+    ctx->pts[a] = a < dim ? points[a] : 1;
+    ctx->len[a] = a < dim ? lengths[a] : 1.0;
+  }
+  ctx->tdim = tdim;
+  ctx->ncomp = tdim * tdim;
+  ctx->mode = nyquist_mode;
+  ctx->Nx = ctx->pts[0];
+  ctx->Ny = ctx->pts[1];
+  ctx->Nz = ctx->pts[2];
+  ctx->n = int64_t(ctx->Nx) * ctx->Ny * ctx->Nz;
+  const bool even = ctx->Nz % 2 == 0;
+  ctx->nzh = (even && nyquist_mode == FM_NYQUIST_ZERO_COMPATIBLE) ? ctx->Nz / 2 : ctx->Nz / 2 + 1;
+  ctx->Lz = even ? ctx->Nz / 2 : ctx->Nz;
+  ctx->device = device;
+  auto fail = [&](int st) {
+    fm_ctx_destroy(ctx);
+    return st;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return fail(FM_E_CUDA);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(FM_E_CUDA);
+  make_plan(ctx->px, ctx->Nx);
+  make_plan(ctx->py, ctx->Ny);
+  make_plan(ctx->pz, ctx->Nz);
+  make_plan(ctx->pzh, even ? ctx->Nz / 2 : 1);
+  std::vector<double2> tw;
+  size_t ox, oy, oz, ozh;
+  twiddles(tw, ctx->Nx, ox);
+  twiddles(tw, ctx->Ny, oy);
+  twiddles(tw, ctx->Nz, oz);
+  twiddles(tw, even ? ctx->Nz / 2 : 1, ozh);
+  if (cudaMalloc(&ctx->d_tw, tw.size() * sizeof(double2)) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(FM_E_CUDA);
+  ctx->px.tw = ctx->d_tw + ox;
+  ctx->py.tw = ctx->d_tw + oy;
+  ctx->pz.tw = ctx->d_tw + oz;
+  ctx->pzh.tw = ctx->d_tw + ozh;
+  const size_t spec_elems = size_t(ctx->ncomp) * ctx->Nx * ctx->Ny * ctx->nzh;
+  if (cudaMalloc(&ctx->spec, spec_elems * sizeof(double2)) != cudaSuccess) return fail(FM_E_OOM);
+  const int64_t half = (ctx->n * ctx->ncomp) / 2;
+  int64_t rb = (half + 255) / 256;
+  ctx->red_blocks = int(rb < 1 ? 1 : (rb > 148 * 4 ? 148 * 4 : rb));
+  if (cudaMalloc(&ctx->d_partial, sizeof(double) * (ctx->red_blocks + 16) * 16) != cudaSuccess)
+    return fail(FM_E_OOM);
+  if (cudaMalloc(&ctx->d_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMemset(ctx->d_scal, 0, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_CUDA);
+  if (cudaMallocHost(&ctx->h_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMalloc(&ctx->d_bad, sizeof(unsigned long long)) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMalloc(&ctx->d_badval, sizeof(double)) != cudaSuccess) return fail(FM_E_OOM);
+  *out = ctx;
+  return FM_OK;
+}
+
+int fm_ctx_destroy(fm_ctx* ctx) {
+  if (!ctx) return FM_OK;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  release_field(ctx->r);
+  release_field(ctx->p);
+  release_field(ctx->Ap);
+  release_field(ctx->tmp);
+  release_field(ctx->rhs);
+  release_field(ctx->dF);
+  release_field(ctx->P);
+  if (ctx->d_tw) cudaFree(ctx->d_tw);
+  if (ctx->spec) cudaFree(ctx->spec);
+  if (ctx->d_partial) cudaFree(ctx->d_partial);
+  if (ctx->d_scal) cudaFree(ctx->d_scal);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  if (ctx->d_bad) cudaFree(ctx->d_bad);
+  if (ctx->d_badval) cudaFree(ctx->d_badval);
+  for (cudaEvent_t e : ctx->prof.pending) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return FM_OK;
+}
+
+const char* fm_last_error(const fm_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int fm_last_error_info(const fm_ctx* ctx, fm_error_info* out) {
+  if (!ctx || !out) return FM_E_INVALID;
+  *out = ctx->last_info;
+  return FM_OK;
+}
+
+int64_t fm_ctx_nodes(const fm_ctx* ctx) { return ctx ? ctx->n : 0; }
+int fm_ctx_tdim(const fm_ctx* ctx) { return ctx ? ctx->tdim : 0; }
+void* fm_ctx_stream(fm_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+int64_t fm_ctx_launch_count(const fm_ctx* ctx) { return ctx ? ctx->cnt.launches : 0; }
+
+int fm_ctx_profile(fm_ctx* ctx, int enable) {
+  if (!ctx) return FM_E_INVALID;
+  if (int st = profile_collect(ctx)) return st;
+  ctx->prof.on = enable != 0;
+  for (double& v : ctx->prof.ms) v = 0.0;
+  ctx->prof.calls = 0;
+  return FM_OK;
+}
+
+int fm_ctx_profile_read(fm_ctx* ctx, double* ms, int64_t* calls) {
+  if (!ctx || !ms || !calls) return FM_E_INVALID;
+  if (int st = profile_collect(ctx)) return st;
+  for (int s = 0; s < kPasses; ++s) ms[s] = ctx->prof.ms[s];
+  *calls = ctx->prof.calls;
+  return FM_OK;
+}
+
+int fm_ctx_synchronize(fm_ctx* ctx) {
+  if (!ctx) return FM_E_INVALID;
+  FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FM_OK;
+}
+
+// ------------------------------------------------------------------ fields
+int fm_field_alloc(fm_ctx* ctx, int ncomp, fm_field** out) {
+  if (!ctx || !out || ncomp < 1 || ncomp > 81) return FM_E_INVALID;
+  fm_field* f = new (std::nothrow) fm_field;
+  if (!f) return FM_E_OOM;
+  if (int st = ensure_field(ctx, *f, ncomp)) {
+    delete f;
+    return st;
+  }
+  FM_CUDA(ctx, cudaMemsetAsync(f->d, 0, sizeof(double) * ncomp * size_t(ctx->n), ctx->stream));
+  *out = f;
+  return FM_OK;
+}
+
+int fm_field_free(fm_ctx* ctx, fm_field* f) {
+  if (!f) return FM_OK;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  release_field(*f);
+  delete f;
+  return FM_OK;
+}
+
+double* fm_field_device_ptr(fm_field* f) { return f ? f->d : nullptr; }
+
+int fm_field_upload(fm_ctx* ctx, fm_field* f, const double* host, int64_t count) {
+  if (!ctx || !f || !host || count != f->n * f->ncomp)
+    return set_error(ctx, FM_E_INVALID, "fm_field_upload: size mismatch");
+  FM_CUDA(ctx, cudaMemcpyAsync(f->d, host, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+  FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FM_OK;
+}
+
+int fm_field_download(fm_ctx* ctx, const fm_field* f, double* host, int64_t count) {
+  if (!ctx || !f || !host || count != f->n * f->ncomp)
+    return set_error(ctx, FM_E_INVALID, "fm_field_download: size mismatch");
+  FM_CUDA(ctx, cudaMemcpyAsync(host, f->d, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FM_OK;
+}
+
+int fm_field_fill(fm_ctx* ctx, fm_field* f, double value) {
+  if (!ctx || !f) return FM_E_INVALID;
+  if (value == 0.0) {
+    FM_CUDA(ctx, cudaMemsetAsync(f->d, 0, sizeof(double) * f->ncomp * size_t(f->n), ctx->stream));
+    return FM_OK;
+  }
+  std::vector<double> t(size_t(f->ncomp), value);
+  if (f->ncomp > 9) return set_error(ctx, FM_E_INVALID, "fill: ncomp > 9 supports value 0 only");
+  return fill_uniform_async(ctx, f->d, t.data(), f->ncomp, f->n);
+}
+
+int fm_field_copy(fm_ctx* ctx, const fm_field* src, fm_field* dst) {
+  if (!ctx || !src || !dst || src->ncomp != dst->ncomp) return set_error(ctx, FM_E_INVALID, "copy: shape mismatch");
+  FM_CUDA(ctx, cudaMemcpyAsync(dst->d, src->d, sizeof(double) * src->ncomp * size_t(src->n),
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+  return FM_OK;
+}
+
+// -------------------------------------------------------------- projection
+int fm_projection_apply(fm_ctx* ctx, const fm_field* A, fm_field* out) {
+  if (!ctx || !A || !out || A->ncomp != ctx->ncomp || out->ncomp != ctx->ncomp)
+    return set_error(ctx, FM_E_INVALID, "apply_projection: field does not match operator");
+  ProArgs pa;
+  pa.kind = PRO_COPY;
+  pa.A = A->d;
+  return projection_run(ctx, pa, out->d, 1.0);
+}
+
+int fm_projected_tangent_apply(fm_ctx* ctx, const fm_field* K, const fm_field* dF, fm_field* out) {
+  if (!ctx || !K || !dF || !out || K->ncomp != ctx->ncomp * ctx->ncomp || dF->ncomp != ctx->ncomp ||
+      out->ncomp != ctx->ncomp)
+    return set_error(ctx, FM_E_INVALID, "apply_projected_tangent: shape mismatch");
+  ProArgs pa;
+  pa.kind = PRO_K4;
+  pa.A = dF->d;
+  pa.K = K->d;
+  return projection_run(ctx, pa, out->d, 1.0);
+}
+
+// ------------------------------------------------------------ constitutive
+int fm_hyper_evaluate(fm_ctx* ctx, const fm_field* F, const fm_field* lambda, const fm_field* mu,
+                      fm_field* P, fm_field* K) {
+  if (!ctx || !F || !lambda || !mu || !P || F->ncomp != ctx->ncomp || P->ncomp != ctx->ncomp ||
+      lambda->ncomp != 1 || mu->ncomp != 1 || (K && K->ncomp != ctx->ncomp * ctx->ncomp))
+    return set_error(ctx, FM_E_INVALID, "hyperelastic_evaluate: parameter field size mismatch");
+  if (int st = hyper_eval_async(ctx, F->d, lambda->d, mu->d, P->d, K ? K->d : nullptr)) return st;
+  return check_bad(ctx);
+}
+
+int fm_simo_evaluate(fm_ctx* ctx, const fm_field* F, const fm_field* F_old,
+                     const fm_field* be_committed, const fm_field* epsp_committed,
+                     const fm_field* lambda, const fm_field* mu, const fm_field* tau_y0,
+                     const fm_field* hardening, fm_field* P, fm_field* K, fm_field* be_trial,
+                     fm_field* epsp_trial) {
+  if (!ctx || ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "simo_evaluate: tensors must be 3x3");
+  if (!F || !F_old || !be_committed || !epsp_committed || !lambda || !mu || !tau_y0 || !hardening ||
+      !P || !be_trial || !epsp_trial || F->ncomp != 9 || F_old->ncomp != 9 || be_committed->ncomp != 9 ||
+      epsp_committed->ncomp != 1 || P->ncomp != 9 || be_trial->ncomp != 9 || epsp_trial->ncomp != 1 ||
+      (K && K->ncomp != 81))
+    return set_error(ctx, FM_E_INVALID, "simo_evaluate: state size mismatch");
+  if (int st = simo_eval_async(ctx, F->d, F_old->d, be_committed->d, epsp_committed->d, lambda->d,
+                               mu->d, tau_y0->d, hardening->d, P->d, K ? K->d : nullptr,
+                               be_trial->d, epsp_trial->d))
+    return st;
+  return check_bad(ctx);
+}
+
+// ------------------------------------------------------------------- BLAS
+static bool same(const fm_field* a, const fm_field* b) { return a && b && a->ncomp == b->ncomp && a->n == b->n; }
+
+int fm_dot(fm_ctx* ctx, const fm_field* a, const fm_field* b, double* out) {
+  if (!ctx || !same(a, b) || !out) return set_error(ctx, FM_E_INVALID, "tensor field shape/dimension mismatch");
+  if (int st = dot_async(ctx, a->d, b->d, a->n * a->ncomp, ctx->d_scal + 8)) return st;
+  if (int st = fetch_scalars(ctx, 9)) return st;
+  *out = ctx->h_scal[8];
+  return FM_OK;
+}
+
+int fm_norm(fm_ctx* ctx, const fm_field* a, double* out) {
+  double s;
+  if (int st = fm_dot(ctx, a, a, &s)) return st;
+  *out = std::sqrt(s);
+  return FM_OK;
+}
+
+int fm_mean(fm_ctx* ctx, const fm_field* a, double* out) {
+  if (!ctx || !a || !out || a->ncomp > 9) return set_error(ctx, FM_E_INVALID, "mean: bad field");
+  if (int st = sum_comp_async(ctx, a->d, a->ncomp, a->n, ctx->d_scal + 16)) return st;
+  if (int st = fetch_scalars(ctx, 16 + a->ncomp)) return st;
+  for (int c = 0; c < a->ncomp; ++c) out[c] = ctx->h_scal[16 + c] / double(a->n);
+  return FM_OK;
+}
+
+int fm_axpy(fm_ctx* ctx, double a, const fm_field* x, fm_field* y) {
+  if (!ctx || !same(x, y)) return set_error(ctx, FM_E_INVALID, "tensor field shape/dimension mismatch");
+  return axpy_async(ctx, a, x->d, y->d, x->n * x->ncomp);
+}
+
+int fm_scale(fm_ctx* ctx, fm_field* x, double s) {
+  if (!ctx || !x) return FM_E_INVALID;
+  return scale_async(ctx, x->d, s, x->n * x->ncomp);
+}
+
+int fm_add(fm_ctx* ctx, fm_field* y, const fm_field* x, double sign) {
+  if (!ctx || !same(x, y)) return set_error(ctx, FM_E_INVALID, "tensor field shape/dimension mismatch");
+  return add_async(ctx, y->d, x->d, sign, x->n * x->ncomp);
+}
+
+int fm_add_uniform(fm_ctx* ctx, fm_field* f, const double* t) {
+  if (!ctx || !f || !t || f->ncomp > 9) return set_error(ctx, FM_E_INVALID, "add_uniform: tensor dimension mismatch");
+  return add_uniform_async(ctx, f->d, t, f->ncomp, f->n);
+}
+
+// ------------------------------------------------------------------ solver
+int fm_cg_solve(fm_ctx* ctx, const fm_field* K, const fm_field* rhs, double eta_cg, int64_t max_cg,
+                fm_field* x, int32_t* iterations, double* rel_residual) {
+  if (!ctx || !K || !rhs || !x || !iterations || !rel_residual || K->ncomp != ctx->ncomp * ctx->ncomp ||
+      rhs->ncomp != ctx->ncomp || x->ncomp != ctx->ncomp)
+    return set_error(ctx, FM_E_INVALID, "cg_solve: shape mismatch");
+  if (!(eta_cg > 0.0 && eta_cg < 1.0)) return set_error(ctx, FM_E_INVALID, "eta_cg must be in (0,1)");
+  if (max_cg < 0) return set_error(ctx, FM_E_INVALID, "max_cg must be >= 0");
+  return cg_run_k4(ctx, K->d, rhs->d, eta_cg, max_cg, x->d, iterations, rel_residual);
+}
+
+int fm_model_create_hyper(fm_ctx* ctx, const double* lambda, const double* mu, int matrix_free,
+                          fm_model** out) {
+  if (!ctx || !lambda || !mu || !out) return FM_E_INVALID;
+  fm_model* m = new (std::nothrow) fm_model;
+  if (!m) return FM_E_OOM;
+  m->kind = 0;
+  m->matrix_free = matrix_free ? 1 : 0;
+  int st = ensure_field(ctx, m->lambda, 1);
+  if (!st) st = ensure_field(ctx, m->mu, 1);
+  if (!st) st = m->matrix_free ? ensure_field(ctx, m->F_eval, ctx->ncomp)
+                               : ensure_field(ctx, m->K, ctx->ncomp * ctx->ncomp);
+  if (!st) st = fm_field_upload(ctx, &m->lambda, lambda, ctx->n);
+  if (!st) st = fm_field_upload(ctx, &m->mu, mu, ctx->n);
+  if (st) {
+    fm_model_destroy(ctx, m);
+    return st;
+  }
+  *out = m;
+  return FM_OK;
+}
+
+int fm_model_create_simo(fm_ctx* ctx, const double* lambda, const double* mu, const double* tau_y0,
+                         const double* hardening, fm_model** out) {
+  if (!ctx || !lambda || !mu || !tau_y0 || !hardening || !out) return FM_E_INVALID;
+  if (ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "Simo model needs tdim 3");
+  fm_model* m = new (std::nothrow) fm_model;
+  if (!m) return FM_E_OOM;
+  m->kind = 1;
+  int st = FM_OK;
+  fm_field* one[] = {&m->lambda, &m->mu, &m->tau_y0, &m->hard, &m->epsp_c, &m->epsp_t};
+  for (fm_field* f : one)
+    if (!st) st = ensure_field(ctx, *f, 1);
+  fm_field* nine[] = {&m->be_c, &m->be_t, &m->f_old};
+  for (fm_field* f : nine)
+    if (!st) st = ensure_field(ctx, *f, 9);
+  if (!st) st = ensure_field(ctx, m->K, 81);
+  if (!st) st = fm_field_upload(ctx, &m->lambda, lambda, ctx->n);
+  if (!st) st = fm_field_upload(ctx, &m->mu, mu, ctx->n);
+  if (!st) st = fm_field_upload(ctx, &m->tau_y0, tau_y0, ctx->n);
+  if (!st) st = fm_field_upload(ctx, &m->hard, hardening, ctx->n);
+  // HistoryState init: be = I, eps_p = 0 (material.cpp:11-12); f_old = I (simo.cpp:208)
+  const double I9[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  if (!st) st = fill_uniform_async(ctx, m->be_c.d, I9, 9, ctx->n);
+  if (!st) st = fill_uniform_async(ctx, m->be_t.d, I9, 9, ctx->n);
+  if (!st) st = fill_uniform_async(ctx, m->f_old.d, I9, 9, ctx->n);
+  if (!st) {
+    cudaMemsetAsync(m->epsp_c.d, 0, sizeof(double) * ctx->n, ctx->stream);
+    cudaMemsetAsync(m->epsp_t.d, 0, sizeof(double) * ctx->n, ctx->stream);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = FM_E_CUDA;
+  }
+  if (st) {
+    fm_model_destroy(ctx, m);
+    return st;
+  }
+  *out = m;
+  return FM_OK;
+}
+
+int fm_model_destroy(fm_ctx* ctx, fm_model* m) {
+  if (!m) return FM_OK;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  for (fm_field* f : {&m->lambda, &m->mu, &m->tau_y0, &m->hard, &m->K, &m->F_eval, &m->be_c,
+                      &m->epsp_c, &m->be_t, &m->epsp_t, &m->f_old})
+    release_field(*f);
+  delete m;
+  return FM_OK;
+}
+
+int fm_model_evaluate(fm_ctx* ctx, fm_model* m, const fm_field* F, fm_field* P) {
+  if (!ctx || !m || !F || !P || F->ncomp != ctx->ncomp || P->ncomp != ctx->ncomp)
+    return set_error(ctx, FM_E_INVALID, "evaluate: shape mismatch");
+  return model_evaluate(ctx, m, F->d, P->d);
+}
+
+int fm_model_commit(fm_ctx* ctx, fm_model* m, const fm_field* F) {
+  if (!ctx || !m || !F || F->ncomp != ctx->ncomp) return set_error(ctx, FM_E_INVALID, "commit: shape mismatch");
+  return model_commit(ctx, m, F->d);
+}
+
+fm_field* fm_model_tangent(fm_model* m) { return (m && m->K.d) ? &m->K : nullptr; }
+
+int fm_model_get_history(fm_ctx* ctx, fm_model* m, int which, double* be, double* epsp) {
+  if (!ctx || !m || m->kind != 1) return set_error(ctx, FM_E_INVALID, "history: not a Simo model");
+  const fm_field& b = which ? m->be_t : m->be_c;
+  const fm_field& e = which ? m->epsp_t : m->epsp_c;
+  if (be)
+    if (int st = fm_field_download(ctx, &b, be, 9 * ctx->n)) return st;
+  if (epsp)
+    if (int st = fm_field_download(ctx, &e, epsp, ctx->n)) return st;
+  return FM_OK;
+}
+
+int fm_model_set_history(fm_ctx* ctx, fm_model* m, const double* be, const double* epsp,
+                         const double* f_old) {
+  if (!ctx || !m || m->kind != 1) return set_error(ctx, FM_E_INVALID, "history: not a Simo model");
+  if (be)
+    if (int st = fm_field_upload(ctx, &m->be_c, be, 9 * ctx->n)) return st;
+  if (epsp)
+    if (int st = fm_field_upload(ctx, &m->epsp_c, epsp, ctx->n)) return st;
+  if (f_old)
+    if (int st = fm_field_upload(ctx, &m->f_old, f_old, 9 * ctx->n)) return st;
+  return FM_OK;
+}
+
+int fm_model_apply(fm_ctx* ctx, fm_model* m, const fm_field* dF, fm_field* out) {
+  if (!ctx || !m || !dF || !out || dF->ncomp != ctx->ncomp || out->ncomp != ctx->ncomp)
+    return set_error(ctx, FM_E_INVALID, "apply: shape mismatch");
+  return model_apply(ctx, m, dF->d, out->d);
+}
+
+int fm_solve_increment(fm_ctx* ctx, fm_model* m, fm_field* F, const double* fbar,
+                       const fm_solver_params* params, fm_report* report, fm_field* P_out) {
+  if (!ctx || !m || !F || !fbar || !params || !report) return FM_E_INVALID;
+  if (P_out && P_out->ncomp != ctx->ncomp) return set_error(ctx, FM_E_INVALID, "P_out shape mismatch");
+  return solve_increment(ctx, m, F, fbar, *params, report, P_out);
+}
+
+}  // extern "C"

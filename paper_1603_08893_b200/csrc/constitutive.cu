@@ -1,0 +1,413 @@
+// Per-voxel constitutive updates on sm_100a: St. Venant-Kirchhoff and the
+// finite-strain J2 (Simo) model.  One thread per voxel, component-major
+// coalesced loads/stores.  Errors report the LOWEST offending node via a
+// 64-bit atomicMin on (node << 4 | status), reproducing the reference's
+// first-throw-in-node-order semantics (hyperelastic.cpp:29, simo.cpp:49,77).
+#include "fm_internal.cuh"
+
+namespace fm {
+
+__device__ __forceinline__ void report_bad(unsigned long long* bad, double* badval, int64_t node,
+                                           int status, double value) {
+  const unsigned long long key = (static_cast<unsigned long long>(node) << 4) | unsigned(status);
+  const unsigned long long old = atomicMin(bad, key);
+  if (key < old && badval) *badval = value;
+}
+
+template <int TD>
+__device__ __forceinline__ double det_t(const double* a) {
+  if (TD == 2) return a[0] * a[3] - a[1] * a[2];
+  return a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+         a[2] * (a[3] * a[7] - a[4] * a[6]);
+}
+
+// Tensor2::inverse, tensor2.hpp:91-113 (3x3 branch).
+__device__ __forceinline__ bool inv3(const double* a, double* inv) {
+  const double d = det_t<3>(a);
+  if (d == 0.0) return false;
+  inv[0] = (a[4] * a[8] - a[5] * a[7]) / d;
+  inv[1] = (a[2] * a[7] - a[1] * a[8]) / d;
+  inv[2] = (a[1] * a[5] - a[2] * a[4]) / d;
+  inv[3] = (a[5] * a[6] - a[3] * a[8]) / d;
+  inv[4] = (a[0] * a[8] - a[2] * a[6]) / d;
+  inv[5] = (a[2] * a[3] - a[0] * a[5]) / d;
+  inv[6] = (a[3] * a[7] - a[4] * a[6]) / d;
+  inv[7] = (a[1] * a[6] - a[0] * a[7]) / d;
+  inv[8] = (a[0] * a[4] - a[1] * a[3]) / d;
+  return true;
+}
+
+// --------------------------------------------------------------------- SVK
+// hyperelastic_evaluate, hyperelastic.cpp:10-65.
+template <int TD>
+__global__ void __launch_bounds__(128) k_hyper(int64_t n, const double* __restrict__ F,
+                                               const double* __restrict__ lam_f,
+                                               const double* __restrict__ mu_f,
+                                               double* __restrict__ P, double* __restrict__ K,
+                                               unsigned long long* bad) {
+  constexpr int NC = TD * TD;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    double f[NC], b[NC], e[NC], s[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) f[c] = __ldg(F + c * n + q);
+    const double lam = __ldg(lam_f + q), g = __ldg(mu_f + q);
+    if (det_t<TD>(f) <= 0.0) {
+      report_bad(bad, nullptr, q, FM_E_INVERTED, 0.0);
+      continue;
+    }
+    double trE = 0.0;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double bij = 0.0, cij = 0.0;
+#pragma unroll
+        for (int k = 0; k < TD; ++k) {
+          bij += f[i * TD + k] * f[j * TD + k];
+          cij += f[k * TD + i] * f[k * TD + j];
+        }
+        b[i * TD + j] = bij;
+        e[i * TD + j] = 0.5 * (cij - (i == j ? 1.0 : 0.0));
+      }
+#pragma unroll
+    for (int i = 0; i < TD; ++i) trE += e[i * TD + i];
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) s[i * TD + j] = lam * trE * (i == j ? 1.0 : 0.0) + 2.0 * g * e[i * TD + j];
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double v = 0.0;
+#pragma unroll
+        for (int k = 0; k < TD; ++k) v += f[i * TD + k] * s[k * TD + j];
+        P[(i * TD + j) * n + q] = v;
+      }
+    if (K) {
+#pragma unroll
+      for (int i = 0; i < TD; ++i)
+#pragma unroll
+        for (int j = 0; j < TD; ++j)
+#pragma unroll
+          for (int k = 0; k < TD; ++k)
+#pragma unroll
+            for (int l = 0; l < TD; ++l) {
+              double v = lam * f[j * TD + i] * f[k * TD + l] + g * f[j * TD + l] * f[k * TD + i];
+              if (i == l) v += g * b[j * TD + k];
+              if (j == k) v += s[i * TD + l];
+              K[(((i * TD + j) * TD + k) * TD + l) * n + q] = v;
+            }
+    }
+  }
+}
+
+// -------------------------------------------------------------------- Simo
+// Symmetric 3x3 eigen-decomposition restating Eigen's
+// SelfAdjointEigenSolver<Matrix3d> (simo.cpp:74): cyclic Jacobi to
+// convergence, ascending eigenvalues, eigenvectors in the columns of V.
+__device__ void sym_eig3(const double Ain[9], double lam[3], double V[9]) {
+  double a00 = Ain[0], a01 = Ain[1], a02 = Ain[2], a11 = Ain[4], a12 = Ain[5], a22 = Ain[8];
+  double v[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    const double off = a01 * a01 + a02 * a02 + a12 * a12;
+    const double dg = a00 * a00 + a11 * a11 + a22 * a22;
+    if (off == 0.0 || off < 1e-36 * dg) break;
+#pragma unroll
+    for (int pq = 0; pq < 3; ++pq) {
+      // (p,q) = (0,1), (0,2), (1,2)
+      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+      double App = p == 0 ? a00 : a11, Aqq = q == 1 ? a11 : a22;
+      double Apq = pq == 0 ? a01 : (pq == 1 ? a02 : a12);
+      if (Apq == 0.0) continue;
+      const double theta = (Aqq - App) / (2.0 * Apq);
+      const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+      const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+      // full symmetric matrix update A <- J^T A J for the rotation in (p,q)
+      double A[3][3] = {{a00, a01, a02}, {a01, a11, a12}, {a02, a12, a22}};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double akp = A[k][p], akq = A[k][q];
+        A[k][p] = c * akp - s * akq;
+        A[k][q] = s * akp + c * akq;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double apk = A[p][k], aqk = A[q][k];
+        A[p][k] = c * apk - s * aqk;
+        A[q][k] = s * apk + c * aqk;
+      }
+      a00 = A[0][0];
+      a11 = A[1][1];
+      a22 = A[2][2];
+      a01 = A[0][1];
+      a02 = A[0][2];
+      a12 = A[1][2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double vkp = v[k * 3 + p], vkq = v[k * 3 + q];
+        v[k * 3 + p] = c * vkp - s * vkq;
+        v[k * 3 + q] = s * vkp + c * vkq;
+      }
+    }
+  }
+  double d[3] = {a00, a11, a22};
+  int o0 = 0, o1 = 1, o2 = 2, tmp;
+  if (d[o1] < d[o0]) { tmp = o0; o0 = o1; o1 = tmp; }
+  if (d[o2] < d[o1]) { tmp = o1; o1 = o2; o2 = tmp; }
+  if (d[o1] < d[o0]) { tmp = o0; o0 = o1; o1 = tmp; }
+  const int ord[3] = {o0, o1, o2};
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    lam[m] = d[ord[m]];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) V[i * 3 + m] = v[i * 3 + ord[m]];
+  }
+}
+
+// log_divided_difference, simo.cpp:18-22.
+__device__ __forceinline__ double log_dd(double a, double b) {
+  const double scale = fmax(a, b);
+  if (fabs(b - a) < 1e-7 * scale) return 2.0 / (a + b);
+  return (log(b) - log(a)) / (b - a);
+}
+
+// simo_evaluate, simo.cpp:26-196.  The algorithmic tangent is assembled in
+// the eigenbasis of be_tr, where dln(be_tr) is diagonal (w_mp) and the
+// isotropic-plus-N(x)N moduli D stay block sparse, so the reference's four
+// 81-entry temporaries (simo.cpp:41) reduce to three 3x3 coefficient sets:
+//   K_ijkl = sum_pq  a_pq U_ip V_jp V_kq U_lq + b_pq U_ip V_jq V_kp U_lq
+//                  + c_pq U_ip V_jq V_kq U_lp,          U = F^-1 V,
+// with a_pq = (lam - c1/3 + c2 N_p N_q) w_qq l_q,  b_pq = (mu + c1/2) w_pq l_q - tau_q,
+//      c_pq = (mu + c1/2) w_qp l_p,  c1 = -6 mu^2 dg/taueq,
+//      c2 = -4 mu^2 (1/(3mu+H) - dg/taueq)   (c1 = c2 = 0 on the elastic branch).
+__global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restrict__ F,
+                                              const double* __restrict__ Fold,
+                                              const double* __restrict__ be_c,
+                                              const double* __restrict__ epsp_c,
+                                              const double* __restrict__ lam_f,
+                                              const double* __restrict__ mu_f,
+                                              const double* __restrict__ ty0_f,
+                                              const double* __restrict__ h_f,
+                                              double* __restrict__ P, double* __restrict__ K,
+                                              double* __restrict__ be_t,
+                                              double* __restrict__ epsp_t,
+                                              unsigned long long* bad, double* badval) {
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const double lam = __ldg(lam_f + q), g = __ldg(mu_f + q), ty0 = __ldg(ty0_f + q),
+                 h = __ldg(h_f + q);
+    double Fm[9], Finv[9], f[9];
+    {
+      double Fo[9], Foinv[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        Fm[c] = __ldg(F + c * n + q);
+        Fo[c] = __ldg(Fold + c * n + q);
+      }
+      if (det_t<3>(Fm) <= 0.0) {
+        report_bad(bad, badval, q, FM_E_INVERTED, 0.0);
+        continue;
+      }
+      if (!inv3(Fm, Finv) || !inv3(Fo, Foinv)) {
+        report_bad(bad, badval, q, FM_E_SINGULAR, 0.0);
+        continue;
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          f[i * 3 + j] = Fm[i * 3 + 0] * Foinv[0 * 3 + j] + Fm[i * 3 + 1] * Foinv[1 * 3 + j] +
+                         Fm[i * 3 + 2] * Foinv[2 * 3 + j];
+    }
+    double bsym[9];
+    {
+      double be[9], tmp[9], bt[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) be[c] = __ldg(be_c + c * n + q);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          tmp[i * 3 + j] = f[i * 3 + 0] * be[0 * 3 + j] + f[i * 3 + 1] * be[1 * 3 + j] +
+                           f[i * 3 + 2] * be[2 * 3 + j];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          bt[i * 3 + j] = tmp[i * 3 + 0] * f[j * 3 + 0] + tmp[i * 3 + 1] * f[j * 3 + 1] +
+                          tmp[i * 3 + 2] * f[j * 3 + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) bsym[i * 3 + j] = 0.5 * (bt[i * 3 + j] + bt[j * 3 + i]);
+    }
+    double lb[3], V[9];
+    sym_eig3(bsym, lb, V);
+    if (lb[0] < 1e-30 || lb[1] < 1e-30 || lb[2] < 1e-30) {  // kMinLogEigenvalue
+      report_bad(bad, badval, q, FM_E_NOT_SPD, lb[0] < 1e-30 ? lb[0] : (lb[1] < 1e-30 ? lb[1] : lb[2]));
+      continue;
+    }
+    double eps[3], tau_d[3], dev[3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) eps[m] = 0.5 * log(lb[m]);
+    const double tr_eps = eps[0] + eps[1] + eps[2];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) tau_d[m] = lam * tr_eps + 2.0 * g * eps[m];
+    const double tau_m = (tau_d[0] + tau_d[1] + tau_d[2]) / 3.0;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) dev[m] = tau_d[m] - tau_m;
+    const double taueq_tr = sqrt(1.5 * (dev[0] * dev[0] + dev[1] * dev[1] + dev[2] * dev[2]));
+    const double ep0 = __ldg(epsp_c + q);
+    const double tauy = ty0 + h * ep0;
+    const double phi = taueq_tr - tauy;
+    const bool plastic = phi >= -1e-12 * tauy;  // simo.cpp:96
+    double dgamma = 0.0, N2[3] = {0.0, 0.0, 0.0}, eps_e[3] = {eps[0], eps[1], eps[2]};
+    if (plastic) {
+      dgamma = fmax(phi, 0.0) / (3.0 * g + h);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) N2[m] = 1.5 * dev[m] / taueq_tr;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        tau_d[m] -= 2.0 * g * dgamma * N2[m];
+        eps_e[m] = eps[m] - dgamma * N2[m];
+      }
+    }
+    // trial history (simo.cpp:110-120)
+    {
+      double ex[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) ex[m] = exp(2.0 * eps_e[m]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          be_t[(i * 3 + j) * n + q] = ex[0] * V[i * 3 + 0] * V[j * 3 + 0] +
+                                      ex[1] * V[i * 3 + 1] * V[j * 3 + 1] +
+                                      ex[2] * V[i * 3 + 2] * V[j * 3 + 2];
+      epsp_t[q] = ep0 + dgamma;
+    }
+    // P = tau F^-T, tau = V diag(tau_d) V^T  (simo.cpp:122-128)
+    {
+      double tau[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          tau[i * 3 + j] = tau_d[0] * V[i * 3 + 0] * V[j * 3 + 0] +
+                           tau_d[1] * V[i * 3 + 1] * V[j * 3 + 1] +
+                           tau_d[2] * V[i * 3 + 2] * V[j * 3 + 2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          P[(i * 3 + j) * n + q] = tau[i * 3 + 0] * Finv[j * 3 + 0] +
+                                   tau[i * 3 + 1] * Finv[j * 3 + 1] +
+                                   tau[i * 3 + 2] * Finv[j * 3 + 2];
+    }
+    if (!K) continue;
+    // eigenbasis coefficients of the algorithmic tangent (simo.cpp:131-194)
+    const double a0 = plastic ? dgamma / taueq_tr : 0.0;
+    const double c1 = plastic ? -6.0 * g * g * a0 : 0.0;
+    const double c2 = plastic ? -4.0 * g * g * (1.0 / (3.0 * g + h) - a0) : 0.0;
+    double w[9];
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) w[m * 3 + p] = log_dd(lb[m], lb[p]);
+    double ca[9], cb[9], cc[9];
+    const double lamp = lam - c1 / 3.0, mup = g + 0.5 * c1;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int qq = 0; qq < 3; ++qq) {
+        ca[p * 3 + qq] = (lamp + c2 * N2[p] * N2[qq]) * w[qq * 3 + qq] * lb[qq];
+        cb[p * 3 + qq] = mup * w[p * 3 + qq] * lb[qq] - tau_d[qq];
+        cc[p * 3 + qq] = mup * w[qq * 3 + p] * lb[p];
+      }
+    double U[9];  // U = F^-1 V
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+        U[i * 3 + p] = Finv[i * 3 + 0] * V[0 * 3 + p] + Finv[i * 3 + 1] * V[1 * 3 + p] +
+                       Finv[i * 3 + 2] * V[2 * 3 + p];
+#pragma unroll 1
+    for (int ij = 0; ij < 9; ++ij) {
+      const int i = ij / 3, j = ij % 3;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          double s = 0.0;
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            const double Uip = U[i * 3 + p];
+#pragma unroll
+            for (int qq = 0; qq < 3; ++qq) {
+              s += Uip * (ca[p * 3 + qq] * V[j * 3 + p] * V[k * 3 + qq] * U[l * 3 + qq] +
+                          cb[p * 3 + qq] * V[j * 3 + qq] * V[k * 3 + p] * U[l * 3 + qq] +
+                          cc[p * 3 + qq] * V[j * 3 + qq] * V[k * 3 + qq] * U[l * 3 + p]);
+            }
+          }
+          K[((ij * 3 + k) * 3 + l) * n + q] = s;
+        }
+    }
+  }
+}
+
+// -------------------------------------------------------------------- host
+int reset_bad(fm_ctx* ctx) {
+  FM_CUDA(ctx, cudaMemsetAsync(ctx->d_bad, 0xFF, sizeof(unsigned long long), ctx->stream));
+  return FM_OK;
+}
+
+int check_bad(fm_ctx* ctx) {
+  unsigned long long key = 0;
+  double val = 0.0;
+  FM_CUDA(ctx, cudaMemcpyAsync(&key, ctx->d_bad, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream));
+  FM_CUDA(ctx, cudaMemcpyAsync(&val, ctx->d_badval, sizeof(val), cudaMemcpyDeviceToHost, ctx->stream));
+  FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (key == ~0ull) return FM_OK;
+  const int status = int(key & 15ull);
+  const int64_t node = int64_t(key >> 4);
+  ctx->last_info = fm_error_info{status, 0, node, val};
+  const char* what = status == FM_E_INVERTED   ? "non-positive det(F) at node "
+                     : status == FM_E_NOT_SPD ? "tensor log requires a positive-definite argument (node "
+                                              : "singular tensor at node ";
+  const int st = set_error(ctx, status, std::string(what) + std::to_string(node));
+  ctx->last_info = fm_error_info{status, 0, node, val};
+  return st;
+}
+
+static int grid_for(int64_t n, int threads) {
+  const int64_t b = (n + threads - 1) / threads;
+  return int(b < 148 * 64 ? (b < 1 ? 1 : b) : 148 * 64);
+}
+
+int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const double* mu, double* P,
+                     double* K) {
+  if (int st = reset_bad(ctx)) return st;
+  const int blocks = grid_for(ctx->n, 128);
+  if (ctx->tdim == 3)
+    k_hyper<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad);
+  else
+    k_hyper<2><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const double* be_c,
+                    const double* epsp_c, const double* lam, const double* mu, const double* ty0,
+                    const double* hard, double* P, double* K, double* be_t, double* epsp_t) {
+  if (ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "simo_evaluate: tensors must be 3x3");
+  if (int st = reset_bad(ctx)) return st;
+  const int blocks = grid_for(ctx->n, 128);
+  k_simo<<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K,
+                                          be_t, epsp_t, ctx->d_bad, ctx->d_badval);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+}  // namespace fm

@@ -1,0 +1,168 @@
+// Internal declarations of the sm_100a fftmech hot path.
+// Layout in HBM:
+//   real fields   : component-major [c][x][y][z] fp64 (the reference layout),
+//   spectral work : [c][x][y][kz] complex fp64, kz in [0, nzh) -- the r2c half
+//                   spectrum along z; for even Nz in ZeroCompatible mode the
+//                   Nyquist column kz = Nz/2 is never stored (ghat = 0 there,
+//                   projection.cpp:94-98), so nzh = Nz/2 and one spectral
+//                   field is exactly as large as one real field.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/fftmech_b200.h"
+
+namespace fm {
+
+constexpr int kMaxStages = 24;
+
+// One axis of the 3-D transform: length N, radix plan, twiddle table
+// tw[k] = exp(-2 pi i k / N) (long-double accurate, device resident).
+struct AxisPlan {
+  int N = 1;
+  int nst = 0;
+  int radix[kMaxStages] = {};
+  const double2* tw = nullptr;
+};
+
+// Kinds of the fused first-pass prologue.
+enum Prologue : int {
+  PRO_COPY = 0,  // G(A): read A
+  PRO_K4 = 1,    // G(K : dF^T): dP_ij = K_jikl dF_kl (projection.cpp:182-192)
+  PRO_SVK = 2,   // matrix-free SVK tangent action from F, lambda, mu
+};
+
+struct Counters {
+  int64_t launches = 0;
+};
+
+// Optional per-pass CUDA-event timing of the projection (bench roofline).
+constexpr int kPasses = 5;
+struct PassProfile {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<cudaEvent_t> pending;  // groups of kPasses + 1 events
+  double ms[kPasses] = {};
+  int64_t calls = 0;
+};
+
+}  // namespace fm
+
+struct fm_field {
+  int ncomp = 0;
+  int64_t n = 0;
+  double* d = nullptr;
+};
+
+struct fm_model {
+  int kind = 0;  // 0 hyperelastic, 1 Simo
+  int matrix_free = 0;
+  fm_field lambda, mu, tau_y0, hard;
+  fm_field K;                   // tangent (81n or 16n); empty when matrix-free
+  fm_field F_eval;              // F at the last evaluate (matrix-free SVK action)
+  fm_field be_c, epsp_c, be_t, epsp_t, f_old;  // Simo history
+};
+
+struct fm_ctx {
+  int dim = 3;
+  int pts[3] = {1, 1, 1};
+  double len[3] = {1, 1, 1};
+  int tdim = 3, ncomp = 9;
+  int64_t n = 0;
+  int mode = 0;
+  int Nx = 1, Ny = 1, Nz = 1;
+  int nzh = 1;  // stored kz columns
+  int Lz = 1;   // complex FFT length along z (Nz/2 for even Nz, Nz otherwise)
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  fm::AxisPlan px, py, pz, pzh;  // pzh: half-length plan for even-Nz r2c
+  double2* d_tw = nullptr;        // all twiddle tables
+  double2* spec = nullptr;        // ncomp * Nx * Ny * nzh
+  // reductions
+  int red_blocks = 0;
+  double* d_partial = nullptr;  // red_blocks * 16
+  double* d_scal = nullptr;     // device scalars (64)
+  double* h_scal = nullptr;     // pinned mirror (64)
+  unsigned long long* d_bad = nullptr;  // lowest offending node (atomicMin)
+  double* d_badval = nullptr;
+  // CG workspace (allocated lazily, tdim^2 components each)
+  fm_field r, p, Ap, tmp, rhs, dF, P;
+  fm::Counters cnt;
+  fm::PassProfile prof;
+  std::string last_error;
+  fm_error_info last_info{};
+};
+
+namespace fm {
+
+// Launch/error helpers ------------------------------------------------------
+int set_error(fm_ctx* ctx, int status, const std::string& msg);
+int check_cuda(fm_ctx* ctx, cudaError_t e, const char* what);
+#define FM_CUDA(ctx, call)                                      \
+  do {                                                          \
+    cudaError_t e_ = (call);                                    \
+    if (e_ != cudaSuccess) return ::fm::check_cuda(ctx, e_, #call); \
+  } while (0)
+#define FM_LAUNCHED(ctx)                                                         \
+  do {                                                                           \
+    (ctx)->cnt.launches++;                                                       \
+    cudaError_t e_ = cudaGetLastError();                                         \
+    if (e_ != cudaSuccess) return ::fm::check_cuda(ctx, e_, "kernel launch");    \
+  } while (0)
+
+int ensure_field(fm_ctx* ctx, fm_field& f, int ncomp);
+void release_field(fm_field& f);
+
+// projection.cu -------------------------------------------------------------
+struct ProArgs {
+  int kind = PRO_COPY;
+  const double* A = nullptr;   // PRO_COPY input / PRO_K4, PRO_SVK: dF
+  const double* K = nullptr;   // PRO_K4
+  const double* F = nullptr;   // PRO_SVK
+  const double* lam = nullptr; // PRO_SVK
+  const double* mu = nullptr;  // PRO_SVK
+};
+// out = scale * n * G(prologue(args)); scale = 1 gives the reference G.
+int projection_run(fm_ctx* ctx, const ProArgs& args, double* out, double scale);
+int profile_collect(fm_ctx* ctx);
+
+// blas.cu -------------------------------------------------------------------
+int dot_async(fm_ctx* ctx, const double* a, const double* b, int64_t count, double* d_out);
+int sum_comp_async(fm_ctx* ctx, const double* a, int ncomp, int64_t n, double* d_out);
+int axpy_async(fm_ctx* ctx, double a, const double* x, double* y, int64_t count);
+int scale_async(fm_ctx* ctx, double* x, double s, int64_t count);
+int add_async(fm_ctx* ctx, double* y, const double* x, double sign, int64_t count);
+int add_uniform_async(fm_ctx* ctx, double* f, const double* t, int ncomp, int64_t n);
+int fill_uniform_async(fm_ctx* ctx, double* f, const double* t, int ncomp, int64_t n);
+int fetch_scalars(fm_ctx* ctx, int count);  // d_scal[0:count] -> h_scal, synchronises
+// CG helpers operating on device scalars (see solver.cu)
+int cg_update_async(fm_ctx* ctx, double* x, double* r, const double* p, const double* Ap,
+                    int64_t count);
+int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count);
+int cg_pap_async(fm_ctx* ctx, const double* p, const double* Ap, int64_t count);
+
+// constitutive.cu -----------------------------------------------------------
+int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const double* mu, double* P,
+                     double* K);
+int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const double* be_c,
+                    const double* epsp_c, const double* lam, const double* mu,
+                    const double* ty0, const double* hard, double* P, double* K, double* be_t,
+                    double* epsp_t);
+int reset_bad(fm_ctx* ctx);
+
+// solver.cu -----------------------------------------------------------------
+int cg_run_k4(fm_ctx* ctx, const double* K, const double* b, double eta_cg, int64_t max_cg,
+              double* x, int32_t* iters, double* rel);
+int model_evaluate(fm_ctx* ctx, fm_model* m, const double* F, double* P);
+int model_commit(fm_ctx* ctx, fm_model* m, const double* F);
+int model_apply(fm_ctx* ctx, fm_model* m, const double* dF, double* out);
+int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* F, const double* fbar,
+                    const fm_solver_params& prm, fm_report* rep, fm_field* P_out);
+// Reads the lowest offending node/status; returns FM_OK or the error status.
+int check_bad(fm_ctx* ctx);
+
+}  // namespace fm

@@ -1,0 +1,438 @@
+// Compatibility projection G and the projected tangent G(K : dF^T) on sm_100a.
+//
+// Restates apply_projection / apply_projected_tangent
+// (reference proj/core/src/projection.cpp:123-194) as five HBM passes over
+// the r2c half spectrum, with the reference's stored ĝ table
+// (projection.cpp:87-104, 72 B/voxel) replaced by an analytic evaluation
+// from the wave vector inside the x pass:
+//   pass 1  z  : prologue (copy | K:dF^T | SVK action) + real-to-complex FFT
+//   pass 2  y  : forward complex FFT
+//   pass 3  x  : forward FFT, Bhat_i. = (Ahat_i . xi) xi / |xi|^2, inverse FFT
+//   pass 4  y  : inverse complex FFT
+//   pass 5  z  : complex-to-real inverse FFT, scale 1/n
+// ghat(-q) = ghat(q) and the Nyquist set is symmetric, so the half spectrum
+// is exact; the discarded imaginary part of the reference's
+// c2c round trip (projection.cpp:157-169) is identically zero here.
+#include <algorithm>
+
+#include "fft_smem.cuh"
+
+namespace fm {
+
+struct Geo {
+  int Nx, Ny, Nz, nzh, Lz, dim, mode;
+  int64_t n;
+  double invL[3];
+};
+
+__device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) ? i : i - n; }
+
+// ------------------------------------------------------------------ pass 1
+template <int TD, int PRO>
+__device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int64_t node,
+                                               double v[TD * TD]) {
+  constexpr int NC = TD * TD;
+  if (PRO == PRO_COPY) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = __ldg(pa.A + c * n + node);
+  } else if (PRO == PRO_K4) {
+    // dP_ij = K_jikl dF_kl (projection.cpp:184)
+    double df[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) df[c] = __ldg(pa.A + c * n + node);
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int kl = 0; kl < NC; ++kl) s += __ldg(pa.K + ((j * TD + i) * NC + kl) * n + node) * df[kl];
+        v[i * TD + j] = s;
+      }
+  } else {
+    // SVK tangent action (hyperelastic.cpp:55-63 contracted analytically):
+    // dP = lam tr(F^T dF) F + mu F dF^T F + mu F F^T dF + dF S
+    double f[NC], d[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      f[c] = __ldg(pa.F + c * n + node);
+      d[c] = __ldg(pa.A + c * n + node);
+    }
+    const double lam = __ldg(pa.lam + node), mu = __ldg(pa.mu + node);
+    double trFd = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) trFd += f[c] * d[c];
+    double e[NC], s[NC], fdt[NC], ffd[NC];
+    double trE = 0.0;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double cij = 0.0, a = 0.0;
+#pragma unroll
+        for (int k = 0; k < TD; ++k) {
+          cij += f[k * TD + i] * f[k * TD + j];
+          a += f[i * TD + k] * d[j * TD + k];  // (F dF^T)_ij
+        }
+        e[i * TD + j] = 0.5 * (cij - (i == j ? 1.0 : 0.0));
+        fdt[i * TD + j] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < TD; ++i) trE += e[i * TD + i];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) s[c] = 2.0 * mu * e[c];
+#pragma unroll
+    for (int i = 0; i < TD; ++i) s[i * TD + i] += lam * trE;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double a = 0.0;  // (F^T dF)_ij
+#pragma unroll
+        for (int k = 0; k < TD; ++k) a += f[k * TD + i] * d[k * TD + j];
+        ffd[i * TD + j] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double a = lam * trFd * f[i * TD + j];
+#pragma unroll
+        for (int k = 0; k < TD; ++k) {
+          a += mu * fdt[i * TD + k] * f[k * TD + j];  // F dF^T F
+          a += mu * f[i * TD + k] * ffd[k * TD + j];  // F (F^T dF)
+          a += d[i * TD + k] * s[k * TD + j];         // dF S
+        }
+        v[i * TD + j] = a;
+      }
+  }
+}
+
+template <int TD, int PRO>
+__global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double2* __restrict__ twN,
+                                              ProArgs pa, double2* __restrict__ spec, int G, int ls) {
+  extern __shared__ double2 sm[];
+  constexpr int NC = TD * TD;
+  const int nxy = g.Nx * g.Ny;
+  const int L0 = blockIdx.x * G;
+  const int Gb = min(G, nxy - L0);
+  double2* A = sm;
+  double2* B = sm + NC * G * ls;
+  const bool even = (g.Nz % 2 == 0);
+  for (int w = threadIdx.x; w < Gb * g.Nz; w += blockDim.x) {
+    const int gi = w / g.Nz, z = w - gi * g.Nz;
+    const int64_t node = int64_t(L0 + gi) * g.Nz + z;
+    double v[NC];
+    prologue_voxel<TD, PRO>(pa, g.n, node, v);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double2* line = A + (c * G + gi) * ls;
+      if (even)
+        reinterpret_cast<double*>(line)[z] = v[c];
+      else
+        line[z] = make_double2(v[c], 0.0);
+    }
+  }
+  __syncthreads();
+  double2* R = fft_smem(A, B, NC * G, ls, 1, plan, -1, false);
+  const int M = g.Lz;
+  for (int w = threadIdx.x; w < NC * Gb * g.nzh; w += blockDim.x) {
+    const int line = w / g.nzh, k = w - line * g.nzh;
+    const int c = line / Gb, gi = line - c * Gb;
+    const double2* Z = R + (c * G + gi) * ls;
+    double2 X;
+    if (even) {
+      // X[k] = E[k] + W_N^k O[k], E = (Z[k] + Z*[M-k])/2, O = -i (Z[k] - Z*[M-k])/2
+      const double2 a = Z[k % M];
+      const double2 b = cconj(Z[(M - k) % M]);
+      const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+      const double2 D = csub(a, b);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      X = cadd(E, cmul(O, __ldg(&twN[k])));
+    } else {
+      X = Z[k];
+    }
+    spec[(int64_t(c) * nxy + L0 + gi) * g.nzh + k] = X;
+  }
+}
+
+// -------------------------------------------------------------- pass 2 / 4
+__global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, double2* __restrict__ spec,
+                                               int TW, int sign) {
+  extern __shared__ double2 sm[];
+  const int kz0 = blockIdx.x * TW;
+  const int x = blockIdx.y, c = blockIdx.z;
+  const int Ny = g.Ny;
+  double2* A = sm;
+  double2* B = sm + Ny * TW;
+  double2* base = spec + (int64_t(c) * g.Nx + x) * Ny * g.nzh;
+  for (int w = threadIdx.x; w < Ny * TW; w += blockDim.x) {
+    const int e = w / TW, t = w - e * TW;
+    const int kz = kz0 + t;
+    A[w] = kz < g.nzh ? base[int64_t(e) * g.nzh + kz] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2* R = fft_smem(A, B, TW, 1, TW, plan, sign, true);
+  for (int w = threadIdx.x; w < Ny * TW; w += blockDim.x) {
+    const int e = w / TW, t = w - e * TW;
+    const int kz = kz0 + t;
+    if (kz < g.nzh) base[int64_t(e) * g.nzh + kz] = R[w];
+  }
+}
+
+// ------------------------------------------------------------------ pass 3
+template <int TD>
+__global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __restrict__ spec,
+                                               int TW) {
+  extern __shared__ double2 sm[];
+  const int kz0 = blockIdx.x * TW;
+  const int y = blockIdx.y, i = blockIdx.z;
+  const int Nx = g.Nx;
+  const int nl = TD * TW;
+  double2* A = sm;
+  double2* B = sm + Nx * nl;
+  const int64_t xstride = int64_t(g.Ny) * g.nzh;
+  for (int w = threadIdx.x; w < Nx * nl; w += blockDim.x) {
+    const int t = w % TW, j = (w / TW) % TD, e = w / nl;
+    const int kz = kz0 + t;
+    A[w] = kz < g.nzh
+               ? spec[(int64_t(i * TD + j) * Nx + e) * xstride + int64_t(y) * g.nzh + kz]
+               : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2* R = fft_smem(A, B, nl, 1, nl, plan, -1, true);
+  double2* S = (R == A) ? B : A;
+  // Bhat_ij = sum_l Ahat_il ghat_lj, ghat = xi (x) xi / |xi|^2 (projection.cpp:87-104,139-152)
+  const int qy = freq_of(y, g.Ny);
+  const bool ny_y = (g.Ny % 2 == 0) && (y == g.Ny / 2);
+  for (int w = threadIdx.x; w < Nx * TW; w += blockDim.x) {
+    const int e = w / TW, t = w - e * TW;
+    const int kz = kz0 + t;
+    if (kz >= g.nzh) continue;
+    const int qx = freq_of(e, Nx), qz = freq_of(kz, g.Nz);
+    const bool nyq = ny_y || ((Nx % 2 == 0) && (e == Nx / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+    double xi[3] = {qx * g.invL[0], qy * g.invL[1], g.dim == 3 ? qz * g.invL[2] : 0.0};
+    const double norm2 = xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2];
+    double2* v = R + e * nl + t;
+    if (norm2 == 0.0 || (nyq && g.mode == FM_NYQUIST_ZERO_COMPATIBLE)) {
+#pragma unroll
+      for (int j = 0; j < TD; ++j) v[j * TW] = make_double2(0.0, 0.0);
+    } else if (!nyq) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int l = 0; l < TD; ++l) {
+        if (l < g.dim) {
+          const double2 a = v[l * TW];
+          s.x += a.x * xi[l];
+          s.y += a.y * xi[l];
+        }
+      }
+      const double inv = 1.0 / norm2;
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        const double f = j < g.dim ? xi[j] * inv : 0.0;
+        v[j * TW] = make_double2(s.x * f, s.y * f);
+      }
+    }  // Nyquist in IdentityEquilibrium mode: ghat = I, keep v
+  }
+  __syncthreads();
+  R = fft_smem(R, S, nl, 1, nl, plan, +1, true);
+  for (int w = threadIdx.x; w < Nx * nl; w += blockDim.x) {
+    const int t = w % TW, j = (w / TW) % TD, e = w / nl;
+    const int kz = kz0 + t;
+    if (kz < g.nzh)
+      spec[(int64_t(i * TD + j) * Nx + e) * xstride + int64_t(y) * g.nzh + kz] = R[w];
+  }
+}
+
+// ------------------------------------------------------------------ pass 5
+template <int TD>
+__global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double2* __restrict__ twN,
+                                              const double2* __restrict__ spec,
+                                              double* __restrict__ out, int G, int ls,
+                                              double scale) {
+  extern __shared__ double2 sm[];
+  constexpr int NC = TD * TD;
+  const int nxy = g.Nx * g.Ny;
+  const int L0 = blockIdx.x * G;
+  const int Gb = min(G, nxy - L0);
+  double2* A = sm;
+  double2* B = sm + NC * G * ls;
+  const bool even = (g.Nz % 2 == 0);
+  for (int w = threadIdx.x; w < NC * Gb * g.nzh; w += blockDim.x) {
+    const int line = w / g.nzh, k = w - line * g.nzh;
+    const int c = line / Gb, gi = line - c * Gb;
+    A[(c * G + gi) * ls + k] = spec[(int64_t(c) * nxy + L0 + gi) * g.nzh + k];
+  }
+  __syncthreads();
+  const int M = g.Lz;
+  for (int w = threadIdx.x; w < NC * Gb * M; w += blockDim.x) {
+    const int line = w / M, k = w - line * M;
+    const int c = line / Gb, gi = line - c * Gb;
+    const double2* X = A + (c * G + gi) * ls;
+    double2 Z;
+    if (even) {
+      // Z[k] = (X[k] + X*[M-k]) + i W_N^{-k} (X[k] - X*[M-k]); X[M] = 0 when not stored
+      const double2 a = X[k];
+      const double2 b = (M - k < g.nzh) ? cconj(X[M - k]) : make_double2(0.0, 0.0);
+      const double2 t = cmulc(csub(a, b), __ldg(&twN[k]));
+      Z = make_double2(a.x + b.x - t.y, a.y + b.y + t.x);
+    } else {
+      Z = k < g.nzh ? X[k] : cconj(X[g.Nz - k]);
+    }
+    B[(c * G + gi) * ls + k] = Z;
+  }
+  __syncthreads();
+  double2* R = fft_smem(B, A, NC * G, ls, 1, plan, +1, false);
+  for (int w = threadIdx.x; w < NC * Gb * g.Nz; w += blockDim.x) {
+    const int line = w / g.Nz, z = w - line * g.Nz;
+    const int c = line / Gb, gi = line - c * Gb;
+    const double2* Zl = R + (c * G + gi) * ls;
+    double v;
+    if (even) {
+      const double2 zz = Zl[z >> 1];
+      v = (z & 1) ? zz.y : zz.x;
+    } else {
+      v = Zl[z].x;
+    }
+    out[int64_t(c) * g.n + int64_t(L0 + gi) * g.Nz + z] = v * scale;
+  }
+}
+
+// ------------------------------------------------------------------- host
+namespace {
+constexpr int kMaxSmem = 227 * 1024;
+
+template <typename K>
+void allow_smem(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+}
+
+Geo make_geo(const fm_ctx* ctx) {
+  Geo g;
+  g.Nx = ctx->Nx;
+  g.Ny = ctx->Ny;
+  g.Nz = ctx->Nz;
+  g.nzh = ctx->nzh;
+  g.Lz = ctx->Lz;
+  g.dim = ctx->dim;
+  g.mode = ctx->mode;
+  g.n = ctx->n;
+  for (int a = 0; a < 3; ++a) g.invL[a] = 1.0 / ctx->len[a];
+  return g;
+}
+
+int tile_width(int nzh, int N, int lines_per_col, int& TW) {
+  TW = std::min(8, nzh);
+  while (TW > 1 && size_t(2) * N * TW * lines_per_col * 16 > size_t(kMaxSmem)) TW /= 2;
+  return size_t(2) * N * TW * lines_per_col * 16 <= size_t(kMaxSmem) ? 0 : -1;
+}
+
+cudaEvent_t prof_event(fm_ctx* ctx) {
+  cudaEvent_t e;
+  if (!ctx->prof.pool.empty()) {
+    e = ctx->prof.pool.back();
+    ctx->prof.pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  return e;
+}
+
+void prof_mark(fm_ctx* ctx) {
+  if (!ctx->prof.on) return;
+  cudaEvent_t e = prof_event(ctx);
+  cudaEventRecord(e, ctx->stream);
+  ctx->prof.pending.push_back(e);
+}
+
+template <int TD>
+int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale) {
+  constexpr int NC = TD * TD;
+  static bool init = false;
+  if (!init) {
+    allow_smem(k_zfwd<TD, PRO_COPY>);
+    allow_smem(k_zfwd<TD, PRO_K4>);
+    allow_smem(k_zfwd<TD, PRO_SVK>);
+    allow_smem(k_ypass);
+    allow_smem(k_xpass<TD>);
+    allow_smem(k_zinv<TD>);
+    init = true;
+  }
+  const Geo g = make_geo(ctx);
+  const int nxy = ctx->Nx * ctx->Ny;
+  const bool even = ctx->Nz % 2 == 0;
+  const AxisPlan& pzp = even ? ctx->pzh : ctx->pz;
+  int ls = std::max(ctx->Lz, ctx->nzh);
+  if (ls % 2 == 0) ls += 1;  // odd pitch: fewer bank conflicts
+  int G = int(std::max<size_t>(1, std::min<size_t>(16, size_t(96 * 1024) / (size_t(2) * NC * ls * 16))));
+  G = std::min(G, nxy);
+  const size_t smz = size_t(2) * NC * G * ls * 16;
+  if (smz > size_t(kMaxSmem))
+    return set_error(ctx, FM_E_UNSUPPORTED, "z line too long for the shared-memory FFT");
+  const dim3 gz((nxy + G - 1) / G);
+  prof_mark(ctx);
+  switch (pa.kind) {
+    case PRO_COPY:
+      k_zfwd<TD, PRO_COPY><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+      break;
+    case PRO_K4:
+      k_zfwd<TD, PRO_K4><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+      break;
+    default:
+      k_zfwd<TD, PRO_SVK><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+      break;
+  }
+  FM_LAUNCHED(ctx);
+  prof_mark(ctx);
+  int TWy, TWx;
+  if (tile_width(ctx->nzh, ctx->Ny, 1, TWy) || tile_width(ctx->nzh, ctx->Nx, TD, TWx))
+    return set_error(ctx, FM_E_UNSUPPORTED, "x/y line too long for the shared-memory FFT");
+  if (ctx->Ny > 1) {
+    const dim3 gy((ctx->nzh + TWy - 1) / TWy, ctx->Nx, NC);
+    k_ypass<<<gy, 256, size_t(2) * ctx->Ny * TWy * 16, ctx->stream>>>(g, ctx->py, ctx->spec, TWy, -1);
+    FM_LAUNCHED(ctx);
+  }
+  prof_mark(ctx);
+  {
+    const dim3 gx((ctx->nzh + TWx - 1) / TWx, ctx->Ny, TD);
+    k_xpass<TD><<<gx, 256, size_t(2) * ctx->Nx * TD * TWx * 16, ctx->stream>>>(g, ctx->px, ctx->spec, TWx);
+    FM_LAUNCHED(ctx);
+  }
+  prof_mark(ctx);
+  if (ctx->Ny > 1) {
+    const dim3 gy((ctx->nzh + TWy - 1) / TWy, ctx->Nx, NC);
+    k_ypass<<<gy, 256, size_t(2) * ctx->Ny * TWy * 16, ctx->stream>>>(g, ctx->py, ctx->spec, TWy, +1);
+    FM_LAUNCHED(ctx);
+  }
+  prof_mark(ctx);
+  k_zinv<TD><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, ctx->spec, out, G, ls,
+                                            scale / double(ctx->n));
+  FM_LAUNCHED(ctx);
+  prof_mark(ctx);
+  if (ctx->prof.on) ctx->prof.calls++;
+  return FM_OK;
+}
+}  // namespace
+
+int profile_collect(fm_ctx* ctx) {
+  auto& pr = ctx->prof;
+  FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (size_t g0 = 0; g0 + kPasses < pr.pending.size() + 0; g0 += kPasses + 1) {
+    for (int s = 0; s < kPasses; ++s) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pr.pending[g0 + s], pr.pending[g0 + s + 1]);
+      pr.ms[s] += ms;
+    }
+  }
+  for (cudaEvent_t e : pr.pending) pr.pool.push_back(e);
+  pr.pending.clear();
+  return FM_OK;
+}
+
+int projection_run(fm_ctx* ctx, const ProArgs& pa, double* out, double scale) {
+  if (ctx->tdim == 3) return run_td<3>(ctx, pa, out, scale);
+  return run_td<2>(ctx, pa, out, scale);
+}
+
+}  // namespace fm

@@ -1,0 +1,262 @@
+// Device-resident CG and Newton drivers (host C++ control flow over the
+// sm_100a kernels).  Control flow restates solver.cpp:19-160 statement by
+// statement; all vectors stay in HBM, and only the 2-3 scalars the
+// reference branches on cross to the host (one pinned read per CG step).
+#include <chrono>
+#include <cmath>
+
+#include "fm_internal.cuh"
+
+namespace fm {
+
+enum Slot { S_RR = 0, S_PAP = 1, S_RRNEW = 2, S_ALPHA = 3, S_BETA = 4, S_FLAG = 5, S_OUT = 8 };
+
+struct Op {
+  int kind = PRO_K4;
+  const double* K = nullptr;
+  const double* F = nullptr;
+  const double* lam = nullptr;
+  const double* mu = nullptr;
+};
+
+int op_apply(fm_ctx* ctx, const Op& op, const double* x, double* out, double scale) {
+  ProArgs pa;
+  pa.kind = op.kind;
+  pa.A = x;
+  pa.K = op.K;
+  pa.F = op.F;
+  pa.lam = op.lam;
+  pa.mu = op.mu;
+  return projection_run(ctx, pa, out, scale);
+}
+
+Op model_op(fm_model* m) {
+  Op op;
+  if (m->kind == 0 && m->matrix_free) {
+    op.kind = PRO_SVK;
+    op.F = m->F_eval.d;
+    op.lam = m->lambda.d;
+    op.mu = m->mu.d;
+  } else {
+    op.kind = PRO_K4;
+    op.K = m->K.d;
+  }
+  return op;
+}
+
+int norm_sync(fm_ctx* ctx, const double* a, int64_t count, double* out) {
+  if (int st = dot_async(ctx, a, a, count, ctx->d_scal + S_OUT)) return st;
+  if (int st = fetch_scalars(ctx, S_OUT + 1)) return st;
+  *out = std::sqrt(ctx->h_scal[S_OUT]);
+  return FM_OK;
+}
+
+int mean_sync(fm_ctx* ctx, const double* a, double* mean) {
+  if (int st = sum_comp_async(ctx, a, ctx->ncomp, ctx->n, ctx->d_scal + 16)) return st;
+  if (int st = fetch_scalars(ctx, 16 + ctx->ncomp)) return st;
+  for (int c = 0; c < ctx->ncomp; ++c) mean[c] = ctx->h_scal[16 + c] / double(ctx->n);
+  return FM_OK;
+}
+
+// cg_solve, solver.cpp:19-58.
+int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t max_cg, double* x,
+           int32_t* iters, double* rel) {
+  const int64_t count = ctx->n * ctx->ncomp;
+  if (int st = ensure_field(ctx, ctx->r, ctx->ncomp)) return st;
+  if (int st = ensure_field(ctx, ctx->p, ctx->ncomp)) return st;
+  if (int st = ensure_field(ctx, ctx->Ap, ctx->ncomp)) return st;
+  FM_CUDA(ctx, cudaMemsetAsync(x, 0, sizeof(double) * count, ctx->stream));  // :22
+  // bnorm = |b|; rr = <r,r> with r = b  (:24, :31-33)
+  if (int st = dot_async(ctx, b, b, count, ctx->d_scal + S_RR)) return st;
+  if (int st = fetch_scalars(ctx, S_RR + 1)) return st;
+  const double bnorm = std::sqrt(ctx->h_scal[S_RR]);
+  if (bnorm == 0.0) {  // :25
+    *iters = 0;
+    *rel = 0.0;
+    return FM_OK;
+  }
+  const int64_t cap = max_cg > 0 ? max_cg : count;  // :27-29 (int64: no overflow past 620^3)
+  FM_CUDA(ctx, cudaMemcpyAsync(ctx->r.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
+  FM_CUDA(ctx, cudaMemcpyAsync(ctx->p.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
+  double rr = ctx->h_scal[S_RR];
+  for (int64_t it = 1; it <= cap; ++it) {
+    if (int st = op_apply(ctx, op, ctx->p.d, ctx->Ap.d, 1.0)) return st;     // :36
+    if (int st = cg_pap_async(ctx, ctx->p.d, ctx->Ap.d, count)) return st;   // :37
+    if (int st = cg_update_async(ctx, x, ctx->r.d, ctx->p.d, ctx->Ap.d, count)) return st;  // :46-48
+    if (int st = fetch_scalars(ctx, S_FLAG + 1)) return st;
+    if (ctx->h_scal[S_FLAG] != 0.0) {  // !(pAp > 0): return without updating x (:38-44)
+      *iters = int32_t(it);
+      *rel = std::sqrt(rr) / bnorm;
+      return FM_OK;
+    }
+    const double rr_new = ctx->h_scal[S_RRNEW];
+    if (std::sqrt(rr_new) <= eta_cg * bnorm) {  // :49-50
+      *iters = int32_t(it);
+      *rel = std::sqrt(rr_new) / bnorm;
+      return FM_OK;
+    }
+    rr = rr_new;
+    if (int st = cg_direction_async(ctx, ctx->p.d, ctx->r.d, count)) return st;  // :51-55
+  }
+  *iters = int32_t(cap);
+  *rel = std::sqrt(rr) / bnorm;
+  const int st = set_error(ctx, FM_E_CG_STALLED,
+                           "conjugate gradient stalled after " + std::to_string(cap) + " iterations");
+  ctx->last_info = fm_error_info{FM_E_CG_STALLED, int32_t(cap), -1, *rel};
+  return st;
+}
+
+int model_evaluate(fm_ctx* ctx, fm_model* m, const double* F, double* P) {
+  int st;
+  if (m->kind == 0) {
+    st = hyper_eval_async(ctx, F, m->lambda.d, m->mu.d, P, m->matrix_free ? nullptr : m->K.d);
+    if (!st && m->matrix_free)
+      FM_CUDA(ctx, cudaMemcpyAsync(m->F_eval.d, F, sizeof(double) * ctx->n * ctx->ncomp,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    st = simo_eval_async(ctx, F, m->f_old.d, m->be_c.d, m->epsp_c.d, m->lambda.d, m->mu.d,
+                         m->tau_y0.d, m->hard.d, P, m->K.d, m->be_t.d, m->epsp_t.d);
+  }
+  if (st) return st;
+  return check_bad(ctx);
+}
+
+int model_apply(fm_ctx* ctx, fm_model* m, const double* dF, double* out) {
+  return op_apply(ctx, model_op(m), dF, out, 1.0);
+}
+
+int cg_run_k4(fm_ctx* ctx, const double* K, const double* b, double eta_cg, int64_t max_cg,
+              double* x, int32_t* iters, double* rel) {
+  Op op;
+  op.kind = PRO_K4;
+  op.K = K;
+  return cg_run(ctx, op, b, eta_cg, max_cg, x, iters, rel);
+}
+
+int model_commit(fm_ctx* ctx, fm_model* m, const double* F) {
+  if (m->kind != 1) return FM_OK;
+  const size_t n = size_t(ctx->n);
+  FM_CUDA(ctx, cudaMemcpyAsync(m->be_c.d, m->be_t.d, 9 * n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  FM_CUDA(ctx, cudaMemcpyAsync(m->epsp_c.d, m->epsp_t.d, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  FM_CUDA(ctx, cudaMemcpyAsync(m->f_old.d, F, 9 * n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  return FM_OK;
+}
+
+static double det_host(const double* a, int d) {
+  if (d == 2) return a[0] * a[3] - a[1] * a[2];
+  return a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+         a[2] * (a[3] * a[7] - a[4] * a[6]);
+}
+
+// solve_increment, solver.cpp:73-160.
+int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
+                    const fm_solver_params& prm, fm_report* rep, fm_field* P_out) {
+  if (!(prm.eta_newton > 0.0 && prm.eta_newton < 1.0))
+    return set_error(ctx, FM_E_INVALID, "eta_newton must be in (0,1)");
+  if (!(prm.eta_cg > 0.0 && prm.eta_cg < 1.0)) return set_error(ctx, FM_E_INVALID, "eta_cg must be in (0,1)");
+  if (prm.max_newton < 1 || prm.max_newton > FM_MAX_PASSES)
+    return set_error(ctx, FM_E_INVALID, "max_newton must be in [1, 64]");
+  if (prm.max_cg < 0) return set_error(ctx, FM_E_INVALID, "max_cg must be >= 0");
+  const int d = ctx->tdim, nc = ctx->ncomp;
+  if (Ff->ncomp != nc) return set_error(ctx, FM_E_INVALID, "increment dimension does not match the state field");
+  if (!(det_host(fbar, d) > 0.0)) return set_error(ctx, FM_E_INVALID, "det(Fbar) must be positive");
+  *rep = fm_report{};
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t count = ctx->n * nc;
+  double* F = Ff->d;
+  if (int st = ensure_field(ctx, ctx->P, nc)) return st;
+  if (int st = ensure_field(ctx, ctx->dF, nc)) return st;
+  if (int st = ensure_field(ctx, ctx->rhs, nc)) return st;
+  if (int st = ensure_field(ctx, ctx->tmp, nc)) return st;
+  double* P = ctx->P.d;
+  const auto finish = [&](bool conv) {
+    rep->converged = conv ? 1 : 0;
+    rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  double norm_ref;
+  if (int st = norm_sync(ctx, F, count, &norm_ref)) return st;  // :88
+  const Op op = model_op(m);
+  const auto drift = [&](double* out) -> int {
+    double mean[9];
+    if (int st = mean_sync(ctx, F, mean)) return st;
+    double dr = 0.0;
+    for (int c = 0; c < nc; ++c) dr = std::max(dr, std::abs(mean[c] - fbar[c]));
+    *out = dr;
+    return FM_OK;
+  };
+  // ---- boundary-condition pass (:101-122)
+  {
+    if (int st = model_evaluate(ctx, m, F, P)) return st;
+    double mean[9], dfbar[9];
+    if (int st = mean_sync(ctx, F, mean)) return st;
+    for (int c = 0; c < nc; ++c) dfbar[c] = fbar[c] - mean[c];
+    if (int st = fill_uniform_async(ctx, ctx->tmp.d, dfbar, nc, ctx->n)) return st;
+    if (int st = op_apply(ctx, op, ctx->tmp.d, ctx->rhs.d, -1.0)) return st;  // rhs = -G(K:dFbar^T)
+    rep->matvecs++;
+    int32_t it = 0;
+    double rel = 0.0;
+    if (int st = cg_run(ctx, op, ctx->rhs.d, prm.eta_cg, prm.max_cg, ctx->dF.d, &it, &rel)) {
+      finish(false);
+      return st;
+    }
+    rep->matvecs += it;
+    if (int st = add_uniform_async(ctx, F, dfbar, nc, ctx->n)) return st;
+    if (int st = add_async(ctx, F, ctx->dF.d, +1.0, count)) return st;
+    double ndf;
+    if (int st = norm_sync(ctx, ctx->dF.d, count, &ndf)) return st;
+    rep->cg_iterations[0] = it;
+    rep->cg_rel_residual[0] = rel;
+    rep->rel_update[0] = ndf / norm_ref;
+    rep->n_passes = 1;
+    double dr;
+    if (int st = drift(&dr)) return st;
+    rep->max_mean_drift = std::max(rep->max_mean_drift, dr);
+  }
+  // ---- Newton equilibrium passes (:125-147)
+  while (true) {
+    if (rep->n_passes >= prm.max_newton) {
+      finish(false);
+      return set_error(ctx, FM_E_NEWTON_DIVERGED,
+                       "Newton did not converge within " + std::to_string(rep->n_passes) + " passes");
+    }
+    if (int st = model_evaluate(ctx, m, F, P)) return st;
+    if (int st = op_apply(ctx, Op{PRO_COPY}, P, ctx->rhs.d, -1.0)) return st;  // rhs = -G(P)
+    int32_t it = 0;
+    double rel = 0.0;
+    if (int st = cg_run(ctx, op, ctx->rhs.d, prm.eta_cg, prm.max_cg, ctx->dF.d, &it, &rel)) {
+      finish(false);
+      return st;
+    }
+    rep->matvecs += it;
+    if (int st = add_async(ctx, F, ctx->dF.d, +1.0, count)) return st;
+    double ndf;
+    if (int st = norm_sync(ctx, ctx->dF.d, count, &ndf)) return st;
+    const double ru = ndf / norm_ref;
+    const int k = rep->n_passes++;
+    rep->cg_iterations[k] = it;
+    rep->cg_rel_residual[k] = rel;
+    rep->rel_update[k] = ru;
+    double dr;
+    if (int st = drift(&dr)) return st;
+    rep->max_mean_drift = std::max(rep->max_mean_drift, dr);
+    if (ru < prm.eta_newton) break;
+  }
+  // ---- refresh at the converged state, residual, commit (:151-155)
+  if (int st = model_evaluate(ctx, m, F, P)) return st;
+  double pnorm;
+  if (int st = norm_sync(ctx, P, count, &pnorm)) return st;
+  if (pnorm > 0.0) {
+    if (int st = op_apply(ctx, Op{PRO_COPY}, P, ctx->tmp.d, 1.0)) return st;
+    double gn;
+    if (int st = norm_sync(ctx, ctx->tmp.d, count, &gn)) return st;
+    rep->equilibrium_rel_residual = gn / pnorm;
+  }
+  if (int st = model_commit(ctx, m, F)) return st;
+  if (P_out)
+    FM_CUDA(ctx, cudaMemcpyAsync(P_out->d, P, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
+  FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  finish(true);
+  return FM_OK;
+}
+
+}  // namespace fm

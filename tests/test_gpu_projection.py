@@ -1,0 +1,152 @@
+"""GPU parity of the projection G and the projected tangent G(K : dF^T)
+against the CPU oracle (restating projection.cpp:123-194), plus the
+reference's own property assertions (test_projection.cpp:96-244) on the GPU."""
+import numpy as np
+import pytest
+
+from paper_1603_08893_b200 import abi
+from paper_1603_08893_b200 import microstructure as M
+
+pytestmark = pytest.mark.gpu
+
+# (points, lengths, tdim, nyquist mode) -- odd, even, prime, anisotropic,
+# 2-d and plane-strain shapes, both Nyquist modes (test_projection.cpp:109-115)
+CASES = [
+    ((5, 5, 5), None, 3, 0),
+    ((5, 3, 7), (1.0, 2.0, 0.5), 3, 0),
+    ((4, 4, 4), None, 3, 0),
+    ((4, 4, 4), None, 3, 1),
+    ((4, 5, 3), (1.0, 0.7, 1.3), 3, 1),
+    ((6, 5), None, 2, 0),
+    ((5, 7), None, 3, 0),
+    ((4, 5), None, 2, 1),
+    ((31, 31, 31), None, 3, 0),
+    ((32, 32, 32), None, 3, 0),
+    ((12, 10, 14), None, 3, 1),
+    ((16, 9, 24), None, 3, 0),
+    ((64, 64, 64), None, 3, 0),
+    ((1, 1, 1), None, 3, 0),
+    ((2, 2, 2), None, 3, 0),
+    ((3, 1, 2), None, 3, 0),
+]
+
+
+def _ids(c):
+    return "x".join(map(str, c[0])) + f"-t{c[2]}-m{c[3]}"
+
+
+@pytest.mark.parametrize("case", CASES, ids=[_ids(c) for c in CASES])
+def test_projection_matches_oracle(case, oracle):
+    pts, lengths, tdim, mode = case
+    nc = tdim * tdim
+    A = M.uniform_field(pts, nc, seed=11 + len(pts))
+    ref, st, _ = oracle.apply_projection(pts, tdim, A, mode=mode, lengths=lengths)
+    assert st == 0
+    with abi.Context(pts, tdim, lengths=lengths, nyquist_mode=mode) as ctx:
+        got = ctx.projection(ctx.field(nc, A)).download()
+    scale = max(np.linalg.norm(ref), 1e-300)
+    assert np.linalg.norm(got - ref) <= 1e-12 * max(scale, 1.0)
+
+
+@pytest.mark.parametrize("case", CASES[:12], ids=[_ids(c) for c in CASES[:12]])
+def test_projected_tangent_matches_oracle(case, oracle):
+    pts, lengths, tdim, mode = case
+    nc = tdim * tdim
+    n = int(np.prod(pts))
+    rng = np.random.default_rng(5)
+    K = rng.uniform(-1, 1, nc * nc * n)
+    dF = rng.uniform(-1, 1, nc * n)
+    ref, st = oracle.apply_projected_tangent(pts, tdim, K, dF, mode=mode, lengths=lengths)
+    assert st == 0
+    with abi.Context(pts, tdim, lengths=lengths, nyquist_mode=mode) as ctx:
+        got = ctx.projected_tangent(ctx.field(nc * nc, K), ctx.field(nc, dF)).download()
+    assert np.linalg.norm(got - ref) <= 1e-12 * max(np.linalg.norm(ref), 1.0)
+
+
+@pytest.mark.parametrize("pts", [(5, 5, 5), (5, 3, 7), (4, 4, 4), (32, 32, 32), (128, 128, 128)])
+def test_idempotent_zero_mean_self_adjoint(pts):
+    # test_projection.cpp:107-136 with the same 1e-10 / 1e-12 tolerances
+    A = M.uniform_field(pts, 9, seed=1)
+    B = M.uniform_field(pts, 9, seed=2)
+    with abi.Context(pts, 3) as ctx:
+        fa, fb = ctx.field(9, A), ctx.field(9, B)
+        GA = ctx.projection(fa)
+        GGA = ctx.projection(GA)
+        GB = ctx.projection(fb)
+        ga, gga = GA.download(), GGA.download()
+        assert np.linalg.norm(gga - ga) < 1e-10 * max(1.0, np.linalg.norm(ga))
+        assert np.all(np.abs(ctx.mean(GA)) < 1e-12)
+        lhs, rhs = ctx.dot(fa, GB), ctx.dot(GA, fb)
+        assert abs(lhs - rhs) <= 1e-10 * abs(rhs)
+
+
+def test_constant_field_projects_to_zero():
+    # test_projection.cpp:96-105
+    pts = (5, 5, 5)
+    n = 125
+    A = np.zeros(9 * n)
+    A[1 * n:2 * n] = 2.0
+    A[8 * n:9 * n] = -0.7
+    with abi.Context(pts, 3) as ctx:
+        out = ctx.projection(ctx.field(9, A)).download()
+    assert np.linalg.norm(out) < 1e-12 * np.linalg.norm(A)
+
+
+def test_fourier_mode_known_answer():
+    """Analytic projection of a single Fourier mode (SURVEY.md §8(d) config 4
+    known-answer test): A_ij = a_ij cos(2 pi q.x) -> (a xi) (x) xi / |xi|^2 cos."""
+    N = 16
+    pts = (N, N, N)
+    q = np.array([1, 2, 3])
+    x = np.stack(np.meshgrid(*[np.arange(N)] * 3, indexing="ij"), axis=-1).reshape(-1, 3) / N
+    phase = np.cos(2 * np.pi * x @ q)
+    a = np.arange(1.0, 10.0).reshape(3, 3)
+    expect_t = (a @ q)[:, None] * q[None, :] / (q @ q)
+    A = np.concatenate([a.reshape(-1)[c] * phase for c in range(9)])
+    E = np.concatenate([expect_t.reshape(-1)[c] * phase for c in range(9)])
+    with abi.Context(pts, 3) as ctx:
+        got = ctx.projection(ctx.field(9, A)).download()
+    assert np.max(np.abs(got - E)) < 1e-12
+
+
+def test_plane_strain_stays_in_plane():
+    # test_projection.cpp:138-148
+    pts = (5, 7)
+    n = 35
+    A = M.uniform_field(pts, 9, seed=9)
+    with abi.Context(pts, 3) as ctx:
+        GA = ctx.projection(ctx.field(9, A)).download().reshape(3, 3, n)
+    assert np.max(np.abs(GA[:, 2, :])) < 1e-12
+
+
+def test_linearity_of_projected_tangent():
+    # test_projection.cpp:201-228
+    pts = (3, 3)
+    tdim = 2
+    n = 9
+    lam, mu = 0.58, 0.38
+    C = np.zeros((2, 2, 2, 2))
+    for i in range(2):
+        for j in range(2):
+            for k in range(2):
+                for l in range(2):
+                    C[i, j, k, l] = lam * (i == j) * (k == l) + mu * ((i == l) * (j == k) + (i == k) * (j == l))
+    K = np.repeat(C.reshape(-1, 1), n, axis=1).reshape(-1)
+    rng = np.random.default_rng(55)
+    x, y = rng.uniform(-1, 1, 4 * n), rng.uniform(-1, 1, 4 * n)
+    with abi.Context(pts, tdim) as ctx:
+        fk = ctx.field(16, K)
+        lhs = ctx.projected_tangent(fk, ctx.field(4, 1.7 * x - 0.3 * y)).download()
+        rx = ctx.projected_tangent(fk, ctx.field(4, x)).download()
+        ry = ctx.projected_tangent(fk, ctx.field(4, y)).download()
+    rhs = 1.7 * rx - 0.3 * ry
+    assert np.linalg.norm(lhs - rhs) < 1e-12 * max(1.0, np.linalg.norm(rhs))
+
+
+def test_shape_mismatch_is_invalid():
+    with abi.Context((4, 4, 4), 3) as ctx:
+        a = ctx.field(9)
+        bad = ctx.field(4)
+        with pytest.raises(abi.FmError) as e:
+            ctx.projection(bad, a)
+        assert e.value.status == 1
