@@ -1,0 +1,119 @@
+// Shared pieces of the projection passes (generic and register-resident).
+#pragma once
+
+#include "fft_reg.cuh"
+
+namespace fm {
+
+struct Geo {
+  int Nx, Ny, Nz, nzh, Lz, dim, mode;
+  int64_t n;
+  double invL[3];
+};
+
+__device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) ? i : i - n; }
+
+// ------------------------------------------------------------------ pass 1
+template <int TD, int PRO>
+__device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int64_t node,
+                                               double v[TD * TD]) {
+  constexpr int NC = TD * TD;
+  if (PRO == PRO_COPY) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[c] = __ldg(pa.A + c * n + node);
+  } else if (PRO == PRO_K4) {
+    // dP_ij = K_jikl dF_kl (projection.cpp:184)
+    double df[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) df[c] = __ldg(pa.A + c * n + node);
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int kl = 0; kl < NC; ++kl) s += __ldg(pa.K + ((j * TD + i) * NC + kl) * n + node) * df[kl];
+        v[i * TD + j] = s;
+      }
+  } else {
+    // SVK tangent action (hyperelastic.cpp:55-63 contracted analytically):
+    // dP = lam tr(F^T dF) F + mu F dF^T F + mu F F^T dF + dF S
+    double f[NC], d[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      f[c] = __ldg(pa.F + c * n + node);
+      d[c] = __ldg(pa.A + c * n + node);
+    }
+    const double lam = __ldg(pa.lam + node), mu = __ldg(pa.mu + node);
+    double trFd = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) trFd += f[c] * d[c];
+    double e[NC], s[NC], fdt[NC], ffd[NC];
+    double trE = 0.0;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double cij = 0.0, a = 0.0;
+#pragma unroll
+        for (int k = 0; k < TD; ++k) {
+          cij += f[k * TD + i] * f[k * TD + j];
+          a += f[i * TD + k] * d[j * TD + k];  // (F dF^T)_ij
+        }
+        e[i * TD + j] = 0.5 * (cij - (i == j ? 1.0 : 0.0));
+        fdt[i * TD + j] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < TD; ++i) trE += e[i * TD + i];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) s[c] = 2.0 * mu * e[c];
+#pragma unroll
+    for (int i = 0; i < TD; ++i) s[i * TD + i] += lam * trE;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double a = 0.0;  // (F^T dF)_ij
+#pragma unroll
+        for (int k = 0; k < TD; ++k) a += f[k * TD + i] * d[k * TD + j];
+        ffd[i * TD + j] = a;
+      }
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double a = lam * trFd * f[i * TD + j];
+#pragma unroll
+        for (int k = 0; k < TD; ++k) {
+          a += mu * fdt[i * TD + k] * f[k * TD + j];  // F dF^T F
+          a += mu * f[i * TD + k] * ffd[k * TD + j];  // F (F^T dF)
+          a += d[i * TD + k] * s[k * TD + j];         // dF S
+        }
+        v[i * TD + j] = a;
+      }
+  }
+}
+
+inline Geo make_geo(const fm_ctx* ctx) {
+  Geo g;
+  g.Nx = ctx->Nx;
+  g.Ny = ctx->Ny;
+  g.Nz = ctx->Nz;
+  g.nzh = ctx->nzh;
+  g.Lz = ctx->Lz;
+  g.dim = ctx->dim;
+  g.mode = ctx->mode;
+  g.n = ctx->n;
+  for (int a = 0; a < 3; ++a) g.invL[a] = 1.0 / ctx->len[a];
+  return g;
+}
+
+
+// Pass launchers of the register-resident path (projection_fast.cu); each
+// returns true when it launched (false: no fast kernel for this shape).
+bool zf_fast(fm_ctx* ctx, const ProArgs& pa, int* st);
+bool y_fast(fm_ctx* ctx, int sign, int* st);
+bool x_fast(fm_ctx* ctx, int* st);
+bool zi_fast(fm_ctx* ctx, double* out, double scale, int* st);
+
+}  // namespace fm

@@ -15,98 +15,9 @@
 // c2c round trip (projection.cpp:157-169) is identically zero here.
 #include <algorithm>
 
-#include "fft_smem.cuh"
+#include "proj_common.cuh"
 
 namespace fm {
-
-struct Geo {
-  int Nx, Ny, Nz, nzh, Lz, dim, mode;
-  int64_t n;
-  double invL[3];
-};
-
-__device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) ? i : i - n; }
-
-// ------------------------------------------------------------------ pass 1
-template <int TD, int PRO>
-__device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int64_t node,
-                                               double v[TD * TD]) {
-  constexpr int NC = TD * TD;
-  if (PRO == PRO_COPY) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c) v[c] = __ldg(pa.A + c * n + node);
-  } else if (PRO == PRO_K4) {
-    // dP_ij = K_jikl dF_kl (projection.cpp:184)
-    double df[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) df[c] = __ldg(pa.A + c * n + node);
-#pragma unroll
-    for (int i = 0; i < TD; ++i)
-#pragma unroll
-      for (int j = 0; j < TD; ++j) {
-        double s = 0.0;
-#pragma unroll
-        for (int kl = 0; kl < NC; ++kl) s += __ldg(pa.K + ((j * TD + i) * NC + kl) * n + node) * df[kl];
-        v[i * TD + j] = s;
-      }
-  } else {
-    // SVK tangent action (hyperelastic.cpp:55-63 contracted analytically):
-    // dP = lam tr(F^T dF) F + mu F dF^T F + mu F F^T dF + dF S
-    double f[NC], d[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      f[c] = __ldg(pa.F + c * n + node);
-      d[c] = __ldg(pa.A + c * n + node);
-    }
-    const double lam = __ldg(pa.lam + node), mu = __ldg(pa.mu + node);
-    double trFd = 0.0;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) trFd += f[c] * d[c];
-    double e[NC], s[NC], fdt[NC], ffd[NC];
-    double trE = 0.0;
-#pragma unroll
-    for (int i = 0; i < TD; ++i)
-#pragma unroll
-      for (int j = 0; j < TD; ++j) {
-        double cij = 0.0, a = 0.0;
-#pragma unroll
-        for (int k = 0; k < TD; ++k) {
-          cij += f[k * TD + i] * f[k * TD + j];
-          a += f[i * TD + k] * d[j * TD + k];  // (F dF^T)_ij
-        }
-        e[i * TD + j] = 0.5 * (cij - (i == j ? 1.0 : 0.0));
-        fdt[i * TD + j] = a;
-      }
-#pragma unroll
-    for (int i = 0; i < TD; ++i) trE += e[i * TD + i];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) s[c] = 2.0 * mu * e[c];
-#pragma unroll
-    for (int i = 0; i < TD; ++i) s[i * TD + i] += lam * trE;
-#pragma unroll
-    for (int i = 0; i < TD; ++i)
-#pragma unroll
-      for (int j = 0; j < TD; ++j) {
-        double a = 0.0;  // (F^T dF)_ij
-#pragma unroll
-        for (int k = 0; k < TD; ++k) a += f[k * TD + i] * d[k * TD + j];
-        ffd[i * TD + j] = a;
-      }
-#pragma unroll
-    for (int i = 0; i < TD; ++i)
-#pragma unroll
-      for (int j = 0; j < TD; ++j) {
-        double a = lam * trFd * f[i * TD + j];
-#pragma unroll
-        for (int k = 0; k < TD; ++k) {
-          a += mu * fdt[i * TD + k] * f[k * TD + j];  // F dF^T F
-          a += mu * f[i * TD + k] * ffd[k * TD + j];  // F (F^T dF)
-          a += d[i * TD + k] * s[k * TD + j];         // dF S
-        }
-        v[i * TD + j] = a;
-      }
-  }
-}
 
 template <int TD, int PRO>
 __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double2* __restrict__ twN,
@@ -308,20 +219,6 @@ void allow_smem(K kernel) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
 }
 
-Geo make_geo(const fm_ctx* ctx) {
-  Geo g;
-  g.Nx = ctx->Nx;
-  g.Ny = ctx->Ny;
-  g.Nz = ctx->Nz;
-  g.nzh = ctx->nzh;
-  g.Lz = ctx->Lz;
-  g.dim = ctx->dim;
-  g.mode = ctx->mode;
-  g.n = ctx->n;
-  for (int a = 0; a < 3; ++a) g.invL[a] = 1.0 / ctx->len[a];
-  return g;
-}
-
 int tile_width(int nzh, int N, int lines_per_col, int& TW) {
   TW = std::min(8, nzh);
   while (TW > 1 && size_t(2) * N * TW * lines_per_col * 16 > size_t(kMaxSmem)) TW /= 2;
@@ -371,44 +268,64 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale) {
   if (smz > size_t(kMaxSmem))
     return set_error(ctx, FM_E_UNSUPPORTED, "z line too long for the shared-memory FFT");
   const dim3 gz((nxy + G - 1) / G);
-  prof_mark(ctx);
-  switch (pa.kind) {
-    case PRO_COPY:
-      k_zfwd<TD, PRO_COPY><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-      break;
-    case PRO_K4:
-      k_zfwd<TD, PRO_K4><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-      break;
-    default:
-      k_zfwd<TD, PRO_SVK><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-      break;
-  }
-  FM_LAUNCHED(ctx);
-  prof_mark(ctx);
   int TWy, TWx;
   if (tile_width(ctx->nzh, ctx->Ny, 1, TWy) || tile_width(ctx->nzh, ctx->Nx, TD, TWx))
     return set_error(ctx, FM_E_UNSUPPORTED, "x/y line too long for the shared-memory FFT");
-  if (ctx->Ny > 1) {
+  int st = FM_OK;
+  // pass 1: z forward (+ prologue)
+  prof_mark(ctx);
+  if (!(TD == 3 && zf_fast(ctx, pa, &st))) {
+    switch (pa.kind) {
+      case PRO_COPY:
+        k_zfwd<TD, PRO_COPY><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+        break;
+      case PRO_K4:
+        k_zfwd<TD, PRO_K4><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+        break;
+      default:
+        k_zfwd<TD, PRO_SVK><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+        break;
+    }
+    FM_LAUNCHED(ctx);
+  } else if (st) {
+    return st;
+  }
+  // pass 2: y forward
+  prof_mark(ctx);
+  if (ctx->Ny > 1 && !(TD == 3 && y_fast(ctx, -1, &st))) {
     const dim3 gy((ctx->nzh + TWy - 1) / TWy, ctx->Nx, NC);
     k_ypass<<<gy, 256, size_t(2) * ctx->Ny * TWy * 16, ctx->stream>>>(g, ctx->py, ctx->spec, TWy, -1);
     FM_LAUNCHED(ctx);
+  } else if (st) {
+    return st;
   }
+  // pass 3: x forward, ghat, x inverse
   prof_mark(ctx);
-  {
+  if (!(TD == 3 && x_fast(ctx, &st))) {
     const dim3 gx((ctx->nzh + TWx - 1) / TWx, ctx->Ny, TD);
     k_xpass<TD><<<gx, 256, size_t(2) * ctx->Nx * TD * TWx * 16, ctx->stream>>>(g, ctx->px, ctx->spec, TWx);
     FM_LAUNCHED(ctx);
+  } else if (st) {
+    return st;
   }
+  // pass 4: y inverse
   prof_mark(ctx);
-  if (ctx->Ny > 1) {
+  if (ctx->Ny > 1 && !(TD == 3 && y_fast(ctx, +1, &st))) {
     const dim3 gy((ctx->nzh + TWy - 1) / TWy, ctx->Nx, NC);
     k_ypass<<<gy, 256, size_t(2) * ctx->Ny * TWy * 16, ctx->stream>>>(g, ctx->py, ctx->spec, TWy, +1);
     FM_LAUNCHED(ctx);
+  } else if (st) {
+    return st;
   }
+  // pass 5: z inverse (c2r), scale
   prof_mark(ctx);
-  k_zinv<TD><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, ctx->spec, out, G, ls,
-                                            scale / double(ctx->n));
-  FM_LAUNCHED(ctx);
+  if (!(TD == 3 && zi_fast(ctx, out, scale / double(ctx->n), &st))) {
+    k_zinv<TD><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, ctx->spec, out, G, ls,
+                                              scale / double(ctx->n));
+    FM_LAUNCHED(ctx);
+  } else if (st) {
+    return st;
+  }
   prof_mark(ctx);
   if (ctx->prof.on) ctx->prof.calls++;
   return FM_OK;

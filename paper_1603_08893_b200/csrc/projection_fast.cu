@@ -1,0 +1,366 @@
+// Register-resident projection passes for power-of-two line lengths
+// (fft_reg.cuh).  Same five-pass structure, spectral layout and arithmetic
+// contract as the generic passes in projection.cu (reference
+// projection.cpp:123-194); these are the kernels the 128^3..1024^3 configs run.
+//
+// Per pass and voxel the HBM traffic is one 9-component read and one write
+// (pass 1 additionally reads K4); everything else stays on chip:
+//   z passes : G z-lines x 9 components staged in shared memory (prologue /
+//              epilogue one thread per voxel, coalesced), M = Nz/2-point
+//              complex FFT with lines interleaved, r2c/c2r untangling in smem.
+//   y pass   : TW = 8 consecutive kz columns per CTA, loads straight into
+//              registers (8 lanes x 16 B = one 128-byte segment).
+//   x pass   : one thread holds all 3 components of its row, so the
+//              projection Bhat_i. = (Ahat_i . xi) xi / |xi|^2 is applied in
+//              registers between the forward and inverse x transforms.
+#include "proj_common.cuh"
+
+namespace fm {
+
+using reg::e_line;
+using reg::e_x;
+
+// ------------------------------------------------------------------ y pass
+template <int N, int TW, int SIGN>
+__global__ void __launch_bounds__(TW*(N / e_line(N))) k_y_fast(Geo g, const double2* __restrict__ tw,
+                                                               double2* __restrict__ spec) {
+  constexpr int E = e_line(N), T = N / E;
+  extern __shared__ double2 sm[];
+  const int l = threadIdx.x % TW, t = threadIdx.x / TW;
+  const int kz = blockIdx.x * TW + l;
+  double2* base = spec + (int64_t(blockIdx.z) * g.Nx + blockIdx.y) * int64_t(N) * g.nzh + kz;
+  double2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = base[int64_t(t + T * m) * g.nzh];
+  reg::fft<N, E, SIGN>(v, sm + l, TW, t, tw);
+#pragma unroll
+  for (int m = 0; m < E; ++m) base[int64_t(t + T * m) * g.nzh] = v[m];
+}
+
+// ------------------------------------------------------------------ x pass
+template <int N, int TW, int TD>
+__global__ void __launch_bounds__(TW*(N / e_x(N))) k_x_fast(Geo g, const double2* __restrict__ tw,
+                                                            double2* __restrict__ spec) {
+  constexpr int E = e_x(N), T = N / E;
+  extern __shared__ double2 sm[];
+  const int l = threadIdx.x % TW, t = threadIdx.x / TW;
+  const int kz = blockIdx.x * TW + l;
+  const int y = blockIdx.y, i = blockIdx.z;
+  const int64_t xstride = int64_t(g.Ny) * g.nzh;
+  double2* base = spec + int64_t(i * TD) * N * xstride + int64_t(y) * g.nzh + kz;
+  double2 v[TD][E];
+#pragma unroll
+  for (int j = 0; j < TD; ++j)
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[j][m] = base[(int64_t(j) * N + t + T * m) * xstride];
+#pragma unroll
+  for (int j = 0; j < TD; ++j) reg::fft<N, E, -1>(v[j], sm + l, TW, t, tw);
+  // Bhat_ij = sum_l Ahat_il ghat_lj  (projection.cpp:87-104, 139-152)
+  const int qy = freq_of(y, g.Ny), qz = freq_of(kz, g.Nz);
+  const bool nyq_yz = ((g.Ny % 2 == 0) && (y == g.Ny / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+  const double xiy = qy * g.invL[1], xiz = (g.dim == 3) ? qz * g.invL[2] : 0.0;
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int kx = t + T * m;
+    const double xix = freq_of(kx, N) * g.invL[0];
+    const double xi[3] = {xix, xiy, xiz};
+    const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
+    const bool nyq = nyq_yz || (kx == N / 2);
+    if (norm2 == 0.0 || (nyq && g.mode == FM_NYQUIST_ZERO_COMPATIBLE)) {
+#pragma unroll
+      for (int j = 0; j < TD; ++j) v[j][m] = make_double2(0.0, 0.0);
+    } else if (!nyq) {
+      double sx = 0.0, sy = 0.0;
+#pragma unroll
+      for (int q = 0; q < TD; ++q)
+        if (q < g.dim) {
+          sx += v[q][m].x * xi[q];
+          sy += v[q][m].y * xi[q];
+        }
+      const double inv = 1.0 / norm2;
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        const double f = j < g.dim ? xi[j] * inv : 0.0;
+        v[j][m] = make_double2(sx * f, sy * f);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < TD; ++j) reg::fft<N, E, +1>(v[j], sm + l, TW, t, tw);
+#pragma unroll
+  for (int j = 0; j < TD; ++j)
+#pragma unroll
+    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[j][m];
+}
+
+// --------------------------------------------------------------- z passes
+template <int M>
+struct ZShape {
+  static constexpr int E = e_line(M);
+  static constexpr int T = M / E;
+  static constexpr int G = T >= 32 ? 1 : 32 / T;  // z-lines per CTA
+  static constexpr int LSL = 9 * G;                // smem lines (9 components x G)
+  static constexpr int LSP = LSL | 1;              // odd pitch: conflict-free strided access
+  static constexpr int THREADS = LSL * T;
+  static constexpr size_t SMEM = size_t(M) * LSP * 16;
+};
+
+template <int M, int PRO>
+__global__ void __launch_bounds__(ZShape<M>::THREADS) k_zf_fast(Geo g, const double2* __restrict__ twM,
+                                                                const double2* __restrict__ twN,
+                                                                ProArgs pa, double2* __restrict__ spec) {
+  using S = ZShape<M>;
+  constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
+  extern __shared__ double2 sm[];
+  double* smd = reinterpret_cast<double*>(sm);
+  const int nxy = g.Nx * g.Ny;
+  const int L0 = blockIdx.x * G;
+  const int Gb = min(G, nxy - L0);
+  // phase 1: prologue, one thread per voxel; z -> packed complex m = z/2
+  for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
+    const int gi = w / N, z = w - gi * N;
+    const int64_t node = int64_t(L0 + gi) * N + z;
+    double v[9];
+    prologue_voxel<3, PRO>(pa, g.n, node, v);
+#pragma unroll
+    for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] = v[c];
+  }
+  __syncthreads();
+  // phase 2: M-point complex FFT of every line, lines fastest across lanes
+  {
+    const int l = threadIdx.x % S::LSL, t = threadIdx.x / S::LSL;
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = sm[(t + T * m) * LSP + l];
+    __syncthreads();
+    reg::fft<M, E, -1>(v, sm + l, LSP, t, twM);
+#pragma unroll
+    for (int m = 0; m < E; ++m) sm[(t + T * m) * LSP + l] = v[m];
+  }
+  __syncthreads();
+  // phase 3: untangle X[k] = E[k] + W_N^k O[k] and store k < M (kz = M dropped)
+  for (int w = threadIdx.x; w < 9 * Gb * M; w += blockDim.x) {
+    const int c = w / (Gb * M), rem = w - c * (Gb * M);
+    const int gi = rem / M, k = rem - gi * M;
+    const int l = c * G + gi;
+    const double2 a = sm[k * LSP + l];
+    const double2 b = cconj(sm[((M - k) & (M - 1)) * LSP + l]);
+    const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+    const double2 D = csub(a, b);
+    const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+    spec[(int64_t(c) * nxy + L0 + gi) * M + k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const double2* __restrict__ twM,
+                                                                const double2* __restrict__ twN,
+                                                                const double2* __restrict__ spec,
+                                                                double* __restrict__ out, double scale) {
+  using S = ZShape<M>;
+  constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
+  extern __shared__ double2 sm[];
+  double* smd = reinterpret_cast<double*>(sm);
+  const int nxy = g.Nx * g.Ny;
+  const int L0 = blockIdx.x * G;
+  const int Gb = min(G, nxy - L0);
+  for (int w = threadIdx.x; w < 9 * Gb * M; w += blockDim.x) {
+    const int c = w / (Gb * M), rem = w - c * (Gb * M);
+    const int gi = rem / M, k = rem - gi * M;
+    sm[k * LSP + c * G + gi] = spec[(int64_t(c) * nxy + L0 + gi) * M + k];
+  }
+  __syncthreads();
+  // Z[k] = (X[k] + X*[M-k]) + i W_N^-k (X[k] - X*[M-k]), X[M] = 0 (ZeroCompatible)
+  constexpr int H = M / 2 + 1;
+  for (int w = threadIdx.x; w < 9 * Gb * H; w += blockDim.x) {
+    const int c = w / (Gb * H), rem = w - c * (Gb * H);
+    const int gi = rem / H, k = rem - gi * H;
+    const int l = c * G + gi;
+    const double2 xk = sm[k * LSP + l];
+    const double2 xm = k == 0 ? make_double2(0.0, 0.0) : sm[(M - k) * LSP + l];
+    {
+      const double2 b = cconj(xm);
+      const double2 t = cmulc(csub(xk, b), __ldg(&twN[k]));
+      sm[k * LSP + l] = make_double2(xk.x + b.x - t.y, xk.y + b.y + t.x);
+    }
+    if (k > 0 && k < M - k) {
+      const double2 b = cconj(xk);
+      const double2 t = cmulc(csub(xm, b), __ldg(&twN[M - k]));
+      sm[(M - k) * LSP + l] = make_double2(xm.x + b.x - t.y, xm.y + b.y + t.x);
+    }
+  }
+  __syncthreads();
+  {
+    const int l = threadIdx.x % S::LSL, t = threadIdx.x / S::LSL;
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = sm[(t + T * m) * LSP + l];
+    __syncthreads();
+    reg::fft<M, E, +1>(v, sm + l, LSP, t, twM);
+#pragma unroll
+    for (int m = 0; m < E; ++m) sm[(t + T * m) * LSP + l] = v[m];
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
+    const int gi = w / N, z = w - gi * N;
+    const int64_t node = int64_t(L0 + gi) * N + z;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) out[c * g.n + node] = smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] * scale;
+  }
+}
+
+// ------------------------------------------------------------------- host
+namespace {
+
+
+template <typename K>
+void allow(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+int tw_of(int N) { return N >= 1024 ? 4 : 8; }
+constexpr int tw_x(int N) { return N >= 1024 ? 2 : (N >= 512 ? 4 : 8); }
+
+template <int N>
+bool y_launch(fm_ctx* ctx, int sign, int* st) {
+  constexpr int TW = N >= 1024 ? 4 : 8;
+  constexpr int T = N / e_line(N);
+  const size_t smem = size_t(N) * TW * 16;
+  const Geo g = make_geo(ctx);
+  const dim3 grid(ctx->nzh / TW, ctx->Nx, ctx->ncomp);
+  if (sign < 0) {
+    static bool a = (allow(k_y_fast<N, TW, -1>, smem), true);
+    (void)a;
+    k_y_fast<N, TW, -1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, ctx->spec);
+  } else {
+    static bool a = (allow(k_y_fast<N, TW, +1>, smem), true);
+    (void)a;
+    k_y_fast<N, TW, +1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, ctx->spec);
+  }
+  ctx->cnt.launches++;
+  const cudaError_t e = cudaGetLastError();
+  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_y_fast");
+  return true;
+}
+
+template <int N>
+bool x_launch(fm_ctx* ctx, int* st) {
+  constexpr int TW = tw_x(N);
+  constexpr int T = N / e_x(N);
+  const size_t smem = size_t(N) * TW * 16;
+  static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
+  (void)a;
+  const Geo g = make_geo(ctx);
+  const dim3 grid(ctx->nzh / TW, ctx->Ny, 3);
+  k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, ctx->spec);
+  ctx->cnt.launches++;
+  const cudaError_t e = cudaGetLastError();
+  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_x_fast");
+  return true;
+}
+
+template <int M>
+bool zf_launch(fm_ctx* ctx, const ProArgs& pa, int* st) {
+  using S = ZShape<M>;
+  const Geo g = make_geo(ctx);
+  const int nxy = ctx->Nx * ctx->Ny;
+  const dim3 grid((nxy + S::G - 1) / S::G);
+  switch (pa.kind) {
+    case PRO_COPY: {
+      static bool a = (allow(k_zf_fast<M, PRO_COPY>, S::SMEM), true);
+      (void)a;
+      k_zf_fast<M, PRO_COPY><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
+      break;
+    }
+    case PRO_K4: {
+      static bool a = (allow(k_zf_fast<M, PRO_K4>, S::SMEM), true);
+      (void)a;
+      k_zf_fast<M, PRO_K4><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
+      break;
+    }
+    default: {
+      static bool a = (allow(k_zf_fast<M, PRO_SVK>, S::SMEM), true);
+      (void)a;
+      k_zf_fast<M, PRO_SVK><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
+      break;
+    }
+  }
+  ctx->cnt.launches++;
+  const cudaError_t e = cudaGetLastError();
+  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_zf_fast");
+  return true;
+}
+
+template <int M>
+bool zi_launch(fm_ctx* ctx, double* out, double scale, int* st) {
+  using S = ZShape<M>;
+  static bool a = (allow(k_zi_fast<M>, S::SMEM), true);
+  (void)a;
+  const Geo g = make_geo(ctx);
+  const int nxy = ctx->Nx * ctx->Ny;
+  const dim3 grid((nxy + S::G - 1) / S::G);
+  k_zi_fast<M><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, ctx->spec, out, scale);
+  ctx->cnt.launches++;
+  const cudaError_t e = cudaGetLastError();
+  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_zi_fast");
+  return true;
+}
+
+bool fast_z_ok(const fm_ctx* ctx) {
+  return ctx->tdim == 3 && ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE && ctx->Nz % 2 == 0 &&
+         ctx->nzh == ctx->Nz / 2;
+}
+bool fast_xy_ok(const fm_ctx* ctx, int N) {
+  return ctx->tdim == 3 && ctx->nzh % tw_of(N) == 0 && ctx->nzh % tw_x(N) == 0;
+}
+
+}  // namespace
+
+#define FM_POW2_CASES(X, N_, ...)              \
+  switch (N_) {                                \
+    case 32: return X<32>(__VA_ARGS__);        \
+    case 64: return X<64>(__VA_ARGS__);        \
+    case 128: return X<128>(__VA_ARGS__);      \
+    case 256: return X<256>(__VA_ARGS__);      \
+    case 512: return X<512>(__VA_ARGS__);      \
+    case 1024: return X<1024>(__VA_ARGS__);    \
+    default: return false;                     \
+  }
+
+bool y_fast(fm_ctx* ctx, int sign, int* st) {
+  if (!fast_xy_ok(ctx, ctx->Ny)) return false;
+  FM_POW2_CASES(y_launch, ctx->Ny, ctx, sign, st)
+}
+
+bool x_fast(fm_ctx* ctx, int* st) {
+  if (!fast_xy_ok(ctx, ctx->Nx)) return false;
+  FM_POW2_CASES(x_launch, ctx->Nx, ctx, st)
+}
+
+bool zf_fast(fm_ctx* ctx, const ProArgs& pa, int* st) {
+  if (!fast_z_ok(ctx)) return false;
+  switch (ctx->Nz / 2) {
+    case 16: return zf_launch<16>(ctx, pa, st);
+    case 32: return zf_launch<32>(ctx, pa, st);
+    case 64: return zf_launch<64>(ctx, pa, st);
+    case 128: return zf_launch<128>(ctx, pa, st);
+    case 256: return zf_launch<256>(ctx, pa, st);
+    case 512: return zf_launch<512>(ctx, pa, st);
+    default: return false;
+  }
+}
+
+bool zi_fast(fm_ctx* ctx, double* out, double scale, int* st) {
+  if (!fast_z_ok(ctx)) return false;
+  switch (ctx->Nz / 2) {
+    case 16: return zi_launch<16>(ctx, out, scale, st);
+    case 32: return zi_launch<32>(ctx, out, scale, st);
+    case 64: return zi_launch<64>(ctx, out, scale, st);
+    case 128: return zi_launch<128>(ctx, out, scale, st);
+    case 256: return zi_launch<256>(ctx, out, scale, st);
+    case 512: return zi_launch<512>(ctx, out, scale, st);
+    default: return false;
+  }
+}
+
+}  // namespace fm

@@ -25,6 +25,13 @@ CASES = [
     ((12, 10, 14), None, 3, 1),
     ((16, 9, 24), None, 3, 0),
     ((64, 64, 64), None, 3, 0),
+    ((128, 64, 32), None, 3, 0),
+    ((32, 256, 64), (2.0, 1.0, 0.5), 3, 0),
+    ((512, 32, 32), None, 3, 0),
+    ((1024, 16, 32), None, 3, 0),
+    ((32, 1024, 16), None, 3, 0),
+    ((16, 16, 1024), None, 3, 0),
+    ((64, 64, 64), None, 3, 1),
     ((1, 1, 1), None, 3, 0),
     ((2, 2, 2), None, 3, 0),
     ((3, 1, 2), None, 3, 0),
