@@ -96,7 +96,8 @@ __device__ __forceinline__ void stage(double2 (&v)[E], double2* sml, int LS, int
   constexpr int T = N / E;
   constexpr int B = E / R;
   constexpr bool last = (Ns * R == N);
-  double2 out[E];
+  // Butterfly b reads v[b + r B] and (last stage) writes v[b + k B]: the
+  // same residue class mod B, so the update is in place.
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     const int j = t + T * b;
@@ -111,17 +112,14 @@ __device__ __forceinline__ void stage(double2 (&v)[E], double2* sml, int LS, int
     Dft<R, SIGN>::run(a);
     if constexpr (last) {
 #pragma unroll
-      for (int k = 0; k < R; ++k) out[b + k * B] = a[k];
+      for (int k = 0; k < R; ++k) v[b + k * B] = a[k];
     } else {
       const int base = (j / Ns) * Ns * R + jm;
 #pragma unroll
       for (int k = 0; k < R; ++k) sml[(base + k * Ns) * LS] = a[k];
     }
   }
-  if constexpr (last) {
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = out[m];
-  } else {
+  if constexpr (!last) {
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = sml[(t + T * m) * LS];
@@ -153,6 +151,7 @@ __device__ __forceinline__ void fft(double2 (&v)[E], double2* sml, int LS, int t
 
 // Elements per thread used by each pass for a line length N.
 __host__ __device__ constexpr int e_line(int N) { return N >= 128 ? 16 : (N >= 8 ? 8 : N); }
+__host__ __device__ constexpr int e_z(int M) { return M >= 8 ? 8 : M; }
 __host__ __device__ constexpr int e_x(int N) { return N >= 8 ? 8 : N; }
 
 }  // namespace reg

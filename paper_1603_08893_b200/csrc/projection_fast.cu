@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(TW*(N / e_line(N))) k_y_fast(Geo g, const doub
 
 // ------------------------------------------------------------------ x pass
 template <int N, int TW, int TD>
-__global__ void __launch_bounds__(TW*(N / e_x(N))) k_x_fast(Geo g, const double2* __restrict__ tw,
+__global__ void __launch_bounds__(TW*(N / e_x(N)), 2) k_x_fast(Geo g, const double2* __restrict__ tw,
                                                             double2* __restrict__ spec) {
   constexpr int E = e_x(N), T = N / E;
   extern __shared__ double2 sm[];
@@ -94,11 +94,14 @@ __global__ void __launch_bounds__(TW*(N / e_x(N))) k_x_fast(Geo g, const double2
 }
 
 // --------------------------------------------------------------- z passes
-template <int M>
+// HEAVY: K4 / SVK prologue (720 B read per voxel): larger E, ~144 threads and
+// ~40 KB per CTA so 4 CTAs per SM overlap their load and FFT phases.
+template <int M, bool HEAVY = false>
 struct ZShape {
-  static constexpr int E = e_line(M);
+  static constexpr int E = HEAVY ? e_line(M) : reg::e_z(M);
   static constexpr int T = M / E;
-  static constexpr int G = T >= 32 ? 1 : 32 / T;  // z-lines per CTA
+  static constexpr int TT = HEAVY ? 16 : 32;
+  static constexpr int G = T >= TT ? 1 : TT / T;  // z-lines per CTA
   static constexpr int LSL = 9 * G;                // smem lines (9 components x G)
   static constexpr int LSP = LSL | 1;              // odd pitch: conflict-free strided access
   static constexpr int THREADS = LSL * T;
@@ -106,10 +109,10 @@ struct ZShape {
 };
 
 template <int M, int PRO>
-__global__ void __launch_bounds__(ZShape<M>::THREADS) k_zf_fast(Geo g, const double2* __restrict__ twM,
+__global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast(Geo g, const double2* __restrict__ twM,
                                                                 const double2* __restrict__ twN,
                                                                 ProArgs pa, double2* __restrict__ spec) {
-  using S = ZShape<M>;
+  using S = ZShape<M, PRO != PRO_COPY>;
   constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
   extern __shared__ double2 sm[];
   double* smd = reinterpret_cast<double*>(sm);
@@ -259,31 +262,23 @@ bool x_launch(fm_ctx* ctx, int* st) {
   return true;
 }
 
-template <int M>
-bool zf_launch(fm_ctx* ctx, const ProArgs& pa, int* st) {
-  using S = ZShape<M>;
+template <int M, int PRO>
+void zf_go(fm_ctx* ctx, const ProArgs& pa) {
+  using S = ZShape<M, PRO != PRO_COPY>;
+  static bool a = (allow(k_zf_fast<M, PRO>, S::SMEM), true);
+  (void)a;
   const Geo g = make_geo(ctx);
   const int nxy = ctx->Nx * ctx->Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
+  k_zf_fast<M, PRO><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
+}
+
+template <int M>
+bool zf_launch(fm_ctx* ctx, const ProArgs& pa, int* st) {
   switch (pa.kind) {
-    case PRO_COPY: {
-      static bool a = (allow(k_zf_fast<M, PRO_COPY>, S::SMEM), true);
-      (void)a;
-      k_zf_fast<M, PRO_COPY><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
-      break;
-    }
-    case PRO_K4: {
-      static bool a = (allow(k_zf_fast<M, PRO_K4>, S::SMEM), true);
-      (void)a;
-      k_zf_fast<M, PRO_K4><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
-      break;
-    }
-    default: {
-      static bool a = (allow(k_zf_fast<M, PRO_SVK>, S::SMEM), true);
-      (void)a;
-      k_zf_fast<M, PRO_SVK><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
-      break;
-    }
+    case PRO_COPY: zf_go<M, PRO_COPY>(ctx, pa); break;
+    case PRO_K4: zf_go<M, PRO_K4>(ctx, pa); break;
+    default: zf_go<M, PRO_SVK>(ctx, pa); break;
   }
   ctx->cnt.launches++;
   const cudaError_t e = cudaGetLastError();
