@@ -363,6 +363,21 @@ class Model:
         return rep.as_dict()
 
 
+def run_program(model, F, fbars, P_out=None, sink=None, **params):
+    """run_program (solver.cpp:162-169): increments in order, history committed
+    at each convergence (inside solve_increment), reports streamed to `sink`.
+    Raises on the first failed increment after notifying the sink of the
+    completed ones.  Returns the list of reports."""
+    reports = []
+    P_out = P_out if P_out is not None else model.ctx.field()
+    for idx, fbar in enumerate(fbars):
+        rep = model.solve_increment(F, fbar, P_out=P_out, **params)
+        reports.append(rep)
+        if sink is not None:
+            sink(idx, fbar, rep, F, P_out, model)
+    return reports
+
+
 def identity_field(points, tdim):
     n = int(np.prod(points))
     F = np.zeros(tdim * tdim * n)

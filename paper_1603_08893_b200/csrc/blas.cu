@@ -93,7 +93,25 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_update(double* __restrict__ 
   const double alpha = scal[S_ALPHA];
   double s = 0.0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride) {
+  const int64_t c2 = count / 2;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* a2 = reinterpret_cast<const double2*>(Ap);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < c2; i += stride) {
+    const double2 pv = __ldg(p2 + i), av = __ldg(a2 + i);
+    double2 xv = x2[i], rv = r2[i];
+    xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+    xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+    rv.x = __dadd_rn(rv.x, __dmul_rn(-alpha, av.x));
+    rv.y = __dadd_rn(rv.y, __dmul_rn(-alpha, av.y));
+    x2[i] = xv;
+    r2[i] = rv;
+    s += rv.x * rv.x;
+    s += rv.y * rv.y;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (count & 1)) {
+    const int64_t i = count - 1;
     x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
     const double ri = __dadd_rn(r[i], __dmul_rn(-alpha, Ap[i]));
     r[i] = ri;
@@ -217,6 +235,13 @@ int cg_update_async(fm_ctx* ctx, double* x, double* r, const double* p, const do
 
 int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count) {
   k_cg_direction<<<ew_blocks(count), 256, 0, ctx->stream>>>(p, r, count, ctx->d_scal);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+// <p,Ap> from the partials the fused z-inverse epilogue wrote (solver.cpp:37-45)
+int cg_pap_finalize_async(fm_ctx* ctx, int n_partials) {
+  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_epi, n_partials, ctx->d_scal, 1, 0);
   FM_LAUNCHED(ctx);
   return FM_OK;
 }

@@ -124,6 +124,8 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
   ctx->red_blocks = int(rb < 1 ? 1 : (rb > 148 * 4 ? 148 * 4 : rb));
   if (cudaMalloc(&ctx->d_partial, sizeof(double) * (ctx->red_blocks + 16) * 16) != cudaSuccess)
     return fail(FM_E_OOM);
+  ctx->epi_cap = int64_t(ctx->Nx) * ctx->Ny + 1;
+  if (cudaMalloc(&ctx->d_epi, sizeof(double) * ctx->epi_cap) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMalloc(&ctx->d_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMemset(ctx->d_scal, 0, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_CUDA);
   if (cudaMallocHost(&ctx->h_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
@@ -146,6 +148,7 @@ int fm_ctx_destroy(fm_ctx* ctx) {
   if (ctx->d_tw) cudaFree(ctx->d_tw);
   if (ctx->spec) cudaFree(ctx->spec);
   if (ctx->d_partial) cudaFree(ctx->d_partial);
+  if (ctx->d_epi) cudaFree(ctx->d_epi);
   if (ctx->d_scal) cudaFree(ctx->d_scal);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
   if (ctx->d_bad) cudaFree(ctx->d_bad);

@@ -85,6 +85,8 @@ struct fm_ctx {
   // reductions
   int red_blocks = 0;
   double* d_partial = nullptr;  // red_blocks * 16
+  double* d_epi = nullptr;      // per-block partials of the fused <p,Ap>
+  int64_t epi_cap = 0;
   double* d_scal = nullptr;     // device scalars (64)
   double* h_scal = nullptr;     // pinned mirror (64)
   unsigned long long* d_bad = nullptr;  // lowest offending node (atomicMin)
@@ -125,9 +127,22 @@ struct ProArgs {
   const double* F = nullptr;   // PRO_SVK
   const double* lam = nullptr; // PRO_SVK
   const double* mu = nullptr;  // PRO_SVK
+  // CG direction update fused into the prologue (solver.cpp:51-55):
+  // p = beta p + r is formed per voxel, written back to p and used as dF.
+  const double* r = nullptr;
+  double* p = nullptr;
+  const double* beta = nullptr;  // device scalar
+};
+// Epilogue of the last pass: per-block partial sums of <pdot, out>
+// (the CG curvature <p, Ap>, solver.cpp:37) written to `partial`.
+struct EpiArgs {
+  const double* pdot = nullptr;
+  double* partial = nullptr;
 };
 // out = scale * n * G(prologue(args)); scale = 1 gives the reference G.
-int projection_run(fm_ctx* ctx, const ProArgs& args, double* out, double scale);
+// Returns the number of partial sums written through epi (0 if none).
+int projection_run(fm_ctx* ctx, const ProArgs& args, double* out, double scale,
+                   const EpiArgs& epi = EpiArgs{}, int* n_partials = nullptr);
 int profile_collect(fm_ctx* ctx);
 
 // blas.cu -------------------------------------------------------------------
@@ -144,6 +159,7 @@ int cg_update_async(fm_ctx* ctx, double* x, double* r, const double* p, const do
                     int64_t count);
 int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count);
 int cg_pap_async(fm_ctx* ctx, const double* p, const double* Ap, int64_t count);
+int cg_pap_finalize_async(fm_ctx* ctx, int n_partials);
 
 // constitutive.cu -----------------------------------------------------------
 int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const double* mu, double* P,

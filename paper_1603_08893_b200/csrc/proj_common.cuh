@@ -2,6 +2,7 @@
 #pragma once
 
 #include "fft_reg.cuh"
+#include "reduce.cuh"
 
 namespace fm {
 
@@ -14,6 +15,23 @@ struct Geo {
 __device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) ? i : i - n; }
 
 // ------------------------------------------------------------------ pass 1
+// dF of one voxel: either read, or (fused CG direction) p = beta p + r.
+template <int NC>
+__device__ __forceinline__ void load_dF(const ProArgs& pa, int64_t n, int64_t node, double* d) {
+  if (pa.r) {
+    const double beta = *pa.beta;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double pc = __dadd_rn(__dmul_rn(pa.p[c * n + node], beta), __ldg(pa.r + c * n + node));
+      pa.p[c * n + node] = pc;
+      d[c] = pc;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) d[c] = __ldg(pa.A + c * n + node);
+  }
+}
+
 template <int TD, int PRO>
 __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int64_t node,
                                                double v[TD * TD]) {
@@ -24,8 +42,7 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
   } else if (PRO == PRO_K4) {
     // dP_ij = K_jikl dF_kl (projection.cpp:184)
     double df[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) df[c] = __ldg(pa.A + c * n + node);
+    load_dF<NC>(pa, n, node, df);
 #pragma unroll
     for (int i = 0; i < TD; ++i)
 #pragma unroll
@@ -39,11 +56,9 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
     // SVK tangent action (hyperelastic.cpp:55-63 contracted analytically):
     // dP = lam tr(F^T dF) F + mu F dF^T F + mu F F^T dF + dF S
     double f[NC], d[NC];
+    load_dF<NC>(pa, n, node, d);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      f[c] = __ldg(pa.F + c * n + node);
-      d[c] = __ldg(pa.A + c * n + node);
-    }
+    for (int c = 0; c < NC; ++c) f[c] = __ldg(pa.F + c * n + node);
     const double lam = __ldg(pa.lam + node), mu = __ldg(pa.mu + node);
     double trFd = 0.0;
 #pragma unroll
@@ -114,6 +129,7 @@ inline Geo make_geo(const fm_ctx* ctx) {
 bool zf_fast(fm_ctx* ctx, const ProArgs& pa, int* st);
 bool y_fast(fm_ctx* ctx, int sign, int* st);
 bool x_fast(fm_ctx* ctx, int* st);
-bool zi_fast(fm_ctx* ctx, double* out, double scale, int* st);
+bool zi_fast(fm_ctx* ctx, double* out, double scale, const EpiArgs& epi, int* st);
+int zi_fast_blocks(const fm_ctx* ctx);  // partial sums the fast z-inverse writes
 
 }  // namespace fm

@@ -161,7 +161,7 @@ template <int TD>
 __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double2* __restrict__ twN,
                                               const double2* __restrict__ spec,
                                               double* __restrict__ out, int G, int ls,
-                                              double scale) {
+                                              double scale, EpiArgs epi) {
   extern __shared__ double2 sm[];
   constexpr int NC = TD * TD;
   const int nxy = g.Nx * g.Ny;
@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double
   }
   __syncthreads();
   double2* R = fft_smem(B, A, NC * G, ls, 1, plan, +1, false);
+  double dot = 0.0;
   for (int w = threadIdx.x; w < NC * Gb * g.Nz; w += blockDim.x) {
     const int line = w / g.Nz, z = w - line * g.Nz;
     const int c = line / Gb, gi = line - c * Gb;
@@ -206,7 +207,13 @@ __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double
     } else {
       v = Zl[z].x;
     }
-    out[int64_t(c) * g.n + int64_t(L0 + gi) * g.Nz + z] = v * scale;
+    const int64_t idx = int64_t(c) * g.n + int64_t(L0 + gi) * g.Nz + z;
+    out[idx] = v * scale;
+    if (epi.partial) dot += __ldg(epi.pdot + idx) * (v * scale);
+  }
+  if (epi.partial) {
+    dot = block_sum_any(dot);
+    if (threadIdx.x == 0) epi.partial[blockIdx.x] = dot;
   }
 }
 
@@ -216,7 +223,12 @@ constexpr int kMaxSmem = 227 * 1024;
 
 template <typename K>
 void allow_smem(K kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  // dynamic limit = 227 KB minus the kernel's static shared memory
+  cudaFuncAttributes attr{};
+  cudaFuncGetAttributes(&attr, kernel);
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kMaxSmem - int(attr.sharedSizeBytes));
+  cudaGetLastError();  // attribute calls must not leave a sticky launch error behind
 }
 
 int tile_width(int nzh, int N, int lines_per_col, int& TW) {
@@ -244,7 +256,7 @@ void prof_mark(fm_ctx* ctx) {
 }
 
 template <int TD>
-int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale) {
+int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiArgs& epi, int* nparts) {
   constexpr int NC = TD * TD;
   static bool init = false;
   if (!init) {
@@ -265,7 +277,7 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale) {
   int G = int(std::max<size_t>(1, std::min<size_t>(16, size_t(96 * 1024) / (size_t(2) * NC * ls * 16))));
   G = std::min(G, nxy);
   const size_t smz = size_t(2) * NC * G * ls * 16;
-  if (smz > size_t(kMaxSmem))
+  if (smz + 1024 > size_t(kMaxSmem))
     return set_error(ctx, FM_E_UNSUPPORTED, "z line too long for the shared-memory FFT");
   const dim3 gz((nxy + G - 1) / G);
   int TWy, TWx;
@@ -319,12 +331,15 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale) {
   }
   // pass 5: z inverse (c2r), scale
   prof_mark(ctx);
-  if (!(TD == 3 && zi_fast(ctx, out, scale / double(ctx->n), &st))) {
+  if (!(TD == 3 && zi_fast(ctx, out, scale / double(ctx->n), epi, &st))) {
     k_zinv<TD><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, ctx->spec, out, G, ls,
-                                              scale / double(ctx->n));
+                                              scale / double(ctx->n), epi);
     FM_LAUNCHED(ctx);
+    if (nparts) *nparts = int(gz.x);
   } else if (st) {
     return st;
+  } else if (nparts) {
+    *nparts = zi_fast_blocks(ctx);
   }
   prof_mark(ctx);
   if (ctx->prof.on) ctx->prof.calls++;
@@ -347,9 +362,11 @@ int profile_collect(fm_ctx* ctx) {
   return FM_OK;
 }
 
-int projection_run(fm_ctx* ctx, const ProArgs& pa, double* out, double scale) {
-  if (ctx->tdim == 3) return run_td<3>(ctx, pa, out, scale);
-  return run_td<2>(ctx, pa, out, scale);
+int projection_run(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiArgs& epi,
+                   int* n_partials) {
+  if (n_partials) *n_partials = 0;
+  if (ctx->tdim == 3) return run_td<3>(ctx, pa, out, scale, epi, n_partials);
+  return run_td<2>(ctx, pa, out, scale, epi, n_partials);
 }
 
 }  // namespace fm

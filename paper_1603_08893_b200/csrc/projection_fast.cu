@@ -159,7 +159,8 @@ template <int M>
 __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const double2* __restrict__ twM,
                                                                 const double2* __restrict__ twN,
                                                                 const double2* __restrict__ spec,
-                                                                double* __restrict__ out, double scale) {
+                                                                double* __restrict__ out, double scale,
+                                                                EpiArgs epi) {
   using S = ZShape<M>;
   constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
   extern __shared__ double2 sm[];
@@ -204,11 +205,20 @@ __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const dou
     for (int m = 0; m < E; ++m) sm[(t + T * m) * LSP + l] = v[m];
   }
   __syncthreads();
+  double dot = 0.0;
   for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
     const int gi = w / N, z = w - gi * N;
     const int64_t node = int64_t(L0 + gi) * N + z;
 #pragma unroll
-    for (int c = 0; c < 9; ++c) out[c * g.n + node] = smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] * scale;
+    for (int c = 0; c < 9; ++c) {
+      const double val = smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] * scale;
+      out[c * g.n + node] = val;
+      if (epi.partial) dot += __ldg(epi.pdot + c * g.n + node) * val;
+    }
+  }
+  if (epi.partial) {  // fused <p, Ap> partial (solver.cpp:37)
+    dot = block_sum_any(dot);
+    if (threadIdx.x == 0) epi.partial[blockIdx.x] = dot;
   }
 }
 
@@ -219,6 +229,7 @@ namespace {
 template <typename K>
 void allow(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  cudaGetLastError();
 }
 
 int tw_of(int N) { return N >= 1024 ? 4 : 8; }
@@ -287,19 +298,40 @@ bool zf_launch(fm_ctx* ctx, const ProArgs& pa, int* st) {
 }
 
 template <int M>
-bool zi_launch(fm_ctx* ctx, double* out, double scale, int* st) {
+bool zi_launch(fm_ctx* ctx, double* out, double scale, const EpiArgs& epi, int* st) {
   using S = ZShape<M>;
   static bool a = (allow(k_zi_fast<M>, S::SMEM), true);
   (void)a;
   const Geo g = make_geo(ctx);
   const int nxy = ctx->Nx * ctx->Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
-  k_zi_fast<M><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, ctx->spec, out, scale);
+  k_zi_fast<M><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, ctx->spec, out, scale, epi);
   ctx->cnt.launches++;
   const cudaError_t e = cudaGetLastError();
   *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_zi_fast");
   return true;
 }
+
+bool fast_z_ok(const fm_ctx* ctx);
+
+}  // namespace
+
+int zi_fast_blocks(const fm_ctx* ctx) {
+  const int nxy = ctx->Nx * ctx->Ny;
+  int G = 0;
+  switch (ctx->Nz / 2) {
+    case 16: G = ZShape<16>::G; break;
+    case 32: G = ZShape<32>::G; break;
+    case 64: G = ZShape<64>::G; break;
+    case 128: G = ZShape<128>::G; break;
+    case 256: G = ZShape<256>::G; break;
+    case 512: G = ZShape<512>::G; break;
+    default: return 0;
+  }
+  return fast_z_ok(ctx) ? (nxy + G - 1) / G : 0;
+}
+
+namespace {
 
 bool fast_z_ok(const fm_ctx* ctx) {
   return ctx->tdim == 3 && ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE && ctx->Nz % 2 == 0 &&
@@ -345,15 +377,15 @@ bool zf_fast(fm_ctx* ctx, const ProArgs& pa, int* st) {
   }
 }
 
-bool zi_fast(fm_ctx* ctx, double* out, double scale, int* st) {
+bool zi_fast(fm_ctx* ctx, double* out, double scale, const EpiArgs& epi, int* st) {
   if (!fast_z_ok(ctx)) return false;
   switch (ctx->Nz / 2) {
-    case 16: return zi_launch<16>(ctx, out, scale, st);
-    case 32: return zi_launch<32>(ctx, out, scale, st);
-    case 64: return zi_launch<64>(ctx, out, scale, st);
-    case 128: return zi_launch<128>(ctx, out, scale, st);
-    case 256: return zi_launch<256>(ctx, out, scale, st);
-    case 512: return zi_launch<512>(ctx, out, scale, st);
+    case 16: return zi_launch<16>(ctx, out, scale, epi, st);
+    case 32: return zi_launch<32>(ctx, out, scale, epi, st);
+    case 64: return zi_launch<64>(ctx, out, scale, epi, st);
+    case 128: return zi_launch<128>(ctx, out, scale, epi, st);
+    case 256: return zi_launch<256>(ctx, out, scale, epi, st);
+    case 512: return zi_launch<512>(ctx, out, scale, epi, st);
     default: return false;
   }
 }

@@ -30,6 +30,28 @@ int op_apply(fm_ctx* ctx, const Op& op, const double* x, double* out, double sca
   return projection_run(ctx, pa, out, scale);
 }
 
+// One CG matvec with the CG vector work fused into its first and last pass:
+//   prologue: p = beta p + r (unless first), dF = p;  epilogue: <p, Ap> partials.
+int op_apply_cg(fm_ctx* ctx, const Op& op, double* p, const double* r, bool first, double* Ap,
+                int* n_partials) {
+  ProArgs pa;
+  pa.kind = op.kind;
+  pa.A = p;
+  pa.K = op.K;
+  pa.F = op.F;
+  pa.lam = op.lam;
+  pa.mu = op.mu;
+  if (!first) {
+    pa.r = r;
+    pa.p = p;
+    pa.beta = ctx->d_scal + S_BETA;
+  }
+  EpiArgs epi;
+  epi.pdot = p;
+  epi.partial = ctx->d_epi;
+  return projection_run(ctx, pa, Ap, 1.0, epi, n_partials);
+}
+
 Op model_op(fm_model* m) {
   Op op;
   if (m->kind == 0 && m->matrix_free) {
@@ -80,8 +102,10 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
   FM_CUDA(ctx, cudaMemcpyAsync(ctx->p.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
   double rr = ctx->h_scal[S_RR];
   for (int64_t it = 1; it <= cap; ++it) {
-    if (int st = op_apply(ctx, op, ctx->p.d, ctx->Ap.d, 1.0)) return st;     // :36
-    if (int st = cg_pap_async(ctx, ctx->p.d, ctx->Ap.d, count)) return st;   // :37
+    // :36-37 with :51-55 of the previous iteration folded in (p = beta p + r)
+    int nparts = 0;
+    if (int st = op_apply_cg(ctx, op, ctx->p.d, ctx->r.d, it == 1, ctx->Ap.d, &nparts)) return st;
+    if (int st = cg_pap_finalize_async(ctx, nparts)) return st;
     if (int st = cg_update_async(ctx, x, ctx->r.d, ctx->p.d, ctx->Ap.d, count)) return st;  // :46-48
     if (int st = fetch_scalars(ctx, S_FLAG + 1)) return st;
     if (ctx->h_scal[S_FLAG] != 0.0) {  // !(pAp > 0): return without updating x (:38-44)
@@ -95,8 +119,7 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
       *rel = std::sqrt(rr_new) / bnorm;
       return FM_OK;
     }
-    rr = rr_new;
-    if (int st = cg_direction_async(ctx, ctx->p.d, ctx->r.d, count)) return st;  // :51-55
+    rr = rr_new;  // p *= beta; p += r happens in the next matvec's prologue
   }
   *iters = int32_t(cap);
   *rel = std::sqrt(rr) / bnorm;

@@ -1,0 +1,115 @@
+"""Generates the committed golden fixtures of BASELINE.json configs 0 and 1
+(31^3) with the CPU oracle (oracle/, restating the reference solver).  The
+oracle is itself pinned to the reference's golden run records (see
+tests/test_oracle_pins.py).  Run: python tests/golden/make_golden.py [0] [1]"""
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle import oracle as O  # noqa: E402
+from paper_1603_08893_b200 import microstructure as M  # noqa: E402
+
+
+def config0():
+    pts = (31, 31, 31)
+    pg = M.corner_cube(pts, 9)
+    lam, mu, _, _ = M.bind_parameters(pg, [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)])
+    t = time.time()
+    F, P, reps, st, _ = O.run_program(pts, 3, 0, lam, mu, M.simple_shear_program(0.1, 1, 3))
+    assert st == 0, st
+    np.savez_compressed(os.path.join(HERE, "config0.npz"), F=F, P=P,
+                        passes=np.array([r["passes"] for r in reps]),
+                        cg_it=np.array([r["cg_it"] + [0] * (64 - len(r["cg_it"])) for r in reps]),
+                        rel_update=np.array([r["rel_update"] + [0.0] * (64 - len(r["rel_update"])) for r in reps]),
+                        eq_rel=np.array([r["eq_rel"] for r in reps]))
+    print("config0", time.time() - t, [r["cg_it"] for r in reps])
+
+
+def config1():
+    pts = (31, 31, 31)
+    pg = M.corner_cube(pts, 9)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    t = time.time()
+    F, P, reps, st, epsp = O.run_program(pts, 3, 1, lam, mu, M.simple_shear_program(0.1, 20, 3),
+                                         ty0=ty, hard=h)
+    assert st == 0, st
+    np.savez_compressed(os.path.join(HERE, "config1.npz"), F=F, P=P, epsp=epsp,
+                        passes=np.array([r["passes"] for r in reps]),
+                        cg_it=np.array([r["cg_it"] + [0] * (64 - len(r["cg_it"])) for r in reps]),
+                        rel_update=np.array([r["rel_update"] + [0.0] * (64 - len(r["rel_update"])) for r in reps]),
+                        eq_rel=np.array([r["eq_rel"] for r in reps]))
+    print("config1", time.time() - t, [r["cg_it"] for r in reps])
+
+
+def config1_band(eps):
+    """CG-count sensitivity band of config 1: the oracle re-run with lambda
+    scaled by (1 + eps), eps = +-1e-15.  Config 1's J2 passes take ~100-300
+    CG iterations, and a 1e-15 relative perturbation alone moves their counts
+    by several iterations; GPU counts are checked against this band."""
+    pts = (31, 31, 31)
+    pg = M.corner_cube(pts, 9)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    _, _, reps, st, _ = O.run_program(pts, 3, 1, lam * (1.0 + eps), mu,
+                                      M.simple_shear_program(0.1, 20, 3), ty0=ty, hard=h)
+    assert st == 0, st
+    tag = "p" if eps > 0 else "m"
+    np.savez_compressed(os.path.join(HERE, f"config1_band_{tag}.npz"),
+                        passes=np.array([r["passes"] for r in reps]),
+                        cg_it=np.array([r["cg_it"] + [0] * (64 - len(r["cg_it"])) for r in reps]))
+    print("band", eps, [r["cg_it"] for r in reps])
+
+
+PERTURB = [("lam", 1e-15), ("lam", -1e-15), ("mu", 1e-15), ("mu", -1e-15), ("lam", 3e-16), ("mu", -3e-16)]
+
+
+def _simo16_run(args):
+    which, eps = args
+    pts = (16, 16, 16)
+    pg = M.corner_cube(pts, 3)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    if which == "lam":
+        lam = lam * (1.0 + eps)
+    elif which == "mu":
+        mu = mu * (1.0 + eps)
+    return O.run_program(pts, 3, 1, lam, mu, M.simple_shear_program(0.02, 4, 3), ty0=ty, hard=h)
+
+
+def simo16():
+    """16^3 J2 case of tests/test_gpu_solver.py: the oracle run plus its
+    CG-count envelope under six 1e-15-level perturbations of lambda / mu."""
+    from multiprocessing import Pool
+    with Pool(7) as pool:
+        runs = pool.map(_simo16_run, [("none", 0.0)] + PERTURB)
+    F, P, reps, st, epsp = runs[0]
+    assert st == 0
+    pad = lambda r: r["cg_it"] + [0] * (64 - len(r["cg_it"]))
+    np.savez_compressed(os.path.join(HERE, "simo16.npz"), F=F, P=P, epsp=epsp,
+                        passes=np.array([r["passes"] for r in reps]),
+                        cg_it=np.array([pad(r) for r in reps]),
+                        band_passes=np.array([[r["passes"] for r in run[2]] for run in runs[1:]]),
+                        band_cg_it=np.array([[pad(r) for r in run[2]] for run in runs[1:]]))
+    print("simo16", [r["cg_it"] for r in reps], [[r["cg_it"] for r in run[2]] for run in runs[1:]])
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["0", "1"]
+    if "simo16" in which:
+        simo16()
+    if "band+" in which:
+        config1_band(1e-15)
+    if "band-" in which:
+        config1_band(-1e-15)
+    if "0" in which:
+        config0()
+    if "1" in which:
+        config1()
