@@ -82,6 +82,36 @@ struct Grid {
 };
 
 // ------------------------------------------------------------- 1-D FFT
+// Twiddles as FFTW's trig generator produces them: octant-reduced, so the
+// quarter / half / eighth points are exact.
+static cplx unit_root(long long k, long long N) {
+  k %= N;
+  if (k < 0) k += N;
+  const long long k8 = 8 * k;
+  const int oct = int(k8 / N);            // octant 0..7 of the angle 2 pi k / N
+  long long r = k8 - (long long)oct * N;  // remainder within the octant, in units of 1/(8N)
+  const bool odd = oct & 1;
+  if (odd) r = N - r;                     // reflect so the reduced angle is in [0, pi/4]
+  const long double tau = 6.283185307179586476925286766559005768L;
+  const long double a = tau * (long double)r / (8.0L * (long double)N);
+  double c = (double)cosl(a), s = (double)sinl(a);
+  if (r == 0) { c = 1.0; s = 0.0; }
+  // angle theta = oct*pi/4 +/- a ; (cos theta, sin theta) by octant
+  double ct, st;
+  switch (oct) {
+    case 0: ct = c; st = s; break;
+    case 1: ct = s; st = c; break;
+    case 2: ct = -s; st = c; break;
+    case 3: ct = -c; st = s; break;
+    case 4: ct = -c; st = -s; break;
+    case 5: ct = -s; st = -c; break;
+    case 6: ct = s; st = -c; break;
+    default: ct = c; st = -s; break;
+  }
+  return cplx(ct, -st);  // exp(-i theta)
+}
+
+
 // Mixed-radix Stockham autosort FFT restating FFTW's unnormalised c2c DFT:
 // X[k] = sum_n x[n] exp(sign * 2 pi i n k / N).  Radices 4,2,3,5 and any
 // remaining prime by a direct O(p^2) butterfly.
@@ -99,11 +129,7 @@ struct Plan1D {
       while (m % p == 0) { radix.push_back(p); m /= p; }
     if (m > 1) radix.push_back(m);
     w.resize(size_t(n));
-    const long double tau = 6.283185307179586476925286766559005768L;
-    for (int k = 0; k < n; ++k) {
-      const long double a = -tau * (long double)k / (long double)n;
-      w[size_t(k)] = cplx((double)cosl(a), (double)sinl(a));
-    }
+    for (int k = 0; k < n; ++k) w[size_t(k)] = unit_root(k, n);
     int Ns = 1;
     for (int R : radix) {
       const int tstep = N / (Ns * R);

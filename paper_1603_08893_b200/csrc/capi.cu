@@ -52,13 +52,39 @@ static void make_plan(AxisPlan& p, int N) {
   if (m > 1) p.radix[p.nst++] = m;
 }
 
+// exp(-2 pi i k / N), exact at the octant points: the angle is reduced to
+// [0, pi/4] and mapped back with exact sign/swap rules, so W^{N/4} = -i,
+// W^{N/2} = -1 and W^{N/8} = (s, -s) with s = sqrt(1/2) exactly once rounded.
+static double2 unit_root(long long k, long long N) {
+  k %= N;
+  if (k < 0) k += N;
+  const long long k8 = 8 * k;
+  const int oct = int(k8 / N);            // octant 0..7 of the angle 2 pi k / N
+  long long r = k8 - (long long)oct * N;  // remainder within the octant, in units of 1/(8N)
+  const bool odd = oct & 1;
+  if (odd) r = N - r;                     // reflect so the reduced angle is in [0, pi/4]
+  const long double tau = 6.283185307179586476925286766559005768L;
+  const long double a = tau * (long double)r / (8.0L * (long double)N);
+  double c = (double)cosl(a), s = (double)sinl(a);
+  if (r == 0) { c = 1.0; s = 0.0; }
+  // angle theta = oct*pi/4 +/- a ; (cos theta, sin theta) by octant
+  double ct, st;
+  switch (oct) {
+    case 0: ct = c; st = s; break;
+    case 1: ct = s; st = c; break;
+    case 2: ct = -s; st = c; break;
+    case 3: ct = -c; st = s; break;
+    case 4: ct = -c; st = -s; break;
+    case 5: ct = -s; st = -c; break;
+    case 6: ct = s; st = -c; break;
+    default: ct = c; st = -s; break;
+  }
+  return make_double2(ct, -st);  // exp(-i theta)
+}
+
 static void twiddles(std::vector<double2>& all, int N, size_t& off) {
   off = all.size();
-  const long double tau = 6.283185307179586476925286766559005768L;
-  for (int k = 0; k < N; ++k) {
-    const long double a = -tau * (long double)k / (long double)N;
-    all.push_back(make_double2((double)cosl(a), (double)sinl(a)));
-  }
+  for (int k = 0; k < N; ++k) all.push_back(unit_root(k, N));
 }
 
 }  // namespace fm

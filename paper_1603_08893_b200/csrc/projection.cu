@@ -184,8 +184,13 @@ __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double
     double2 Z;
     if (even) {
       // Z[k] = (X[k] + X*[M-k]) + i W_N^{-k} (X[k] - X*[M-k]); X[M] = 0 when not stored
-      const double2 a = X[k];
-      const double2 b = (M - k < g.nzh) ? cconj(X[M - k]) : make_double2(0.0, 0.0);
+      // Re(ifft) as the reference takes it (projection.cpp:157-162): the kz = 0
+      // and kz = M columns of a real field are real, so their (round-off)
+      // imaginary parts are dropped, not folded into the output.
+      double2 a = X[k];
+      if (k == 0) a.y = 0.0;
+      double2 b = (M - k < g.nzh) ? cconj(X[M - k]) : make_double2(0.0, 0.0);
+      if (k == 0) b.y = 0.0;
       const double2 t = cmulc(csub(a, b), __ldg(&twN[k]));
       Z = make_double2(a.x + b.x - t.y, a.y + b.y + t.x);
     } else {

@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const dou
     const int c = w / (Gb * H), rem = w - c * (Gb * H);
     const int gi = rem / H, k = rem - gi * H;
     const int l = c * G + gi;
-    const double2 xk = sm[k * LSP + l];
+    double2 xk = sm[k * LSP + l];
+    if (k == 0) xk.y = 0.0;  // Re(ifft): drop the round-off imaginary part of kz = 0
     const double2 xm = k == 0 ? make_double2(0.0, 0.0) : sm[(M - k) * LSP + l];
     {
       const double2 b = cconj(xm);

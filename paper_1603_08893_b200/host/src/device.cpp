@@ -1,0 +1,68 @@
+#include "device.hpp"
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <tuple>
+
+#include "fftmech/errors.hpp"
+#include "fftmech/solver.hpp"
+
+namespace fftmech::detail {
+
+Device::~Device() {
+  if (h) fm_ctx_destroy(h);
+}
+
+std::shared_ptr<Device> device_for(const GridShape& shape, int tdim, int mode) {
+  using Key = std::tuple<int, int, int, int, double, double, double, int, int>;
+  static std::mutex mu;
+  static std::map<Key, std::weak_ptr<Device>> registry;
+  const Key key{shape.dim, shape.points[0], shape.points[1], shape.points[2], shape.lengths[0],
+                shape.lengths[1], shape.lengths[2], tdim, mode};
+  std::lock_guard<std::mutex> lock(mu);
+  if (auto live = registry[key].lock()) return live;
+  auto dev = std::make_shared<Device>();
+  dev->shape = shape;
+  dev->tdim = tdim;
+  dev->mode = mode;
+  const char* env = std::getenv("FFTMECH_DEVICE");
+  const int device = env ? std::atoi(env) : 0;
+  const int32_t pts[3] = {shape.points[0], shape.points[1], shape.points[2]};
+  const double len[3] = {shape.lengths[0], shape.lengths[1], shape.lengths[2]};
+  const int st = fm_ctx_create(shape.dim, pts, len, tdim, mode, device, &dev->h);
+  if (st == FM_E_INVALID) throw std::invalid_argument("tensor dim must be in [grid dim, 3]");
+  if (st != FM_OK) throw Error("fftmech: no usable CUDA device for the sm_100a kernels (status " + std::to_string(st) + ")");
+  registry[key] = dev;
+  return dev;
+}
+
+void throw_status(fm_ctx* h, int status, const std::string& where) {
+  fm_error_info info{};
+  if (h) fm_last_error_info(h, &info);
+  const std::string msg = where + ": " + (h ? fm_last_error(h) : "error");
+  switch (status) {
+    case FM_E_INVALID: throw std::invalid_argument(msg);
+    case FM_E_INVERTED: throw InvertedElement(static_cast<std::size_t>(info.node));
+    case FM_E_NOT_SPD: throw NotPositiveDefinite(static_cast<std::size_t>(info.node), info.value);
+    case FM_E_SINGULAR: throw SingularTensor(static_cast<std::size_t>(info.node));
+    case FM_E_CG_STALLED: throw CgStalled(info.cg_iterations, info.value);
+    default: throw Error(msg);
+  }
+}
+
+DevField::DevField(const std::shared_ptr<Device>& dev, int ncomp) : dev_(dev) {
+  check(dev_->h, fm_field_alloc(dev_->h, ncomp, &f_), "fm_field_alloc");
+}
+DevField::~DevField() {
+  if (f_) fm_field_free(dev_->h, f_);
+}
+void DevField::upload(std::span<const double> host) {
+  check(dev_->h, fm_field_upload(dev_->h, f_, host.data(), static_cast<int64_t>(host.size())), "upload");
+}
+void DevField::download(std::span<double> host) const {
+  check(dev_->h, fm_field_download(dev_->h, f_, host.data(), static_cast<int64_t>(host.size())), "download");
+}
+
+}  // namespace fftmech::detail

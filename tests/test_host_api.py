@@ -1,0 +1,30 @@
+"""The drop-in C++ API (paper_1603_08893_b200/host): reference-style client
+code compiled against `namespace fftmech` and linked to the CUDA library."""
+import os
+import subprocess
+
+import pytest
+
+LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1603_08893_b200", "lib")
+BIN = os.path.join(LIB, "test_host_api")
+
+
+def test_host_library_links_the_cuda_library():
+    assert os.path.exists(os.path.join(LIB, "libfftmech_host.so")) and os.path.exists(BIN)
+    out = subprocess.run(["ldd", BIN], capture_output=True, text=True).stdout
+    assert "libfftmech_host.so" in out and "libfftmech_b200.so" in out
+    syms = subprocess.run(["nm", "-DC", "--defined-only", os.path.join(LIB, "libfftmech_host.so")],
+                          capture_output=True, text=True).stdout
+    for name in ["fftmech::build_projection", "fftmech::apply_projection", "fftmech::apply_projected_tangent",
+                 "fftmech::cg_solve", "fftmech::solve_increment", "fftmech::run_program",
+                 "fftmech::HyperelasticModel::evaluate", "fftmech::SimoPlasticityModel::evaluate",
+                 "fftmech::make_cubic_inclusion", "fftmech::bind_parameters"]:
+        assert name in syms, name
+
+
+@pytest.mark.gpu
+def test_reference_style_cpp_client_passes_on_gpu():
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "[FAIL]" not in r.stdout
