@@ -288,8 +288,8 @@ class Field:
         self.ctx.check(lib().fm_field_upload(self.ctx.h, self.h, a, a.size))
         return self
 
-    def download(self):
-        out = np.empty(self.size)
+    def download(self, out=None):
+        out = np.empty(self.size) if out is None else out
         self.ctx.check(lib().fm_field_download(self.ctx.h, self.h, out, out.size))
         return out
 

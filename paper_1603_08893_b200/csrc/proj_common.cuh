@@ -16,23 +16,30 @@ __device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) 
 
 // ------------------------------------------------------------------ pass 1
 // dF of one voxel: either read, or (fused CG direction) p = beta p + r.
-template <int NC>
+// The new p is only formed here; store_dir() writes it back after every load
+// of the voxel has been issued (a store before the K4 loads would, through
+// possible aliasing, serialise them).
+template <int NC, bool DIR>
 __device__ __forceinline__ void load_dF(const ProArgs& pa, int64_t n, int64_t node, double* d) {
-  if (pa.r) {
+  if constexpr (DIR) {
     const double beta = *pa.beta;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const double pc = __dadd_rn(__dmul_rn(pa.p[c * n + node], beta), __ldg(pa.r + c * n + node));
-      pa.p[c * n + node] = pc;
-      d[c] = pc;
-    }
+    for (int c = 0; c < NC; ++c)
+      d[c] = __dadd_rn(__dmul_rn(__ldg(pa.p + c * n + node), beta), __ldg(pa.r + c * n + node));
   } else {
 #pragma unroll
     for (int c = 0; c < NC; ++c) d[c] = __ldg(pa.A + c * n + node);
   }
 }
+template <int NC, bool DIR>
+__device__ __forceinline__ void store_dir(const ProArgs& pa, int64_t n, int64_t node, const double* d) {
+  if constexpr (DIR) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) pa.p[c * n + node] = d[c];
+  }
+}
 
-template <int TD, int PRO>
+template <int TD, int PRO, bool DIR = false>
 __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int64_t node,
                                                double v[TD * TD]) {
   constexpr int NC = TD * TD;
@@ -42,7 +49,7 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
   } else if (PRO == PRO_K4) {
     // dP_ij = K_jikl dF_kl (projection.cpp:184)
     double df[NC];
-    load_dF<NC>(pa, n, node, df);
+    load_dF<NC, DIR>(pa, n, node, df);
 #pragma unroll
     for (int i = 0; i < TD; ++i)
 #pragma unroll
@@ -52,11 +59,12 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
         for (int kl = 0; kl < NC; ++kl) s += __ldg(pa.K + ((j * TD + i) * NC + kl) * n + node) * df[kl];
         v[i * TD + j] = s;
       }
+    store_dir<NC, DIR>(pa, n, node, df);
   } else {
     // SVK tangent action (hyperelastic.cpp:55-63 contracted analytically):
     // dP = lam tr(F^T dF) F + mu F dF^T F + mu F F^T dF + dF S
     double f[NC], d[NC];
-    load_dF<NC>(pa, n, node, d);
+    load_dF<NC, DIR>(pa, n, node, d);
 #pragma unroll
     for (int c = 0; c < NC; ++c) f[c] = __ldg(pa.F + c * n + node);
     const double lam = __ldg(pa.lam + node), mu = __ldg(pa.mu + node);
@@ -106,6 +114,7 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
         }
         v[i * TD + j] = a;
       }
+    store_dir<NC, DIR>(pa, n, node, d);
   }
 }
 

@@ -19,7 +19,7 @@
 
 namespace fm {
 
-template <int TD, int PRO>
+template <int TD, int PRO, bool DIR>
 __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double2* __restrict__ twN,
                                               ProArgs pa, double2* __restrict__ spec, int G, int ls) {
   extern __shared__ double2 sm[];
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double
     const int gi = w / g.Nz, z = w - gi * g.Nz;
     const int64_t node = int64_t(L0 + gi) * g.Nz + z;
     double v[NC];
-    prologue_voxel<TD, PRO>(pa, g.n, node, v);
+    prologue_voxel<TD, PRO, DIR>(pa, g.n, node, v);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       double2* line = A + (c * G + gi) * ls;
@@ -236,9 +236,11 @@ void allow_smem(K kernel) {
   cudaGetLastError();  // attribute calls must not leave a sticky launch error behind
 }
 
-int tile_width(int nzh, int N, int lines_per_col, int& TW) {
+int tile_width(int nzh, int N, int lines_per_col, int& TW, int64_t other_blocks) {
   TW = std::min(8, nzh);
   while (TW > 1 && size_t(2) * N * TW * lines_per_col * 16 > size_t(kMaxSmem)) TW /= 2;
+  // small grids: prefer more CTAs (>= 2 per SM) over wider tiles
+  while (TW > 2 && int64_t((nzh + TW - 1) / TW) * other_blocks < 2 * 148) TW /= 2;
   return size_t(2) * N * TW * lines_per_col * 16 <= size_t(kMaxSmem) ? 0 : -1;
 }
 
@@ -265,9 +267,11 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   constexpr int NC = TD * TD;
   static bool init = false;
   if (!init) {
-    allow_smem(k_zfwd<TD, PRO_COPY>);
-    allow_smem(k_zfwd<TD, PRO_K4>);
-    allow_smem(k_zfwd<TD, PRO_SVK>);
+    allow_smem(k_zfwd<TD, PRO_COPY, false>);
+    allow_smem(k_zfwd<TD, PRO_K4, false>);
+    allow_smem(k_zfwd<TD, PRO_SVK, false>);
+    allow_smem(k_zfwd<TD, PRO_K4, true>);
+    allow_smem(k_zfwd<TD, PRO_SVK, true>);
     allow_smem(k_ypass);
     allow_smem(k_xpass<TD>);
     allow_smem(k_zinv<TD>);
@@ -280,29 +284,32 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   int ls = std::max(ctx->Lz, ctx->nzh);
   if (ls % 2 == 0) ls += 1;  // odd pitch: fewer bank conflicts
   int G = int(std::max<size_t>(1, std::min<size_t>(16, size_t(96 * 1024) / (size_t(2) * NC * ls * 16))));
+  // small grids: spread the z lines over at least two CTAs per SM
+  G = std::min(G, std::max(1, nxy / (2 * 148)));
   G = std::min(G, nxy);
+  const int zthreads = (G * NC * ctx->Nz >= 2048 || G * ctx->Nz >= 256) ? 256 : 128;
   const size_t smz = size_t(2) * NC * G * ls * 16;
   if (smz + 1024 > size_t(kMaxSmem))
     return set_error(ctx, FM_E_UNSUPPORTED, "z line too long for the shared-memory FFT");
   const dim3 gz((nxy + G - 1) / G);
   int TWy, TWx;
-  if (tile_width(ctx->nzh, ctx->Ny, 1, TWy) || tile_width(ctx->nzh, ctx->Nx, TD, TWx))
+  if (tile_width(ctx->nzh, ctx->Ny, 1, TWy, int64_t(ctx->Nx) * NC) || tile_width(ctx->nzh, ctx->Nx, TD, TWx, int64_t(ctx->Ny) * TD))
     return set_error(ctx, FM_E_UNSUPPORTED, "x/y line too long for the shared-memory FFT");
   int st = FM_OK;
   // pass 1: z forward (+ prologue)
   prof_mark(ctx);
   if (!(TD == 3 && zf_fast(ctx, pa, &st))) {
-    switch (pa.kind) {
-      case PRO_COPY:
-        k_zfwd<TD, PRO_COPY><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-        break;
-      case PRO_K4:
-        k_zfwd<TD, PRO_K4><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-        break;
-      default:
-        k_zfwd<TD, PRO_SVK><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-        break;
-    }
+    const bool dir = pa.r != nullptr;
+    if (pa.kind == PRO_COPY)
+      k_zfwd<TD, PRO_COPY, false><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+    else if (pa.kind == PRO_K4 && !dir)
+      k_zfwd<TD, PRO_K4, false><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+    else if (pa.kind == PRO_K4)
+      k_zfwd<TD, PRO_K4, true><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+    else if (!dir)
+      k_zfwd<TD, PRO_SVK, false><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
+    else
+      k_zfwd<TD, PRO_SVK, true><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
     FM_LAUNCHED(ctx);
   } else if (st) {
     return st;
@@ -337,7 +344,7 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   // pass 5: z inverse (c2r), scale
   prof_mark(ctx);
   if (!(TD == 3 && zi_fast(ctx, out, scale / double(ctx->n), epi, &st))) {
-    k_zinv<TD><<<gz, 256, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, ctx->spec, out, G, ls,
+    k_zinv<TD><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, ctx->spec, out, G, ls,
                                               scale / double(ctx->n), epi);
     FM_LAUNCHED(ctx);
     if (nparts) *nparts = int(gz.x);

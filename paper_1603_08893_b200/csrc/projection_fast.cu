@@ -13,6 +13,8 @@
 //   x pass   : one thread holds all 3 components of its row, so the
 //              projection Bhat_i. = (Ahat_i . xi) xi / |xi|^2 is applied in
 //              registers between the forward and inverse x transforms.
+#include <cstdlib>
+
 #include "proj_common.cuh"
 
 namespace fm {
@@ -93,6 +95,70 @@ __global__ void __launch_bounds__(TW*(N / e_x(N)), 2) k_x_fast(Geo g, const doub
     for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[j][m];
 }
 
+// x pass, shared-memory staged variant: the three components of a row are
+// transformed one at a time (E elements per thread in registers), parked in
+// shared memory at the positions the thread owns, projected there, and
+// transformed back -- trading one extra smem round trip for 1/3 of the
+// registers (more CTAs per SM).
+template <int N, int TW, int E>
+__global__ void __launch_bounds__(TW*(N / E)) k_x_fast2(Geo g, const double2* __restrict__ tw,
+                                                       double2* __restrict__ spec) {
+  constexpr int T = N / E;
+  extern __shared__ double2 sm[];
+  const int l = threadIdx.x % TW, t = threadIdx.x / TW;
+  const int kz = blockIdx.x * TW + l;
+  const int y = blockIdx.y, i = blockIdx.z;
+  const int64_t xstride = int64_t(g.Ny) * g.nzh;
+  double2* base = spec + int64_t(i * 3) * N * xstride + int64_t(y) * g.nzh + kz;
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = base[(int64_t(j) * N + t + T * m) * xstride];
+    double2* S = sm + j * N * TW + l;
+    reg::fft<N, E, -1>(v, S, TW, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) S[(t + T * m) * TW] = v[m];
+  }
+  const int qy = freq_of(y, g.Ny), qz = freq_of(kz, g.Nz);
+  const bool nyq_yz = ((g.Ny % 2 == 0) && (y == g.Ny / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+  const double xiy = qy * g.invL[1], xiz = (g.dim == 3) ? qz * g.invL[2] : 0.0;
+#pragma unroll 2
+  for (int m = 0; m < E; ++m) {  // own positions only: no barrier needed
+    const int kx = t + T * m;
+    double2* s0 = sm + kx * TW + l;
+    const double xix = freq_of(kx, N) * g.invL[0];
+    const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
+    const bool nyq = nyq_yz || (kx == N / 2);
+    double2 a0 = s0[0], a1 = s0[N * TW], a2 = s0[2 * N * TW];
+    if (norm2 == 0.0 || (nyq && g.mode == FM_NYQUIST_ZERO_COMPATIBLE)) {
+      a0 = a1 = a2 = make_double2(0.0, 0.0);
+    } else if (!nyq) {
+      const double sx = a0.x * xix + a1.x * xiy + a2.x * xiz;
+      const double sy = a0.y * xix + a1.y * xiy + a2.y * xiz;
+      const double inv = 1.0 / norm2;
+      const double f0 = xix * inv, f1 = xiy * inv, f2 = xiz * inv;
+      a0 = make_double2(sx * f0, sy * f0);
+      a1 = make_double2(sx * f1, sy * f1);
+      a2 = make_double2(sx * f2, sy * f2);
+    }
+    s0[0] = a0;
+    s0[N * TW] = a1;
+    s0[2 * N * TW] = a2;
+  }
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    double2 v[E];
+    double2* S = sm + j * N * TW + l;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = S[(t + T * m) * TW];
+    __syncthreads();  // every thread has its inputs before the exchanges overwrite S
+    reg::fft<N, E, +1>(v, S, TW, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
+  }
+}
+
 // --------------------------------------------------------------- z passes
 // HEAVY: K4 / SVK prologue (720 B read per voxel): larger E, ~144 threads and
 // ~40 KB per CTA so 4 CTAs per SM overlap their load and FFT phases.
@@ -108,7 +174,7 @@ struct ZShape {
   static constexpr size_t SMEM = size_t(M) * LSP * 16;
 };
 
-template <int M, int PRO>
+template <int M, int PRO, bool DIR>
 __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast(Geo g, const double2* __restrict__ twM,
                                                                 const double2* __restrict__ twN,
                                                                 ProArgs pa, double2* __restrict__ spec) {
@@ -124,7 +190,7 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
     const int gi = w / N, z = w - gi * N;
     const int64_t node = int64_t(L0 + gi) * N + z;
     double v[9];
-    prologue_voxel<3, PRO>(pa, g.n, node, v);
+    prologue_voxel<3, PRO, DIR>(pa, g.n, node, v);
 #pragma unroll
     for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] = v[c];
   }
@@ -258,40 +324,68 @@ bool y_launch(fm_ctx* ctx, int sign, int* st) {
   return true;
 }
 
+int x_variant() {
+  static int v = [] {
+    const char* e = getenv("FM_XPASS");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
+template <int N, int E>
+void x2_go(fm_ctx* ctx) {
+  constexpr int TW = 8;
+  constexpr int T = N / E;
+  const size_t smem = size_t(3) * N * TW * 16;
+  static bool a = (allow(k_x_fast2<N, TW, E>, smem), true);
+  (void)a;
+  const Geo g = make_geo(ctx);
+  const dim3 grid(ctx->nzh / TW, ctx->Ny, 3);
+  k_x_fast2<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, ctx->spec);
+}
+
 template <int N>
 bool x_launch(fm_ctx* ctx, int* st) {
   constexpr int TW = tw_x(N);
   constexpr int T = N / e_x(N);
   const size_t smem = size_t(N) * TW * 16;
-  static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
-  (void)a;
-  const Geo g = make_geo(ctx);
-  const dim3 grid(ctx->nzh / TW, ctx->Ny, 3);
-  k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, ctx->spec);
+  const int var = (N <= 512 && ctx->nzh % 8 == 0) ? x_variant() : 1;
+  if (var == 2) {
+    x2_go<N, e_line(N)>(ctx);
+  } else if (var == 3) {
+    x2_go<N, e_x(N)>(ctx);
+  } else {
+    static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
+    (void)a;
+    const Geo g = make_geo(ctx);
+    const dim3 grid(ctx->nzh / TW, ctx->Ny, 3);
+    k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, ctx->spec);
+  }
   ctx->cnt.launches++;
   const cudaError_t e = cudaGetLastError();
   *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_x_fast");
   return true;
 }
 
-template <int M, int PRO>
+template <int M, int PRO, bool DIR>
 void zf_go(fm_ctx* ctx, const ProArgs& pa) {
   using S = ZShape<M, PRO != PRO_COPY>;
-  static bool a = (allow(k_zf_fast<M, PRO>, S::SMEM), true);
+  static bool a = (allow(k_zf_fast<M, PRO, DIR>, S::SMEM), true);
   (void)a;
   const Geo g = make_geo(ctx);
   const int nxy = ctx->Nx * ctx->Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
-  k_zf_fast<M, PRO><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
+  k_zf_fast<M, PRO, DIR><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
 }
 
 template <int M>
 bool zf_launch(fm_ctx* ctx, const ProArgs& pa, int* st) {
-  switch (pa.kind) {
-    case PRO_COPY: zf_go<M, PRO_COPY>(ctx, pa); break;
-    case PRO_K4: zf_go<M, PRO_K4>(ctx, pa); break;
-    default: zf_go<M, PRO_SVK>(ctx, pa); break;
-  }
+  const bool dir = pa.r != nullptr;
+  if (pa.kind == PRO_COPY) zf_go<M, PRO_COPY, false>(ctx, pa);
+  else if (pa.kind == PRO_K4 && !dir) zf_go<M, PRO_K4, false>(ctx, pa);
+  else if (pa.kind == PRO_K4) zf_go<M, PRO_K4, true>(ctx, pa);
+  else if (!dir) zf_go<M, PRO_SVK, false>(ctx, pa);
+  else zf_go<M, PRO_SVK, true>(ctx, pa);
   ctx->cnt.launches++;
   const cudaError_t e = cudaGetLastError();
   *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_zf_fast");
