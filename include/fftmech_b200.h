@@ -102,6 +102,28 @@ int fm_ctx_profile_read(fm_ctx* ctx, double* ms /* 5 */, int64_t* calls);
 /* Number of this library's kernels launched on the context so far. */
 int64_t fm_ctx_launch_count(const fm_ctx* ctx);
 
+/* ---- slab decomposition ---------------------------------
+ * Rank r of P owns x-planes [r Nx/P, (r+1) Nx/P) of every field; the
+ * projection runs its z/y passes on the x-slab and its x pass on the y-slab,
+ * with two all-to-alls (grouped ncclSend/ncclRecv over NVLink) in between.
+ * Nx and Ny must be divisible by P; CG scalars are combined across ranks in
+ * rank order (deterministic). */
+/* One rank per device.  `points` is the GLOBAL grid; fields created on this
+ * context hold the local slab (Nx/P * Ny * Nz nodes per component).
+ * nccl_unique_id: the 128-byte id from fm_nccl_unique_id on rank 0. */
+int fm_ctx_create_dist(int dim, const int32_t* points, const double* lengths, int tdim, int nyquist_mode,
+                       int device, int nranks, int rank, const void* nccl_unique_id, fm_ctx** out);
+int fm_nccl_unique_id(void* out, int bytes);
+/* Virtual ranks: run all P slab ranks on this one device (the all-to-all is
+ * a device copy) -- validates the decomposition against P = 1 bit for bit. */
+int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P);
+int fm_ctx_ranks(const fm_ctx* ctx, int* nranks, int* rank, int* virtual_mode);
+/* Transpose plan (host only, no device needed): complex-element offsets of
+ * the (src -> dst, component) chunk in src's packed buffer B and in dst's
+ * x-pass buffer A, and its length. */
+int fm_dist_chunk(int P, int Nx, int Ny, int nzh, int ncomp, int src, int dst, int comp, int64_t* b_off,
+                  int64_t* a_off, int64_t* count);
+
 /* ---- fields -------------------------------------------------------------- */
 int fm_field_alloc(fm_ctx* ctx, int ncomp, fm_field** out);
 int fm_field_free(fm_ctx* ctx, fm_field* f);

@@ -109,7 +109,32 @@ _SIGS = {
     "fm_model_set_history": (C.c_int, [_P, _P, _P, _P, _P]),
     "fm_model_apply": (C.c_int, [_P, _P, _P, _P]),
     "fm_solve_increment": (C.c_int, [_P, _P, _P, _dp, C.POINTER(SolverParams), C.POINTER(Report), _P]),
+    "fm_ctx_create_dist": (C.c_int, [C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double), C.c_int, C.c_int,
+                                     C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_P)]),
+    "fm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
+    "fm_ctx_set_virtual_ranks": (C.c_int, [_P, C.c_int]),
+    "fm_ctx_ranks": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "fm_dist_chunk": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it and shares it, e.g. via torch.distributed)."""
+    buf = C.create_string_buffer(128)
+    st = lib().fm_nccl_unique_id(buf, 128)
+    if st != FM_OK:
+        raise FmError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def dist_chunk(P, Nx, Ny, nzh, ncomp, src, dst, comp):
+    """Transpose plan of the slab decomposition (host only): (b_off, a_off, count)."""
+    b, a, n = C.c_int64(), C.c_int64(), C.c_int64()
+    st = lib().fm_dist_chunk(P, Nx, Ny, nzh, ncomp, src, dst, comp, C.byref(b), C.byref(a), C.byref(n))
+    if st != FM_OK:
+        raise FmError(st, "fm_dist_chunk")
+    return b.value, a.value, n.value
 
 
 def declared_symbols():
@@ -144,19 +169,34 @@ class Context:
     """fm_ctx: grid + FFT plans + workspace on one device (replaces
     ProjectionOperator / build_projection, projection.hpp:40-66)."""
 
-    def __init__(self, points, tdim=None, lengths=None, nyquist_mode=0, device=0):
+    def __init__(self, points, tdim=None, lengths=None, nyquist_mode=0, device=0, dist=None):
+        """dist = (nranks, rank, nccl_unique_id): one slab rank per device; fields
+        then hold this rank's x-slab (Nx/nranks planes)."""
         L = lib()
         dim, pts, ln = _grid(points, lengths)
         self.points = tuple(points)
         self.tdim = tdim if tdim is not None else dim
-        self.n = int(np.prod(points))
         self.ncomp = self.tdim * self.tdim
         h = _P()
-        st = L.fm_ctx_create(dim, pts, ln, self.tdim, nyquist_mode, device, C.byref(h))
+        if dist is None:
+            st = L.fm_ctx_create(dim, pts, ln, self.tdim, nyquist_mode, device, C.byref(h))
+        else:
+            nranks, rank, uid = dist
+            st = L.fm_ctx_create_dist(dim, pts, ln, self.tdim, nyquist_mode, device, nranks, rank, uid, C.byref(h))
         if st != FM_OK:
             raise FmError(st, "fm_ctx_create failed (is a CUDA device visible?)")
         self.h = h
+        self.n = int(L.fm_ctx_nodes(h))  # nodes held here (the local slab when distributed)
         self._fields = []
+
+    def set_virtual_ranks(self, P):
+        """Run the slab-decomposed projection with P ranks emulated on this device."""
+        self.check(lib().fm_ctx_set_virtual_ranks(self.h, P))
+
+    def ranks(self):
+        nr, r, v = C.c_int(), C.c_int(), C.c_int()
+        self.check(lib().fm_ctx_ranks(self.h, C.byref(nr), C.byref(r), C.byref(v)))
+        return nr.value, r.value, bool(v.value)
 
     def close(self):
         if getattr(self, "h", None):

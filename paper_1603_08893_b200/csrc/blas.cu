@@ -59,6 +59,21 @@ __global__ void __launch_bounds__(kRedThreads) k_sum_comp_partial(const double* 
   if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
 }
 
+// CG scalar logic on the (globally summed) value s.
+__device__ __forceinline__ void cg_scalar_op(double* scal, int op, double s) {
+  if (op == 1) {  // solver.cpp:37-45
+    scal[S_PAP] = s;
+    const bool bad = !(s > 0.0);
+    scal[S_FLAG] = bad ? 1.0 : 0.0;
+    scal[S_ALPHA] = bad ? 0.0 : scal[S_RR] / s;
+  } else if (op == 2) {  // solver.cpp:48-53
+    if (scal[S_FLAG] != 0.0) return;
+    scal[S_RRNEW] = s;
+    scal[S_BETA] = s / scal[S_RR];
+    scal[S_RR] = s;
+  }
+}
+
 // op: 0 -> out[slot + comp] = sum;  1 -> CG pAp step;  2 -> CG rr_new step
 __global__ void __launch_bounds__(kRedThreads) k_finalize(const double* __restrict__ partial,
                                                           int nb, double* scal, int op, int slot) {
@@ -67,20 +82,14 @@ __global__ void __launch_bounds__(kRedThreads) k_finalize(const double* __restri
   for (int i = threadIdx.x; i < nb; i += blockDim.x) s += p[i];
   s = block_sum(s);
   if (threadIdx.x != 0) return;
-  if (op == 0) {
+  if (op == 0)
     scal[slot + blockIdx.x] = s;
-  } else if (op == 1) {  // solver.cpp:37-45
-    scal[S_PAP] = s;
-    const bool bad = !(s > 0.0);
-    scal[S_FLAG] = bad ? 1.0 : 0.0;
-    scal[S_ALPHA] = bad ? 0.0 : scal[S_RR] / s;
-  } else {  // solver.cpp:48-53
-    if (scal[S_FLAG] != 0.0) return;
-    scal[S_RRNEW] = s;
-    scal[S_BETA] = s / scal[S_RR];
-    scal[S_RR] = s;
-  }
+  else
+    cg_scalar_op(scal, op, s);
 }
+
+// distributed: the CG op applied after the cross-rank combination of scal[slot]
+__global__ void k_scalar_op(double* scal, int op, int slot) { cg_scalar_op(scal, op, scal[slot]); }
 
 // x += alpha p; r -= alpha Ap; partial <r,r>   (solver.cpp:46-48)
 __global__ void __launch_bounds__(kRedThreads) k_cg_update(double* __restrict__ x,
@@ -167,12 +176,28 @@ static int ew_blocks(int64_t count) {
   return int(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
 }
 
+// Finalise a reduction whose block partials are in `partial`: op 0 stores the
+// sum in scal[slot]; op 1/2 run the CG scalar step on it.  Distributed: the
+// local sum is combined across ranks (ordered) before the op is applied.
+static int finalize(fm_ctx* ctx, const double* partial, int nb, double* scal, int op, int slot) {
+  if (!distributed(ctx) || op == 0) {
+    k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(partial, nb, scal, op, slot);
+    FM_LAUNCHED(ctx);
+    return op == 0 ? combine_ranks(ctx, scal + slot, 1) : FM_OK;
+  }
+  constexpr int kLocal = 40;  // scratch slot for the local value
+  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(partial, nb, scal, 0, kLocal);
+  FM_LAUNCHED(ctx);
+  if (int st = combine_ranks(ctx, scal + kLocal, 1)) return st;
+  k_scalar_op<<<1, 1, 0, ctx->stream>>>(scal, op, kLocal);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
 int dot_async(fm_ctx* ctx, const double* a, const double* b, int64_t count, double* d_out) {
   k_dot_partial<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(a, b, count, ctx->d_partial);
   FM_LAUNCHED(ctx);
-  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, ctx->red_blocks, d_out, 0, 0);
-  FM_LAUNCHED(ctx);
-  return FM_OK;
+  return finalize(ctx, ctx->d_partial, ctx->red_blocks, d_out, 0, 0);
 }
 
 int sum_comp_async(fm_ctx* ctx, const double* a, int ncomp, int64_t n, double* d_out) {
@@ -181,7 +206,7 @@ int sum_comp_async(fm_ctx* ctx, const double* a, int ncomp, int64_t n, double* d
   FM_LAUNCHED(ctx);
   k_finalize<<<ncomp, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, nb, d_out, 0, 0);
   FM_LAUNCHED(ctx);
-  return FM_OK;
+  return combine_ranks(ctx, d_out, ncomp);
 }
 
 int axpy_async(fm_ctx* ctx, double a, const double* x, double* y, int64_t count) {
@@ -228,9 +253,7 @@ int cg_update_async(fm_ctx* ctx, double* x, double* r, const double* p, const do
   k_cg_update<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(x, r, p, Ap, count, ctx->d_scal,
                                                                 ctx->d_partial);
   FM_LAUNCHED(ctx);
-  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, ctx->red_blocks, ctx->d_scal, 2, 0);
-  FM_LAUNCHED(ctx);
-  return FM_OK;
+  return finalize(ctx, ctx->d_partial, ctx->red_blocks, ctx->d_scal, 2, 0);
 }
 
 int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count) {
@@ -241,18 +264,14 @@ int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count) {
 
 // <p,Ap> from the partials the fused z-inverse epilogue wrote (solver.cpp:37-45)
 int cg_pap_finalize_async(fm_ctx* ctx, int n_partials) {
-  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_epi, n_partials, ctx->d_scal, 1, 0);
-  FM_LAUNCHED(ctx);
-  return FM_OK;
+  return finalize(ctx, ctx->d_epi, n_partials, ctx->d_scal, 1, 0);
 }
 
 // pAp finalisation used by the CG driver
 int cg_pap_async(fm_ctx* ctx, const double* p, const double* Ap, int64_t count) {
   k_dot_partial<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(p, Ap, count, ctx->d_partial);
   FM_LAUNCHED(ctx);
-  k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, ctx->red_blocks, ctx->d_scal, 1, 0);
-  FM_LAUNCHED(ctx);
-  return FM_OK;
+  return finalize(ctx, ctx->d_partial, ctx->red_blocks, ctx->d_scal, 1, 0);
 }
 
 }  // namespace fm

@@ -116,6 +116,8 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
   ctx->Ny = ctx->pts[1];
   ctx->Nz = ctx->pts[2];
   ctx->n = int64_t(ctx->Nx) * ctx->Ny * ctx->Nz;
+  ctx->n_global = ctx->n;
+  ctx->n_local_stride = ctx->n;
   const bool even = ctx->Nz % 2 == 0;
   ctx->nzh = (even && nyquist_mode == FM_NYQUIST_ZERO_COMPATIBLE) ? ctx->Nz / 2 : ctx->Nz / 2 + 1;
   ctx->Lz = even ? ctx->Nz / 2 : ctx->Nz;
@@ -145,12 +147,13 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
   ctx->pzh.tw = ctx->d_tw + ozh;
   const size_t spec_elems = size_t(ctx->ncomp) * ctx->Nx * ctx->Ny * ctx->nzh;
   if (cudaMalloc(&ctx->spec, spec_elems * sizeof(double2)) != cudaSuccess) return fail(FM_E_OOM);
+  ctx->spec_rank_elems = int64_t(spec_elems);
   const int64_t half = (ctx->n * ctx->ncomp) / 2;
   int64_t rb = (half + 255) / 256;
   ctx->red_blocks = int(rb < 1 ? 1 : (rb > 148 * 4 ? 148 * 4 : rb));
   if (cudaMalloc(&ctx->d_partial, sizeof(double) * (ctx->red_blocks + 16) * 16) != cudaSuccess)
     return fail(FM_E_OOM);
-  ctx->epi_cap = int64_t(ctx->Nx) * ctx->Ny + 1;
+  ctx->epi_cap = int64_t(ctx->Nx) * ctx->Ny + 64;
   if (cudaMalloc(&ctx->d_epi, sizeof(double) * ctx->epi_cap) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMalloc(&ctx->d_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMemset(ctx->d_scal, 0, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_CUDA);
@@ -170,11 +173,14 @@ int fm_ctx_destroy(fm_ctx* ctx) {
   release_field(ctx->tmp);
   release_field(ctx->rhs);
   release_field(ctx->dF);
-  release_field(ctx->P);
+  release_field(ctx->Pw);
   if (ctx->d_tw) cudaFree(ctx->d_tw);
   if (ctx->spec) cudaFree(ctx->spec);
   if (ctx->d_partial) cudaFree(ctx->d_partial);
   if (ctx->d_epi) cudaFree(ctx->d_epi);
+  if (ctx->spec2) cudaFree(ctx->spec2);
+  if (ctx->d_gather) cudaFree(ctx->d_gather);
+  dist_destroy(ctx);
   if (ctx->d_scal) cudaFree(ctx->d_scal);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
   if (ctx->d_bad) cudaFree(ctx->d_bad);
@@ -183,6 +189,68 @@ int fm_ctx_destroy(fm_ctx* ctx) {
   for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
+  return FM_OK;
+}
+
+// ---- slab decomposition ----------------------------------------------------
+static int setup_slabs(fm_ctx* ctx, int P) {
+  if (P < 1 || ctx->Nx % P || ctx->Ny % P)
+    return set_error(ctx, FM_E_UNSUPPORTED, "slab decomposition needs Nx and Ny divisible by the rank count");
+  ctx->P = P;
+  ctx->spec_rank_elems = int64_t(ctx->ncomp) * (ctx->Nx / P) * ctx->Ny * ctx->nzh;
+  if (P > 1 && !ctx->spec2) {
+    const size_t bytes = size_t(ctx->spec_rank_elems) * (ctx->virt ? P : 1) * sizeof(double2);
+    FM_CUDA(ctx, cudaMalloc(&ctx->spec2, bytes));
+  }
+  if (!ctx->d_gather) FM_CUDA(ctx, cudaMalloc(&ctx->d_gather, sizeof(double) * 64 * size_t(P)));
+  return FM_OK;
+}
+
+int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P) {
+  if (!ctx || P < 1) return FM_E_INVALID;
+  if (ctx->nccl) return set_error(ctx, FM_E_INVALID, "context is distributed over devices");
+  ctx->virt = P > 1;
+  if (P == 1) {
+    ctx->P = 1;
+    ctx->spec_rank_elems = int64_t(ctx->ncomp) * ctx->Nx * ctx->Ny * ctx->nzh;
+    return FM_OK;
+  }
+  return setup_slabs(ctx, P);
+}
+
+int fm_ctx_create_dist(int dim, const int32_t* points, const double* lengths, int tdim, int nyquist_mode,
+                       int device, int nranks, int rank, const void* nccl_unique_id, fm_ctx** out) {
+  if (!out || !nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks || !points) return FM_E_INVALID;
+  if (nranks == 1) return fm_ctx_create(dim, points, lengths, tdim, nyquist_mode, device, out);
+  if (dim != 3 || points[0] % nranks || points[1] % nranks) return FM_E_UNSUPPORTED;
+  // the context is created for the whole grid (plans, workspace sized per slab below)
+  int st = fm_ctx_create(dim, points, lengths, tdim, nyquist_mode, device, out);
+  if (st) return st;
+  fm_ctx* ctx = *out;
+  ctx->rank = rank;
+  ctx->n_global = ctx->n;
+  ctx->n = ctx->n_global / nranks;  // local x-slab: fields hold n_local nodes
+  ctx->n_local_stride = ctx->n;
+  ctx->node_offset = int64_t(rank) * ctx->n;
+  // re-size the per-rank workspace: A and B hold one slab's spectrum each
+  cudaFree(ctx->spec);
+  ctx->spec = nullptr;
+  const size_t rank_elems = size_t(ctx->ncomp) * (ctx->Nx / nranks) * ctx->Ny * ctx->nzh;
+  if (cudaMalloc(&ctx->spec, rank_elems * sizeof(double2)) != cudaSuccess) st = FM_E_OOM;
+  if (!st) st = dist_init_nccl(ctx, nccl_unique_id, nranks, rank);
+  if (!st) st = setup_slabs(ctx, nranks);
+  if (st) {
+    fm_ctx_destroy(ctx);
+    *out = nullptr;
+  }
+  return st;
+}
+
+int fm_ctx_ranks(const fm_ctx* ctx, int* nranks, int* rank, int* virtual_mode) {
+  if (!ctx) return FM_E_INVALID;
+  if (nranks) *nranks = ctx->P;
+  if (rank) *rank = ctx->rank;
+  if (virtual_mode) *virtual_mode = ctx->virt ? 1 : 0;
   return FM_OK;
 }
 
@@ -351,7 +419,7 @@ int fm_mean(fm_ctx* ctx, const fm_field* a, double* out) {
   if (!ctx || !a || !out || a->ncomp > 9) return set_error(ctx, FM_E_INVALID, "mean: bad field");
   if (int st = sum_comp_async(ctx, a->d, a->ncomp, a->n, ctx->d_scal + 16)) return st;
   if (int st = fetch_scalars(ctx, 16 + a->ncomp)) return st;
-  for (int c = 0; c < a->ncomp; ++c) out[c] = ctx->h_scal[16 + c] / double(a->n);
+  for (int c = 0; c < a->ncomp; ++c) out[c] = ctx->h_scal[16 + c] / double(ctx->n_global);
   return FM_OK;
 }
 

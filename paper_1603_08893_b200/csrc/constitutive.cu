@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(128) k_hyper(int64_t n, const double* __restri
                                                const double* __restrict__ lam_f,
                                                const double* __restrict__ mu_f,
                                                double* __restrict__ P, double* __restrict__ K,
-                                               unsigned long long* bad) {
+                                               unsigned long long* bad, int64_t noff) {
   constexpr int NC = TD * TD;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
        q += int64_t(gridDim.x) * blockDim.x) {
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(128) k_hyper(int64_t n, const double* __restri
     for (int c = 0; c < NC; ++c) f[c] = __ldg(F + c * n + q);
     const double lam = __ldg(lam_f + q), g = __ldg(mu_f + q);
     if (det_t<TD>(f) <= 0.0) {
-      report_bad(bad, nullptr, q, FM_E_INVERTED, 0.0);
+      report_bad(bad, nullptr, noff + q, FM_E_INVERTED, 0.0);
       continue;
     }
     double trE = 0.0;
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restric
                                               double* __restrict__ P, double* __restrict__ K,
                                               double* __restrict__ be_t,
                                               double* __restrict__ epsp_t,
-                                              unsigned long long* bad, double* badval) {
+                                              unsigned long long* bad, double* badval, int64_t noff) {
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
        q += int64_t(gridDim.x) * blockDim.x) {
     const double lam = __ldg(lam_f + q), g = __ldg(mu_f + q), ty0 = __ldg(ty0_f + q),
@@ -207,11 +207,11 @@ __global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restric
         Fo[c] = __ldg(Fold + c * n + q);
       }
       if (det_t<3>(Fm) <= 0.0) {
-        report_bad(bad, badval, q, FM_E_INVERTED, 0.0);
+        report_bad(bad, badval, noff + q, FM_E_INVERTED, 0.0);
         continue;
       }
       if (!inv3(Fm, Finv) || !inv3(Fo, Foinv)) {
-        report_bad(bad, badval, q, FM_E_SINGULAR, 0.0);
+        report_bad(bad, badval, noff + q, FM_E_SINGULAR, 0.0);
         continue;
       }
 #pragma unroll
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restric
     double lb[3], V[9];
     sym_eig3(bsym, lb, V);
     if (lb[0] < 1e-30 || lb[1] < 1e-30 || lb[2] < 1e-30) {  // kMinLogEigenvalue
-      report_bad(bad, badval, q, FM_E_NOT_SPD, lb[0] < 1e-30 ? lb[0] : (lb[1] < 1e-30 ? lb[1] : lb[2]));
+      report_bad(bad, badval, noff + q, FM_E_NOT_SPD, lb[0] < 1e-30 ? lb[0] : (lb[1] < 1e-30 ? lb[1] : lb[2]));
       continue;
     }
     double eps[3], tau_d[3], dev[3];
@@ -364,6 +364,7 @@ int reset_bad(fm_ctx* ctx) {
 }
 
 int check_bad(fm_ctx* ctx) {
+  if (int st = combine_min_u64(ctx, ctx->d_bad)) return st;  // lowest offending node over all ranks
   unsigned long long key = 0;
   double val = 0.0;
   FM_CUDA(ctx, cudaMemcpyAsync(&key, ctx->d_bad, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream));
@@ -391,9 +392,9 @@ int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const doub
   if (int st = reset_bad(ctx)) return st;
   const int blocks = grid_for(ctx->n, 128);
   if (ctx->tdim == 3)
-    k_hyper<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad);
+    k_hyper<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
   else
-    k_hyper<2><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad);
+    k_hyper<2><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
   FM_LAUNCHED(ctx);
   return FM_OK;
 }
@@ -405,7 +406,7 @@ int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const doub
   if (int st = reset_bad(ctx)) return st;
   const int blocks = grid_for(ctx->n, 128);
   k_simo<<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K,
-                                          be_t, epsp_t, ctx->d_bad, ctx->d_badval);
+                                          be_t, epsp_t, ctx->d_bad, ctx->d_badval, ctx->node_offset);
   FM_LAUNCHED(ctx);
   return FM_OK;
 }

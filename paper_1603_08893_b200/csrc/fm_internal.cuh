@@ -72,7 +72,9 @@ struct fm_ctx {
   int pts[3] = {1, 1, 1};
   double len[3] = {1, 1, 1};
   int tdim = 3, ncomp = 9;
-  int64_t n = 0;
+  int64_t n = 0;         // nodes held by this context (the local slab when distributed)
+  int64_t n_global = 0;  // nodes of the whole grid (1/n of the transform, means, CG cap)
+  int64_t node_offset = 0;  // global index of local node 0 (error reports)
   int mode = 0;
   int Nx = 1, Ny = 1, Nz = 1;
   int nzh = 1;  // stored kz columns
@@ -81,7 +83,15 @@ struct fm_ctx {
   cudaStream_t stream = nullptr;
   fm::AxisPlan px, py, pz, pzh;  // pzh: half-length plan for even-Nz r2c
   double2* d_tw = nullptr;        // all twiddle tables
-  double2* spec = nullptr;        // ncomp * Nx * Ny * nzh
+  double2* spec = nullptr;        // ncomp * Nx * Ny * nzh  (A: z/y side; also the x-pass buffer)
+  double2* spec2 = nullptr;       // packed all-to-all staging (B), only when P > 1
+  // slab decomposition over P ranks; P = 1: single device
+  int P = 1, rank = 0;
+  bool virt = false;              // all P ranks emulated on this one device
+  int64_t n_local_stride = 0;     // component stride of real fields (n, or n_local when distributed)
+  int64_t spec_rank_elems = 0;    // complex elements of one rank's spectral buffer
+  void* nccl = nullptr;           // ncclComm_t when distributed over devices
+  double* d_gather = nullptr;     // all-gather staging of per-rank scalars
   // reductions
   int red_blocks = 0;
   double* d_partial = nullptr;  // red_blocks * 16
@@ -92,7 +102,7 @@ struct fm_ctx {
   unsigned long long* d_bad = nullptr;  // lowest offending node (atomicMin)
   double* d_badval = nullptr;
   // CG workspace (allocated lazily, tdim^2 components each)
-  fm_field r, p, Ap, tmp, rhs, dF, P;
+  fm_field r, p, Ap, tmp, rhs, dF, Pw;  // Pw: the stress workspace
   fm::Counters cnt;
   fm::PassProfile prof;
   std::string last_error;
@@ -144,6 +154,14 @@ struct EpiArgs {
 int projection_run(fm_ctx* ctx, const ProArgs& args, double* out, double scale,
                    const EpiArgs& epi = EpiArgs{}, int* n_partials = nullptr);
 int profile_collect(fm_ctx* ctx);
+// dist.cu: the slab all-to-all (dir +1: packed B -> x-pass A, -1: back)
+int transpose(fm_ctx* ctx, int dir);
+// Ordered cross-rank sum of `count` device scalars (no-op unless distributed).
+int combine_ranks(fm_ctx* ctx, double* d_vals, int count);
+int combine_min_u64(fm_ctx* ctx, unsigned long long* d_key);
+int dist_init_nccl(fm_ctx* ctx, const void* unique_id, int nranks, int rank);
+void dist_destroy(fm_ctx* ctx);
+inline bool distributed(const fm_ctx* ctx) { return ctx->nccl != nullptr && ctx->P > 1; }
 
 // blas.cu -------------------------------------------------------------------
 int dot_async(fm_ctx* ctx, const double* a, const double* b, int64_t count, double* d_out);

@@ -6,11 +6,28 @@
 
 namespace fm {
 
+// Geometry one pass sees.  Single device: the whole grid.  Slab rank r of P
+// (SURVEY.md §8(e)): z / y passes see the x-slab (Nx = Nx_global / P, all y,
+// all z); the x pass sees all x for its y-slab (Ny = Ny_global / P, y0 = r Ny).
 struct Geo {
   int Nx, Ny, Nz, nzh, Lz, dim, mode;
-  int64_t n;
+  int64_t n;     // component stride of real fields
+  int64_t roff;  // node offset of this slab inside the real fields
   double invL[3];
+  int P, Yl;     // y passes: ranks and y per rank (packed transpose layout)
+  int y0, Nyg;   // x pass: global y of local y = 0, global Ny (frequencies)
 };
+
+// Spectral layouts.  std: [c][x][y][kz].  packed (y-pass side of the
+// all-to-all): [dst][c][x][yl][kz], dst = y / Yl, so the block bound for
+// each destination rank is contiguous.  P = 1 makes both identical.
+__device__ __forceinline__ int64_t spec_std(const Geo& g, int c, int x, int y, int kz) {
+  return ((int64_t(c) * g.Nx + x) * g.Ny + y) * g.nzh + kz;
+}
+__device__ __forceinline__ int64_t spec_packed(const Geo& g, int NC, int c, int x, int y, int kz) {
+  const int dst = y / g.Yl, yl = y - dst * g.Yl;
+  return (((int64_t(dst) * NC + c) * g.Nx + x) * g.Yl + yl) * g.nzh + kz;
+}
 
 __device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) ? i : i - n; }
 
@@ -128,17 +145,51 @@ inline Geo make_geo(const fm_ctx* ctx) {
   g.dim = ctx->dim;
   g.mode = ctx->mode;
   g.n = ctx->n;
+  g.roff = 0;
   for (int a = 0; a < 3; ++a) g.invL[a] = 1.0 / ctx->len[a];
+  g.P = 1;
+  g.Yl = ctx->Ny;
+  g.y0 = 0;
+  g.Nyg = ctx->Ny;
+  return g;
+}
+// z and y passes of slab rank r: local x-slab, all y and z.
+inline Geo geo_zy(const fm_ctx* ctx, int r) {
+  Geo g = make_geo(ctx);
+  g.P = ctx->P;
+  g.Nx = ctx->Nx / ctx->P;
+  g.Yl = ctx->Ny / ctx->P;
+  g.roff = ctx->virt ? int64_t(r) * g.Nx * ctx->Ny * ctx->Nz : 0;
+  g.n = ctx->n_local_stride;
+  return g;
+}
+// Spectral buffers of slab rank r: A (z/y side, reused in place by the x pass,
+// [c][x][yl][kz] after the transpose) and B (packed all-to-all staging).  One
+// rank per device when distributed; all P ranks side by side in the virtual
+// mode.  P = 1: B == A (the y passes run in place).
+inline double2* spec_a(fm_ctx* ctx, int r) {
+  return ctx->spec + (ctx->virt ? int64_t(r) * ctx->spec_rank_elems : 0);
+}
+inline double2* spec_b(fm_ctx* ctx, int r) {
+  if (ctx->P == 1) return ctx->spec;
+  return ctx->spec2 + (ctx->virt ? int64_t(r) * ctx->spec_rank_elems : 0);
+}
+// x pass of slab rank r: all x, local y-slab.
+inline Geo geo_x(const fm_ctx* ctx, int r) {
+  Geo g = make_geo(ctx);
+  g.Ny = ctx->Ny / ctx->P;
+  g.y0 = r * g.Ny;
   return g;
 }
 
 
 // Pass launchers of the register-resident path (projection_fast.cu); each
 // returns true when it launched (false: no fast kernel for this shape).
-bool zf_fast(fm_ctx* ctx, const ProArgs& pa, int* st);
-bool y_fast(fm_ctx* ctx, int sign, int* st);
-bool x_fast(fm_ctx* ctx, int* st);
-bool zi_fast(fm_ctx* ctx, double* out, double scale, const EpiArgs& epi, int* st);
-int zi_fast_blocks(const fm_ctx* ctx);  // partial sums the fast z-inverse writes
+bool zf_fast(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int* st);
+bool y_fast(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st);
+bool x_fast(fm_ctx* ctx, const Geo& g, double2* spec, int* st);
+bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
+             int* st);
+int zi_fast_blocks(const fm_ctx* ctx, const Geo& g);  // partial sums the fast z-inverse writes
 
 }  // namespace fm

@@ -6,19 +6,25 @@
 // (projection.cpp:87-104, 72 B/voxel) replaced by an analytic evaluation
 // from the wave vector inside the x pass:
 //   pass 1  z  : prologue (copy | K:dF^T | SVK action) + real-to-complex FFT
-//   pass 2  y  : forward complex FFT
+//   pass 2  y  : forward complex FFT (writes the all-to-all packed layout)
 //   pass 3  x  : forward FFT, Bhat_i. = (Ahat_i . xi) xi / |xi|^2, inverse FFT
-//   pass 4  y  : inverse complex FFT
+//   pass 4  y  : inverse complex FFT (reads the packed layout)
 //   pass 5  z  : complex-to-real inverse FFT, scale 1/n
 // ghat(-q) = ghat(q) and the Nyquist set is symmetric, so the half spectrum
-// is exact; the discarded imaginary part of the reference's
-// c2c round trip (projection.cpp:157-169) is identically zero here.
+// is exact; the imaginary residue the reference checks
+// (projection.cpp:157-169) is dropped exactly as its Re() does.
+//
+// Slab decomposition over P ranks: passes 1-2 and 4-5 run
+// on x-slabs, pass 3 on y-slabs, with the all-to-all between them (dist.cu).
+// This file holds the generic kernels (any line length, tdim 2 or 3) and the
+// pass dispatcher; projection_fast.cu the register-resident ones.
 #include <algorithm>
 
 #include "proj_common.cuh"
 
 namespace fm {
 
+// ------------------------------------------------------------------ pass 1
 template <int TD, int PRO, bool DIR>
 __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double2* __restrict__ twN,
                                               ProArgs pa, double2* __restrict__ spec, int G, int ls) {
@@ -32,7 +38,7 @@ __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double
   const bool even = (g.Nz % 2 == 0);
   for (int w = threadIdx.x; w < Gb * g.Nz; w += blockDim.x) {
     const int gi = w / g.Nz, z = w - gi * g.Nz;
-    const int64_t node = int64_t(L0 + gi) * g.Nz + z;
+    const int64_t node = g.roff + int64_t(L0 + gi) * g.Nz + z;
     double v[NC];
     prologue_voxel<TD, PRO, DIR>(pa, g.n, node, v);
 #pragma unroll
@@ -68,26 +74,29 @@ __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double
 }
 
 // -------------------------------------------------------------- pass 2 / 4
-__global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, double2* __restrict__ spec,
-                                               int TW, int sign) {
+// sign -1: std in -> packed out (forward); +1: packed in -> std out.
+__global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, const double2* in,
+                                               double2* out, int TW, int sign) {  // in == out when P = 1
   extern __shared__ double2 sm[];
   const int kz0 = blockIdx.x * TW;
-  const int x = blockIdx.y, c = blockIdx.z;
+  const int x = blockIdx.y, c = blockIdx.z, NC = gridDim.z;
   const int Ny = g.Ny;
   double2* A = sm;
   double2* B = sm + Ny * TW;
-  double2* base = spec + (int64_t(c) * g.Nx + x) * Ny * g.nzh;
   for (int w = threadIdx.x; w < Ny * TW; w += blockDim.x) {
     const int e = w / TW, t = w - e * TW;
     const int kz = kz0 + t;
-    A[w] = kz < g.nzh ? base[int64_t(e) * g.nzh + kz] : make_double2(0.0, 0.0);
+    if (kz < g.nzh)
+      A[w] = in[sign < 0 ? spec_std(g, c, x, e, kz) : spec_packed(g, NC, c, x, e, kz)];
+    else
+      A[w] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   double2* R = fft_smem(A, B, TW, 1, TW, plan, sign, true);
   for (int w = threadIdx.x; w < Ny * TW; w += blockDim.x) {
     const int e = w / TW, t = w - e * TW;
     const int kz = kz0 + t;
-    if (kz < g.nzh) base[int64_t(e) * g.nzh + kz] = R[w];
+    if (kz < g.nzh) out[sign < 0 ? spec_packed(g, NC, c, x, e, kz) : spec_std(g, c, x, e, kz)] = R[w];
   }
 }
 
@@ -114,8 +123,9 @@ __global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __
   double2* R = fft_smem(A, B, nl, 1, nl, plan, -1, true);
   double2* S = (R == A) ? B : A;
   // Bhat_ij = sum_l Ahat_il ghat_lj, ghat = xi (x) xi / |xi|^2 (projection.cpp:87-104,139-152)
-  const int qy = freq_of(y, g.Ny);
-  const bool ny_y = (g.Ny % 2 == 0) && (y == g.Ny / 2);
+  const int yg = g.y0 + y;
+  const int qy = freq_of(yg, g.Nyg);
+  const bool ny_y = (g.Nyg % 2 == 0) && (yg == g.Nyg / 2);
   for (int w = threadIdx.x; w < Nx * TW; w += blockDim.x) {
     const int e = w / TW, t = w - e * TW;
     const int kz = kz0 + t;
@@ -183,7 +193,7 @@ __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double
     const double2* X = A + (c * G + gi) * ls;
     double2 Z;
     if (even) {
-      // Z[k] = (X[k] + X*[M-k]) + i W_N^{-k} (X[k] - X*[M-k]); X[M] = 0 when not stored
+      // Z[k] = (X[k] + X*[M-k]) + i W_N^{-k} (X[k] - X*[M-k]); X[M] = 0 when not stored.
       // Re(ifft) as the reference takes it (projection.cpp:157-162): the kz = 0
       // and kz = M columns of a real field are real, so their (round-off)
       // imaginary parts are dropped, not folded into the output.
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double
     } else {
       v = Zl[z].x;
     }
-    const int64_t idx = int64_t(c) * g.n + int64_t(L0 + gi) * g.Nz + z;
+    const int64_t idx = int64_t(c) * g.n + g.roff + int64_t(L0 + gi) * g.Nz + z;
     out[idx] = v * scale;
     if (epi.partial) dot += __ldg(epi.pdot + idx) * (v * scale);
   }
@@ -244,7 +254,30 @@ int tile_width(int nzh, int N, int lines_per_col, int& TW, int64_t other_blocks)
   return size_t(2) * N * TW * lines_per_col * 16 <= size_t(kMaxSmem) ? 0 : -1;
 }
 
-cudaEvent_t prof_event(fm_ctx* ctx) {
+// Launch shape of the generic z passes for a (slab) geometry.
+struct ZLaunch {
+  int G, ls, threads;
+  size_t smem;
+  dim3 grid;
+};
+
+ZLaunch z_launch(const fm_ctx* ctx, const Geo& g) {
+  const int NC = ctx->ncomp;
+  const int nxy = g.Nx * g.Ny;
+  ZLaunch L;
+  L.ls = std::max(ctx->Lz, ctx->nzh);
+  if (L.ls % 2 == 0) L.ls += 1;  // odd pitch: fewer bank conflicts
+  int G = int(std::max<size_t>(1, std::min<size_t>(16, size_t(96 * 1024) / (size_t(2) * NC * L.ls * 16))));
+  G = std::min(G, std::max(1, nxy / (2 * 148)));  // small grids: >= 2 CTAs per SM
+  L.G = std::min(G, nxy);
+  L.threads = (L.G * NC * ctx->Nz >= 2048 || L.G * ctx->Nz >= 256) ? 256 : 128;
+  L.smem = size_t(2) * NC * L.G * L.ls * 16;
+  L.grid = dim3((nxy + L.G - 1) / L.G);
+  return L;
+}
+
+void prof_mark(fm_ctx* ctx) {
+  if (!ctx->prof.on) return;
   cudaEvent_t e;
   if (!ctx->prof.pool.empty()) {
     e = ctx->prof.pool.back();
@@ -252,107 +285,124 @@ cudaEvent_t prof_event(fm_ctx* ctx) {
   } else {
     cudaEventCreate(&e);
   }
-  return e;
-}
-
-void prof_mark(fm_ctx* ctx) {
-  if (!ctx->prof.on) return;
-  cudaEvent_t e = prof_event(ctx);
   cudaEventRecord(e, ctx->stream);
   ctx->prof.pending.push_back(e);
 }
 
 template <int TD>
-int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiArgs& epi, int* nparts) {
-  constexpr int NC = TD * TD;
+void init_generic() {
   static bool init = false;
-  if (!init) {
-    allow_smem(k_zfwd<TD, PRO_COPY, false>);
-    allow_smem(k_zfwd<TD, PRO_K4, false>);
-    allow_smem(k_zfwd<TD, PRO_SVK, false>);
-    allow_smem(k_zfwd<TD, PRO_K4, true>);
-    allow_smem(k_zfwd<TD, PRO_SVK, true>);
-    allow_smem(k_ypass);
-    allow_smem(k_xpass<TD>);
-    allow_smem(k_zinv<TD>);
-    init = true;
-  }
-  const Geo g = make_geo(ctx);
-  const int nxy = ctx->Nx * ctx->Ny;
+  if (init) return;
+  allow_smem(k_zfwd<TD, PRO_COPY, false>);
+  allow_smem(k_zfwd<TD, PRO_K4, false>);
+  allow_smem(k_zfwd<TD, PRO_SVK, false>);
+  allow_smem(k_zfwd<TD, PRO_K4, true>);
+  allow_smem(k_zfwd<TD, PRO_SVK, true>);
+  allow_smem(k_ypass);
+  allow_smem(k_xpass<TD>);
+  allow_smem(k_zinv<TD>);
+  init = true;
+}
+
+template <int TD>
+int pass_zf(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* A) {
+  int st = FM_OK;
+  if (TD == 3 && zf_fast(ctx, g, pa, A, &st)) return st;
+  const ZLaunch L = z_launch(ctx, g);
+  if (L.smem + 1024 > size_t(kMaxSmem)) return set_error(ctx, FM_E_UNSUPPORTED, "z line too long for the shared-memory FFT");
   const bool even = ctx->Nz % 2 == 0;
   const AxisPlan& pzp = even ? ctx->pzh : ctx->pz;
-  int ls = std::max(ctx->Lz, ctx->nzh);
-  if (ls % 2 == 0) ls += 1;  // odd pitch: fewer bank conflicts
-  int G = int(std::max<size_t>(1, std::min<size_t>(16, size_t(96 * 1024) / (size_t(2) * NC * ls * 16))));
-  // small grids: spread the z lines over at least two CTAs per SM
-  G = std::min(G, std::max(1, nxy / (2 * 148)));
-  G = std::min(G, nxy);
-  const int zthreads = (G * NC * ctx->Nz >= 2048 || G * ctx->Nz >= 256) ? 256 : 128;
-  const size_t smz = size_t(2) * NC * G * ls * 16;
-  if (smz + 1024 > size_t(kMaxSmem))
-    return set_error(ctx, FM_E_UNSUPPORTED, "z line too long for the shared-memory FFT");
-  const dim3 gz((nxy + G - 1) / G);
-  int TWy, TWx;
-  if (tile_width(ctx->nzh, ctx->Ny, 1, TWy, int64_t(ctx->Nx) * NC) || tile_width(ctx->nzh, ctx->Nx, TD, TWx, int64_t(ctx->Ny) * TD))
-    return set_error(ctx, FM_E_UNSUPPORTED, "x/y line too long for the shared-memory FFT");
+  const bool dir = pa.r != nullptr;
+  cudaStream_t s = ctx->stream;
+  if (pa.kind == PRO_COPY)
+    k_zfwd<TD, PRO_COPY, false><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
+  else if (pa.kind == PRO_K4 && !dir)
+    k_zfwd<TD, PRO_K4, false><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
+  else if (pa.kind == PRO_K4)
+    k_zfwd<TD, PRO_K4, true><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
+  else if (!dir)
+    k_zfwd<TD, PRO_SVK, false><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
+  else
+    k_zfwd<TD, PRO_SVK, true><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+template <int TD>
+int pass_y(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out) {
+  if (g.Ny <= 1 && g.P == 1) return FM_OK;  // length-1 transform, identical layouts
   int st = FM_OK;
-  // pass 1: z forward (+ prologue)
-  prof_mark(ctx);
-  if (!(TD == 3 && zf_fast(ctx, pa, &st))) {
-    const bool dir = pa.r != nullptr;
-    if (pa.kind == PRO_COPY)
-      k_zfwd<TD, PRO_COPY, false><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-    else if (pa.kind == PRO_K4 && !dir)
-      k_zfwd<TD, PRO_K4, false><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-    else if (pa.kind == PRO_K4)
-      k_zfwd<TD, PRO_K4, true><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-    else if (!dir)
-      k_zfwd<TD, PRO_SVK, false><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-    else
-      k_zfwd<TD, PRO_SVK, true><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, pa, ctx->spec, G, ls);
-    FM_LAUNCHED(ctx);
-  } else if (st) {
+  if (TD == 3 && y_fast(ctx, g, sign, in, out, &st)) return st;
+  int TW;
+  if (tile_width(ctx->nzh, g.Ny, 1, TW, int64_t(g.Nx) * ctx->ncomp))
+    return set_error(ctx, FM_E_UNSUPPORTED, "y line too long for the shared-memory FFT");
+  const dim3 grid((ctx->nzh + TW - 1) / TW, g.Nx, ctx->ncomp);
+  k_ypass<<<grid, 256, size_t(2) * g.Ny * TW * 16, ctx->stream>>>(g, ctx->py, in, out, TW, sign);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+template <int TD>
+int pass_x(fm_ctx* ctx, const Geo& g, double2* T) {
+  int st = FM_OK;
+  if (TD == 3 && x_fast(ctx, g, T, &st)) return st;
+  int TW;
+  if (tile_width(ctx->nzh, g.Nx, TD, TW, int64_t(g.Ny) * TD))
+    return set_error(ctx, FM_E_UNSUPPORTED, "x line too long for the shared-memory FFT");
+  const dim3 grid((ctx->nzh + TW - 1) / TW, g.Ny, TD);
+  k_xpass<TD><<<grid, 256, size_t(2) * g.Nx * TD * TW * 16, ctx->stream>>>(g, ctx->px, T, TW);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+template <int TD>
+int pass_zi(fm_ctx* ctx, const Geo& g, const double2* A, double* out, double scale, const EpiArgs& epi,
+            int* nparts) {
+  int st = FM_OK;
+  if (TD == 3 && zi_fast(ctx, g, A, out, scale, epi, &st)) {
+    if (nparts) *nparts = zi_fast_blocks(ctx, g);
     return st;
   }
-  // pass 2: y forward
+  const ZLaunch L = z_launch(ctx, g);
+  const AxisPlan& pzp = (ctx->Nz % 2 == 0) ? ctx->pzh : ctx->pz;
+  k_zinv<TD><<<L.grid, L.threads, L.smem, ctx->stream>>>(g, pzp, ctx->pz.tw, A, out, L.G, L.ls, scale, epi);
+  FM_LAUNCHED(ctx);
+  if (nparts) *nparts = int(L.grid.x);
+  return FM_OK;
+}
+
+template <int TD>
+int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiArgs& epi, int* nparts) {
+  init_generic<TD>();
+  const int r0 = ctx->virt ? 0 : ctx->rank;
+  const int r1 = ctx->virt ? ctx->P : ctx->rank + 1;
+  const double sc = scale / double(ctx->n_global);
   prof_mark(ctx);
-  if (ctx->Ny > 1 && !(TD == 3 && y_fast(ctx, -1, &st))) {
-    const dim3 gy((ctx->nzh + TWy - 1) / TWy, ctx->Nx, NC);
-    k_ypass<<<gy, 256, size_t(2) * ctx->Ny * TWy * 16, ctx->stream>>>(g, ctx->py, ctx->spec, TWy, -1);
-    FM_LAUNCHED(ctx);
-  } else if (st) {
-    return st;
-  }
-  // pass 3: x forward, ghat, x inverse
+  for (int r = r0; r < r1; ++r)
+    if (int st = pass_zf<TD>(ctx, geo_zy(ctx, r), pa, spec_a(ctx, r))) return st;
   prof_mark(ctx);
-  if (!(TD == 3 && x_fast(ctx, &st))) {
-    const dim3 gx((ctx->nzh + TWx - 1) / TWx, ctx->Ny, TD);
-    k_xpass<TD><<<gx, 256, size_t(2) * ctx->Nx * TD * TWx * 16, ctx->stream>>>(g, ctx->px, ctx->spec, TWx);
-    FM_LAUNCHED(ctx);
-  } else if (st) {
-    return st;
-  }
-  // pass 4: y inverse
+  for (int r = r0; r < r1; ++r)
+    if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), -1, spec_a(ctx, r), spec_b(ctx, r))) return st;
   prof_mark(ctx);
-  if (ctx->Ny > 1 && !(TD == 3 && y_fast(ctx, +1, &st))) {
-    const dim3 gy((ctx->nzh + TWy - 1) / TWy, ctx->Nx, NC);
-    k_ypass<<<gy, 256, size_t(2) * ctx->Ny * TWy * 16, ctx->stream>>>(g, ctx->py, ctx->spec, TWy, +1);
-    FM_LAUNCHED(ctx);
-  } else if (st) {
-    return st;
-  }
-  // pass 5: z inverse (c2r), scale
+  if (ctx->P > 1)
+    if (int st = transpose(ctx, +1)) return st;
+  for (int r = r0; r < r1; ++r)
+    if (int st = pass_x<TD>(ctx, geo_x(ctx, r), spec_a(ctx, r))) return st;
+  if (ctx->P > 1)
+    if (int st = transpose(ctx, -1)) return st;
   prof_mark(ctx);
-  if (!(TD == 3 && zi_fast(ctx, out, scale / double(ctx->n), epi, &st))) {
-    k_zinv<TD><<<gz, zthreads, smz, ctx->stream>>>(g, pzp, ctx->pz.tw, ctx->spec, out, G, ls,
-                                              scale / double(ctx->n), epi);
-    FM_LAUNCHED(ctx);
-    if (nparts) *nparts = int(gz.x);
-  } else if (st) {
-    return st;
-  } else if (nparts) {
-    *nparts = zi_fast_blocks(ctx);
+  for (int r = r0; r < r1; ++r)
+    if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), +1, spec_b(ctx, r), spec_a(ctx, r))) return st;
+  prof_mark(ctx);
+  int total = 0;
+  for (int r = r0; r < r1; ++r) {
+    EpiArgs e = epi;
+    if (e.partial) e.partial += total;
+    int np = 0;
+    if (int st = pass_zi<TD>(ctx, geo_zy(ctx, r), spec_a(ctx, r), out, sc, e, &np)) return st;
+    total += np;
   }
+  if (nparts) *nparts = total;
   prof_mark(ctx);
   if (ctx->prof.on) ctx->prof.calls++;
   return FM_OK;
@@ -362,7 +412,7 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
 int profile_collect(fm_ctx* ctx) {
   auto& pr = ctx->prof;
   FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  for (size_t g0 = 0; g0 + kPasses < pr.pending.size() + 0; g0 += kPasses + 1) {
+  for (size_t g0 = 0; g0 + kPasses < pr.pending.size(); g0 += kPasses + 1) {
     for (int s = 0; s < kPasses; ++s) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, pr.pending[g0 + s], pr.pending[g0 + s + 1]);

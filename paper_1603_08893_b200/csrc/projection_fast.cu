@@ -23,20 +23,28 @@ using reg::e_line;
 using reg::e_x;
 
 // ------------------------------------------------------------------ y pass
+// SIGN -1: std layout in, packed (all-to-all) layout out; +1: the reverse.
+// With P = 1 both layouts coincide and in == out (in place).
 template <int N, int TW, int SIGN>
 __global__ void __launch_bounds__(TW*(N / e_line(N))) k_y_fast(Geo g, const double2* __restrict__ tw,
-                                                               double2* __restrict__ spec) {
+                                                               const double2* in, double2* out) {
   constexpr int E = e_line(N), T = N / E;
   extern __shared__ double2 sm[];
   const int l = threadIdx.x % TW, t = threadIdx.x / TW;
   const int kz = blockIdx.x * TW + l;
-  double2* base = spec + (int64_t(blockIdx.z) * g.Nx + blockIdx.y) * int64_t(N) * g.nzh + kz;
+  const int x = blockIdx.y, c = blockIdx.z, NC = gridDim.z;
   double2 v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = base[int64_t(t + T * m) * g.nzh];
+  for (int m = 0; m < E; ++m) {
+    const int y = t + T * m;
+    v[m] = in[SIGN < 0 ? spec_std(g, c, x, y, kz) : spec_packed(g, NC, c, x, y, kz)];
+  }
   reg::fft<N, E, SIGN>(v, sm + l, TW, t, tw);
 #pragma unroll
-  for (int m = 0; m < E; ++m) base[int64_t(t + T * m) * g.nzh] = v[m];
+  for (int m = 0; m < E; ++m) {
+    const int y = t + T * m;
+    out[SIGN < 0 ? spec_packed(g, NC, c, x, y, kz) : spec_std(g, c, x, y, kz)] = v[m];
+  }
 }
 
 // ------------------------------------------------------------------ x pass
@@ -58,8 +66,9 @@ __global__ void __launch_bounds__(TW*(N / e_x(N)), 2) k_x_fast(Geo g, const doub
 #pragma unroll
   for (int j = 0; j < TD; ++j) reg::fft<N, E, -1>(v[j], sm + l, TW, t, tw);
   // Bhat_ij = sum_l Ahat_il ghat_lj  (projection.cpp:87-104, 139-152)
-  const int qy = freq_of(y, g.Ny), qz = freq_of(kz, g.Nz);
-  const bool nyq_yz = ((g.Ny % 2 == 0) && (y == g.Ny / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+  const int yg = g.y0 + y;  // global y (slab decomposition: y-slab of this rank)
+  const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
+  const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
   const double xiy = qy * g.invL[1], xiz = (g.dim == 3) ? qz * g.invL[2] : 0.0;
 #pragma unroll
   for (int m = 0; m < E; ++m) {
@@ -120,8 +129,9 @@ __global__ void __launch_bounds__(TW*(N / E)) k_x_fast2(Geo g, const double2* __
 #pragma unroll
     for (int m = 0; m < E; ++m) S[(t + T * m) * TW] = v[m];
   }
-  const int qy = freq_of(y, g.Ny), qz = freq_of(kz, g.Nz);
-  const bool nyq_yz = ((g.Ny % 2 == 0) && (y == g.Ny / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+  const int yg = g.y0 + y;  // global y (slab decomposition: y-slab of this rank)
+  const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
+  const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
   const double xiy = qy * g.invL[1], xiz = (g.dim == 3) ? qz * g.invL[2] : 0.0;
 #pragma unroll 2
   for (int m = 0; m < E; ++m) {  // own positions only: no barrier needed
@@ -188,7 +198,7 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
   // phase 1: prologue, one thread per voxel; z -> packed complex m = z/2
   for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
     const int gi = w / N, z = w - gi * N;
-    const int64_t node = int64_t(L0 + gi) * N + z;
+    const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
     double v[9];
     prologue_voxel<3, PRO, DIR>(pa, g.n, node, v);
 #pragma unroll
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const dou
   double dot = 0.0;
   for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
     const int gi = w / N, z = w - gi * N;
-    const int64_t node = int64_t(L0 + gi) * N + z;
+    const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
       const double val = smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] * scale;
@@ -292,7 +302,6 @@ __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const dou
 // ------------------------------------------------------------------- host
 namespace {
 
-
 template <typename K>
 void allow(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
@@ -302,25 +311,28 @@ void allow(K kernel, size_t bytes) {
 int tw_of(int N) { return N >= 1024 ? 4 : 8; }
 constexpr int tw_x(int N) { return N >= 1024 ? 2 : (N >= 512 ? 4 : 8); }
 
+int launched(fm_ctx* ctx, const char* what) {
+  ctx->cnt.launches++;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FM_OK : check_cuda(ctx, e, what);
+}
+
 template <int N>
-bool y_launch(fm_ctx* ctx, int sign, int* st) {
+bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st) {
   constexpr int TW = N >= 1024 ? 4 : 8;
   constexpr int T = N / e_line(N);
   const size_t smem = size_t(N) * TW * 16;
-  const Geo g = make_geo(ctx);
-  const dim3 grid(ctx->nzh / TW, ctx->Nx, ctx->ncomp);
+  const dim3 grid(ctx->nzh / TW, g.Nx, ctx->ncomp);
   if (sign < 0) {
     static bool a = (allow(k_y_fast<N, TW, -1>, smem), true);
     (void)a;
-    k_y_fast<N, TW, -1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, ctx->spec);
+    k_y_fast<N, TW, -1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
   } else {
     static bool a = (allow(k_y_fast<N, TW, +1>, smem), true);
     (void)a;
-    k_y_fast<N, TW, +1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, ctx->spec);
+    k_y_fast<N, TW, +1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
   }
-  ctx->cnt.launches++;
-  const cudaError_t e = cudaGetLastError();
-  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_y_fast");
+  *st = launched(ctx, "k_y_fast");
   return true;
 }
 
@@ -333,100 +345,70 @@ int x_variant() {
 }
 
 template <int N, int E>
-void x2_go(fm_ctx* ctx) {
+void x2_go(fm_ctx* ctx, const Geo& g, double2* spec) {
   constexpr int TW = 8;
   constexpr int T = N / E;
   const size_t smem = size_t(3) * N * TW * 16;
   static bool a = (allow(k_x_fast2<N, TW, E>, smem), true);
   (void)a;
-  const Geo g = make_geo(ctx);
-  const dim3 grid(ctx->nzh / TW, ctx->Ny, 3);
-  k_x_fast2<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, ctx->spec);
+  const dim3 grid(ctx->nzh / TW, g.Ny, 3);
+  k_x_fast2<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
 
 template <int N>
-bool x_launch(fm_ctx* ctx, int* st) {
+bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   constexpr int TW = tw_x(N);
   constexpr int T = N / e_x(N);
   const size_t smem = size_t(N) * TW * 16;
   const int var = (N <= 512 && ctx->nzh % 8 == 0) ? x_variant() : 1;
   if (var == 2) {
-    x2_go<N, e_line(N)>(ctx);
+    x2_go<N, e_line(N)>(ctx, g, spec);
   } else if (var == 3) {
-    x2_go<N, e_x(N)>(ctx);
+    x2_go<N, e_x(N)>(ctx, g, spec);
   } else {
     static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
     (void)a;
-    const Geo g = make_geo(ctx);
-    const dim3 grid(ctx->nzh / TW, ctx->Ny, 3);
-    k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, ctx->spec);
+    const dim3 grid(ctx->nzh / TW, g.Ny, 3);
+    k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
   }
-  ctx->cnt.launches++;
-  const cudaError_t e = cudaGetLastError();
-  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_x_fast");
+  *st = launched(ctx, "k_x_fast");
   return true;
 }
 
 template <int M, int PRO, bool DIR>
-void zf_go(fm_ctx* ctx, const ProArgs& pa) {
+void zf_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   using S = ZShape<M, PRO != PRO_COPY>;
   static bool a = (allow(k_zf_fast<M, PRO, DIR>, S::SMEM), true);
   (void)a;
-  const Geo g = make_geo(ctx);
-  const int nxy = ctx->Nx * ctx->Ny;
+  const int nxy = g.Nx * g.Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
-  k_zf_fast<M, PRO, DIR><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, ctx->spec);
+  k_zf_fast<M, PRO, DIR><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
 }
 
 template <int M>
-bool zf_launch(fm_ctx* ctx, const ProArgs& pa, int* st) {
+bool zf_launch(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int* st) {
   const bool dir = pa.r != nullptr;
-  if (pa.kind == PRO_COPY) zf_go<M, PRO_COPY, false>(ctx, pa);
-  else if (pa.kind == PRO_K4 && !dir) zf_go<M, PRO_K4, false>(ctx, pa);
-  else if (pa.kind == PRO_K4) zf_go<M, PRO_K4, true>(ctx, pa);
-  else if (!dir) zf_go<M, PRO_SVK, false>(ctx, pa);
-  else zf_go<M, PRO_SVK, true>(ctx, pa);
-  ctx->cnt.launches++;
-  const cudaError_t e = cudaGetLastError();
-  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_zf_fast");
+  if (pa.kind == PRO_COPY) zf_go<M, PRO_COPY, false>(ctx, g, pa, spec);
+  else if (pa.kind == PRO_K4 && !dir) zf_go<M, PRO_K4, false>(ctx, g, pa, spec);
+  else if (pa.kind == PRO_K4) zf_go<M, PRO_K4, true>(ctx, g, pa, spec);
+  else if (!dir) zf_go<M, PRO_SVK, false>(ctx, g, pa, spec);
+  else zf_go<M, PRO_SVK, true>(ctx, g, pa, spec);
+  *st = launched(ctx, "k_zf_fast");
   return true;
 }
 
 template <int M>
-bool zi_launch(fm_ctx* ctx, double* out, double scale, const EpiArgs& epi, int* st) {
+bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
+               int* st) {
   using S = ZShape<M>;
   static bool a = (allow(k_zi_fast<M>, S::SMEM), true);
   (void)a;
-  const Geo g = make_geo(ctx);
-  const int nxy = ctx->Nx * ctx->Ny;
+  const int nxy = g.Nx * g.Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
-  k_zi_fast<M><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, ctx->spec, out, scale, epi);
-  ctx->cnt.launches++;
-  const cudaError_t e = cudaGetLastError();
-  *st = e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_zi_fast");
+  k_zi_fast<M><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+  *st = launched(ctx, "k_zi_fast");
   return true;
 }
-
-bool fast_z_ok(const fm_ctx* ctx);
-
-}  // namespace
-
-int zi_fast_blocks(const fm_ctx* ctx) {
-  const int nxy = ctx->Nx * ctx->Ny;
-  int G = 0;
-  switch (ctx->Nz / 2) {
-    case 16: G = ZShape<16>::G; break;
-    case 32: G = ZShape<32>::G; break;
-    case 64: G = ZShape<64>::G; break;
-    case 128: G = ZShape<128>::G; break;
-    case 256: G = ZShape<256>::G; break;
-    case 512: G = ZShape<512>::G; break;
-    default: return 0;
-  }
-  return fast_z_ok(ctx) ? (nxy + G - 1) / G : 0;
-}
-
-namespace {
 
 bool fast_z_ok(const fm_ctx* ctx) {
   return ctx->tdim == 3 && ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE && ctx->Nz % 2 == 0 &&
@@ -449,40 +431,51 @@ bool fast_xy_ok(const fm_ctx* ctx, int N) {
     default: return false;                     \
   }
 
-bool y_fast(fm_ctx* ctx, int sign, int* st) {
-  if (!fast_xy_ok(ctx, ctx->Ny)) return false;
-  FM_POW2_CASES(y_launch, ctx->Ny, ctx, sign, st)
-}
-
-bool x_fast(fm_ctx* ctx, int* st) {
-  if (!fast_xy_ok(ctx, ctx->Nx)) return false;
-  FM_POW2_CASES(x_launch, ctx->Nx, ctx, st)
-}
-
-bool zf_fast(fm_ctx* ctx, const ProArgs& pa, int* st) {
-  if (!fast_z_ok(ctx)) return false;
-  switch (ctx->Nz / 2) {
-    case 16: return zf_launch<16>(ctx, pa, st);
-    case 32: return zf_launch<32>(ctx, pa, st);
-    case 64: return zf_launch<64>(ctx, pa, st);
-    case 128: return zf_launch<128>(ctx, pa, st);
-    case 256: return zf_launch<256>(ctx, pa, st);
-    case 512: return zf_launch<512>(ctx, pa, st);
-    default: return false;
+#define FM_HALF_CASES(X, M_, ...)              \
+  switch (M_) {                                \
+    case 16: return X<16>(__VA_ARGS__);        \
+    case 32: return X<32>(__VA_ARGS__);        \
+    case 64: return X<64>(__VA_ARGS__);        \
+    case 128: return X<128>(__VA_ARGS__);      \
+    case 256: return X<256>(__VA_ARGS__);      \
+    case 512: return X<512>(__VA_ARGS__);      \
+    default: return false;                     \
   }
+
+bool y_fast(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st) {
+  if (!fast_xy_ok(ctx, g.Ny)) return false;
+  FM_POW2_CASES(y_launch, g.Ny, ctx, g, sign, in, out, st)
 }
 
-bool zi_fast(fm_ctx* ctx, double* out, double scale, const EpiArgs& epi, int* st) {
+bool x_fast(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
+  if (!fast_xy_ok(ctx, g.Nx)) return false;
+  FM_POW2_CASES(x_launch, g.Nx, ctx, g, spec, st)
+}
+
+bool zf_fast(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int* st) {
   if (!fast_z_ok(ctx)) return false;
+  FM_HALF_CASES(zf_launch, ctx->Nz / 2, ctx, g, pa, spec, st)
+}
+
+bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
+             int* st) {
+  if (!fast_z_ok(ctx)) return false;
+  FM_HALF_CASES(zi_launch, ctx->Nz / 2, ctx, g, spec, out, scale, epi, st)
+}
+
+int zi_fast_blocks(const fm_ctx* ctx, const Geo& g) {
+  const int nxy = g.Nx * g.Ny;
+  int G = 0;
   switch (ctx->Nz / 2) {
-    case 16: return zi_launch<16>(ctx, out, scale, epi, st);
-    case 32: return zi_launch<32>(ctx, out, scale, epi, st);
-    case 64: return zi_launch<64>(ctx, out, scale, epi, st);
-    case 128: return zi_launch<128>(ctx, out, scale, epi, st);
-    case 256: return zi_launch<256>(ctx, out, scale, epi, st);
-    case 512: return zi_launch<512>(ctx, out, scale, epi, st);
-    default: return false;
+    case 16: G = ZShape<16>::G; break;
+    case 32: G = ZShape<32>::G; break;
+    case 64: G = ZShape<64>::G; break;
+    case 128: G = ZShape<128>::G; break;
+    case 256: G = ZShape<256>::G; break;
+    case 512: G = ZShape<512>::G; break;
+    default: return 0;
   }
+  return (nxy + G - 1) / G;
 }
 
 }  // namespace fm

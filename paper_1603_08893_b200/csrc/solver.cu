@@ -76,7 +76,7 @@ int norm_sync(fm_ctx* ctx, const double* a, int64_t count, double* out) {
 int mean_sync(fm_ctx* ctx, const double* a, double* mean) {
   if (int st = sum_comp_async(ctx, a, ctx->ncomp, ctx->n, ctx->d_scal + 16)) return st;
   if (int st = fetch_scalars(ctx, 16 + ctx->ncomp)) return st;
-  for (int c = 0; c < ctx->ncomp; ++c) mean[c] = ctx->h_scal[16 + c] / double(ctx->n);
+  for (int c = 0; c < ctx->ncomp; ++c) mean[c] = ctx->h_scal[16 + c] / double(ctx->n_global);
   return FM_OK;
 }
 
@@ -97,7 +97,7 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
     *rel = 0.0;
     return FM_OK;
   }
-  const int64_t cap = max_cg > 0 ? max_cg : count;  // :27-29 (int64: no overflow past 620^3)
+  const int64_t cap = max_cg > 0 ? max_cg : ctx->n_global * ctx->ncomp;  // :27-29 (int64: no overflow past 620^3)
   FM_CUDA(ctx, cudaMemcpyAsync(ctx->r.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
   FM_CUDA(ctx, cudaMemcpyAsync(ctx->p.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
   double rr = ctx->h_scal[S_RR];
@@ -187,11 +187,11 @@ int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t count = ctx->n * nc;
   double* F = Ff->d;
-  if (int st = ensure_field(ctx, ctx->P, nc)) return st;
+  if (int st = ensure_field(ctx, ctx->Pw, nc)) return st;
   if (int st = ensure_field(ctx, ctx->dF, nc)) return st;
   if (int st = ensure_field(ctx, ctx->rhs, nc)) return st;
   if (int st = ensure_field(ctx, ctx->tmp, nc)) return st;
-  double* P = ctx->P.d;
+  double* P = ctx->Pw.d;
   const auto finish = [&](bool conv) {
     rep->converged = conv ? 1 : 0;
     rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

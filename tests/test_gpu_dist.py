@@ -1,0 +1,58 @@
+"""Slab decomposition validated on one B200: P slab ranks
+emulated on the device ("virtual ranks", the all-to-all is a device copy)
+must reproduce the P = 1 projection bit for bit -- the z / y / x passes
+compute the same lines in the same order, only the layouts between them
+change -- and the Newton solve must match the single-rank run."""
+import numpy as np
+import pytest
+
+from paper_1603_08893_b200 import abi
+from paper_1603_08893_b200 import microstructure as M
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("pts,P", [((64, 64, 64), 2), ((64, 64, 64), 8), ((32, 32, 32), 4),
+                                   ((128, 64, 32), 8), ((12, 10, 14), 2), ((16, 24, 9), 4),
+                                   ((256, 256, 32), 8)])
+def test_virtual_ranks_bitwise_equal(pts, P):
+    A = M.uniform_field(pts, 9, seed=3)
+    n = int(np.prod(pts))
+    K = np.random.default_rng(1).uniform(-1, 1, 81 * n)
+    with abi.Context(pts, 3) as ctx:
+        fa, fk = ctx.field(9, A), ctx.field(81, K)
+        g1 = ctx.projection(fa).download()
+        m1 = ctx.projected_tangent(fk, fa).download()
+        ctx.set_virtual_ranks(P)
+        assert ctx.ranks() == (P, 0, True)
+        gp = ctx.projection(fa).download()
+        mp = ctx.projected_tangent(fk, fa).download()
+    assert np.array_equal(g1, gp)
+    assert np.array_equal(m1, mp)
+
+
+def test_virtual_ranks_solve_matches_single_rank():
+    pts = (32, 32, 32)
+    pg = M.bernoulli(pts, 0.3, seed=2)
+    lam, mu, _, _ = M.bind_parameters(pg, [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)])
+    fb = M.simple_shear_program(0.1, 1, 3)[0]
+    out = []
+    for P in (1, 4):
+        with abi.Context(pts, 3) as ctx:
+            ctx.set_virtual_ranks(P)
+            model = abi.Model(ctx, "hyper", lam, mu, matrix_free=True)
+            F = ctx.field(9, abi.identity_field(pts, 3))
+            rep = model.solve_increment(F, fb)
+            out.append((F.download(), rep))
+            model.close()
+    (F1, r1), (F4, r4) = out
+    assert r1["passes"] == r4["passes"]
+    assert all(abs(a - b) <= 1 for a, b in zip(r1["cg_it"], r4["cg_it"]))
+    assert np.linalg.norm(F1 - F4) / np.linalg.norm(F1) < 1e-12
+
+
+def test_indivisible_grid_is_rejected():
+    with abi.Context((10, 12, 8), 3) as ctx:
+        with pytest.raises(abi.FmError) as e:
+            ctx.set_virtual_ranks(4)
+        assert e.value.status == 11
