@@ -183,7 +183,12 @@ int fm_model_destroy(fm_ctx* ctx, fm_model* m);
 int fm_model_evaluate(fm_ctx* ctx, fm_model* m, const fm_field* F, fm_field* P);
 /* MaterialModel::commit (simo.cpp:220-223); no-op for hyperelastic. */
 int fm_model_commit(fm_ctx* ctx, fm_model* m, const fm_field* F);
-/* Model-owned tangent field (NULL when matrix-free). */
+/* Tangent storage of a Simo model: 0 = K4 (81 slabs, the reference form,
+ * default), 1 = compact eigenbasis form (45 slabs: V, U = F^-1 V and three
+ * 3x3 coefficient sets; the matvec forms dP = V W U^T) -- what lets the
+ * 512^3 J2 configuration fit on one B200.  K4 is then not materialised. */
+int fm_model_set_tangent_form(fm_ctx* ctx, fm_model* m, int form);
+/* Model-owned tangent field (NULL when matrix-free or compact). */
 fm_field* fm_model_tangent(fm_model* m);
 /* History access (Simo): which = 0 committed, 1 trial; be has 9n, epsp n. */
 int fm_model_get_history(fm_ctx* ctx, fm_model* m, int which, double* be, double* epsp);

@@ -112,6 +112,7 @@ _SIGS = {
     "fm_ctx_create_dist": (C.c_int, [C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_double), C.c_int, C.c_int,
                                      C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_P)]),
     "fm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
+    "fm_model_set_tangent_form": (C.c_int, [_P, _P, C.c_int]),
     "fm_ctx_set_virtual_ranks": (C.c_int, [_P, C.c_int]),
     "fm_ctx_ranks": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fm_dist_chunk": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -342,7 +343,7 @@ class Field:
 class Model:
     """fm_model: MaterialModel (material.hpp:45-65) resident on the device."""
 
-    def __init__(self, ctx, kind, lam, mu, ty0=None, hard=None, matrix_free=False):
+    def __init__(self, ctx, kind, lam, mu, ty0=None, hard=None, matrix_free=False, compact=False):
         self.ctx = ctx
         h = _P()
         f = lambda a: np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
@@ -350,6 +351,8 @@ class Model:
             ctx.check(lib().fm_model_create_hyper(ctx.h, f(lam), f(mu), int(matrix_free), C.byref(h)))
         else:
             ctx.check(lib().fm_model_create_simo(ctx.h, f(lam), f(mu), f(ty0), f(hard), C.byref(h)))
+            if compact:
+                ctx.check(lib().fm_model_set_tangent_form(ctx.h, h, 1))
         self.h = h
         self.kind = kind
 

@@ -515,7 +515,7 @@ int fm_model_create_simo(fm_ctx* ctx, const double* lambda, const double* mu, co
 int fm_model_destroy(fm_ctx* ctx, fm_model* m) {
   if (!m) return FM_OK;
   if (ctx) cudaStreamSynchronize(ctx->stream);
-  for (fm_field* f : {&m->lambda, &m->mu, &m->tau_y0, &m->hard, &m->K, &m->F_eval, &m->be_c,
+  for (fm_field* f : {&m->lambda, &m->mu, &m->tau_y0, &m->hard, &m->K, &m->Kc, &m->F_eval, &m->be_c,
                       &m->epsp_c, &m->be_t, &m->epsp_t, &m->f_old})
     release_field(*f);
   delete m;
@@ -534,6 +534,22 @@ int fm_model_commit(fm_ctx* ctx, fm_model* m, const fm_field* F) {
 }
 
 fm_field* fm_model_tangent(fm_model* m) { return (m && m->K.d) ? &m->K : nullptr; }
+
+int fm_model_set_tangent_form(fm_ctx* ctx, fm_model* m, int form) {
+  if (!ctx || !m || form < 0 || form > 1) return FM_E_INVALID;
+  if (m->kind != 1) return form == 0 ? FM_OK : set_error(ctx, FM_E_INVALID, "compact tangent: Simo model only");
+  if (form == m->compact) return FM_OK;
+  cudaStreamSynchronize(ctx->stream);
+  if (form == 1) {
+    release_field(m->K);
+    if (int st = ensure_field(ctx, m->Kc, 45)) return st;
+  } else {
+    release_field(m->Kc);
+    if (int st = ensure_field(ctx, m->K, 81)) return st;
+  }
+  m->compact = form;
+  return FM_OK;
+}
 
 int fm_model_get_history(fm_ctx* ctx, fm_model* m, int which, double* be, double* epsp) {
   if (!ctx || !m || m->kind != 1) return set_error(ctx, FM_E_INVALID, "history: not a Simo model");

@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restric
                                               double* __restrict__ P, double* __restrict__ K,
                                               double* __restrict__ be_t,
                                               double* __restrict__ epsp_t,
-                                              unsigned long long* bad, double* badval, int64_t noff) {
+                                              unsigned long long* bad, double* badval, int64_t noff,
+                                              double* __restrict__ Kc) {
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
        q += int64_t(gridDim.x) * blockDim.x) {
     const double lam = __ldg(lam_f + q), g = __ldg(mu_f + q), ty0 = __ldg(ty0_f + q),
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restric
                                    tau[i * 3 + 1] * Finv[j * 3 + 1] +
                                    tau[i * 3 + 2] * Finv[j * 3 + 2];
     }
-    if (!K) continue;
+    if (!K && !Kc) continue;
     // eigenbasis coefficients of the algorithmic tangent (simo.cpp:131-194)
     const double a0 = plastic ? dgamma / taueq_tr : 0.0;
     const double c1 = plastic ? -6.0 * g * g * a0 : 0.0;
@@ -333,6 +334,17 @@ __global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restric
       for (int p = 0; p < 3; ++p)
         U[i * 3 + p] = Finv[i * 3 + 0] * V[0 * 3 + p] + Finv[i * 3 + 1] * V[1 * 3 + p] +
                        Finv[i * 3 + 2] * V[2 * 3 + p];
+    if (Kc) {  // compact J2 tangent: V, U, a, b, c (45 slabs, 360 B/voxel)
+#pragma unroll
+      for (int e = 0; e < 9; ++e) {
+        Kc[(0 + e) * n + q] = V[e];
+        Kc[(9 + e) * n + q] = U[e];
+        Kc[(18 + e) * n + q] = ca[e];
+        Kc[(27 + e) * n + q] = cb[e];
+        Kc[(36 + e) * n + q] = cc[e];
+      }
+    }
+    if (!K) continue;
 #pragma unroll 1
     for (int ij = 0; ij < 9; ++ij) {
       const int i = ij / 3, j = ij % 3;
@@ -401,12 +413,12 @@ int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const doub
 
 int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const double* be_c,
                     const double* epsp_c, const double* lam, const double* mu, const double* ty0,
-                    const double* hard, double* P, double* K, double* be_t, double* epsp_t) {
+                    const double* hard, double* P, double* K, double* be_t, double* epsp_t, double* Kc) {
   if (ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "simo_evaluate: tensors must be 3x3");
   if (int st = reset_bad(ctx)) return st;
   const int blocks = grid_for(ctx->n, 128);
   k_simo<<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K,
-                                          be_t, epsp_t, ctx->d_bad, ctx->d_badval, ctx->node_offset);
+                                          be_t, epsp_t, ctx->d_bad, ctx->d_badval, ctx->node_offset, Kc);
   FM_LAUNCHED(ctx);
   return FM_OK;
 }

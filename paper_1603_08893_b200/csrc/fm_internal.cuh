@@ -34,6 +34,7 @@ enum Prologue : int {
   PRO_COPY = 0,  // G(A): read A
   PRO_K4 = 1,    // G(K : dF^T): dP_ij = K_jikl dF_kl (projection.cpp:182-192)
   PRO_SVK = 2,   // matrix-free SVK tangent action from F, lambda, mu
+  PRO_J2C = 3,   // compact J2 tangent (V, U, a, b, c): dP = V W U^T, W from D = V^T dF U
 };
 
 struct Counters {
@@ -62,7 +63,9 @@ struct fm_model {
   int kind = 0;  // 0 hyperelastic, 1 Simo
   int matrix_free = 0;
   fm_field lambda, mu, tau_y0, hard;
-  fm_field K;                   // tangent (81n or 16n); empty when matrix-free
+  fm_field K;                   // tangent (81n or 16n); empty when matrix-free / compact
+  int compact = 0;              // Simo: keep the 45-slab compact tangent instead of K4
+  fm_field Kc;                  // compact J2 tangent (45n)
   fm_field F_eval;              // F at the last evaluate (matrix-free SVK action)
   fm_field be_c, epsp_c, be_t, epsp_t, f_old;  // Simo history
 };
@@ -185,7 +188,7 @@ int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const doub
 int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const double* be_c,
                     const double* epsp_c, const double* lam, const double* mu,
                     const double* ty0, const double* hard, double* P, double* K, double* be_t,
-                    double* epsp_t);
+                    double* epsp_t, double* Kc = nullptr);
 int reset_bad(fm_ctx* ctx);
 
 // solver.cu -----------------------------------------------------------------

@@ -77,6 +77,52 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
         v[i * TD + j] = s;
       }
     store_dir<NC, DIR>(pa, n, node, df);
+  } else if (PRO == PRO_J2C) {
+    // Compact J2 tangent action (constitutive.cu, simo.cpp:131-194 in the
+    // eigenbasis): D = V^T dF U, W_qp = b_pq D_pq + c_pq D_qp + d_pq sum_r a_pr D_rr,
+    // dP = V W U^T  (== K_jikl dF_kl of the assembled K4).
+    if constexpr (TD == 3) {
+      double d[9];
+      load_dF<9, DIR>(pa, n, node, d);
+      double V[9], U[9], D[9], T[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) {
+        V[e] = __ldg(pa.K + (0 + e) * n + node);
+        U[e] = __ldg(pa.K + (9 + e) * n + node);
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          T[k * 3 + b] = d[k * 3 + 0] * U[0 * 3 + b] + d[k * 3 + 1] * U[1 * 3 + b] + d[k * 3 + 2] * U[2 * 3 + b];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          D[a * 3 + b] = V[0 * 3 + a] * T[0 * 3 + b] + V[1 * 3 + a] * T[1 * 3 + b] + V[2 * 3 + a] * T[2 * 3 + b];
+      double W[9];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        double ap = 0.0;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) ap += __ldg(pa.K + (18 + p * 3 + r) * n + node) * D[r * 3 + r];
+#pragma unroll
+        for (int qq = 0; qq < 3; ++qq)
+          W[qq * 3 + p] = __ldg(pa.K + (27 + p * 3 + qq) * n + node) * D[p * 3 + qq] +
+                          __ldg(pa.K + (36 + p * 3 + qq) * n + node) * D[qq * 3 + p] + (p == qq ? ap : 0.0);
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+          T[i * 3 + p] = V[i * 3 + 0] * W[0 * 3 + p] + V[i * 3 + 1] * W[1 * 3 + p] + V[i * 3 + 2] * W[2 * 3 + p];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          v[i * 3 + j] = T[i * 3 + 0] * U[j * 3 + 0] + T[i * 3 + 1] * U[j * 3 + 1] + T[i * 3 + 2] * U[j * 3 + 2];
+      store_dir<9, DIR>(pa, n, node, d);
+    }
   } else {
     // SVK tangent action (hyperelastic.cpp:55-63 contracted analytically):
     // dP = lam tr(F^T dF) F + mu F dF^T F + mu F F^T dF + dF S

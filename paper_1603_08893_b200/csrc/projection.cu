@@ -298,6 +298,8 @@ void init_generic() {
   allow_smem(k_zfwd<TD, PRO_SVK, false>);
   allow_smem(k_zfwd<TD, PRO_K4, true>);
   allow_smem(k_zfwd<TD, PRO_SVK, true>);
+  allow_smem(k_zfwd<TD, PRO_J2C, false>);
+  allow_smem(k_zfwd<TD, PRO_J2C, true>);
   allow_smem(k_ypass);
   allow_smem(k_xpass<TD>);
   allow_smem(k_zinv<TD>);
@@ -320,6 +322,10 @@ int pass_zf(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* A) {
     k_zfwd<TD, PRO_K4, false><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
   else if (pa.kind == PRO_K4)
     k_zfwd<TD, PRO_K4, true><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
+  else if (pa.kind == PRO_J2C && !dir)
+    k_zfwd<TD, PRO_J2C, false><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
+  else if (pa.kind == PRO_J2C)
+    k_zfwd<TD, PRO_J2C, true><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
   else if (!dir)
     k_zfwd<TD, PRO_SVK, false><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
   else

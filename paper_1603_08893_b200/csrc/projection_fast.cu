@@ -391,6 +391,8 @@ bool zf_launch(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int*
   if (pa.kind == PRO_COPY) zf_go<M, PRO_COPY, false>(ctx, g, pa, spec);
   else if (pa.kind == PRO_K4 && !dir) zf_go<M, PRO_K4, false>(ctx, g, pa, spec);
   else if (pa.kind == PRO_K4) zf_go<M, PRO_K4, true>(ctx, g, pa, spec);
+  else if (pa.kind == PRO_J2C && !dir) zf_go<M, PRO_J2C, false>(ctx, g, pa, spec);
+  else if (pa.kind == PRO_J2C) zf_go<M, PRO_J2C, true>(ctx, g, pa, spec);
   else if (!dir) zf_go<M, PRO_SVK, false>(ctx, g, pa, spec);
   else zf_go<M, PRO_SVK, true>(ctx, g, pa, spec);
   *st = launched(ctx, "k_zf_fast");

@@ -59,6 +59,9 @@ Op model_op(fm_model* m) {
     op.F = m->F_eval.d;
     op.lam = m->lambda.d;
     op.mu = m->mu.d;
+  } else if (m->kind == 1 && m->compact) {
+    op.kind = PRO_J2C;
+    op.K = m->Kc.d;
   } else {
     op.kind = PRO_K4;
     op.K = m->K.d;
@@ -138,7 +141,8 @@ int model_evaluate(fm_ctx* ctx, fm_model* m, const double* F, double* P) {
                                    cudaMemcpyDeviceToDevice, ctx->stream));
   } else {
     st = simo_eval_async(ctx, F, m->f_old.d, m->be_c.d, m->epsp_c.d, m->lambda.d, m->mu.d,
-                         m->tau_y0.d, m->hard.d, P, m->K.d, m->be_t.d, m->epsp_t.d);
+                         m->tau_y0.d, m->hard.d, P, m->compact ? nullptr : m->K.d, m->be_t.d, m->epsp_t.d,
+                         m->compact ? m->Kc.d : nullptr);
   }
   if (st) return st;
   return check_bad(ctx);

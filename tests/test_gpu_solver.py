@@ -18,9 +18,9 @@ def rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-def gpu_run(points, tdim, kind, lam, mu, fbars, ty=None, h=None, matrix_free=False, **prm):
+def gpu_run(points, tdim, kind, lam, mu, fbars, ty=None, h=None, matrix_free=False, compact=False, **prm):
     with abi.Context(points, tdim) as ctx:
-        model = abi.Model(ctx, kind, lam, mu, ty, h, matrix_free=matrix_free)
+        model = abi.Model(ctx, kind, lam, mu, ty, h, matrix_free=matrix_free, compact=compact)
         F = ctx.field(tdim * tdim, abi.identity_field(points, tdim))
         P = ctx.field(tdim * tdim)
         reps = abi.run_program(model, F, fbars, P_out=P, **prm)
@@ -121,7 +121,8 @@ def _as_reps(passes, cg):
     return [{"passes": int(p), "cg_it": [int(v) for v in c[:int(p)]]} for p, c in zip(passes, cg)]
 
 
-def test_cube_simo_matches_oracle(oracle):
+@pytest.mark.parametrize("compact", [False, True])
+def test_cube_simo_matches_oracle(oracle, compact):
     pts = (7, 7, 7)
     pg = M.corner_cube(pts, 3)
     phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
@@ -131,14 +132,15 @@ def test_cube_simo_matches_oracle(oracle):
     F_ref, P_ref, reps_ref, st, ep_ref = oracle.run_program(pts, 3, 1, lam, mu, fb, ty0=ty, hard=h)
     assert st == 0
     band = [oracle.run_program(pts, 3, 1, lam * (1 + s), mu, fb, ty0=ty, hard=h)[2] for s in (1e-15, -1e-15)]
-    F, P, reps, ep = gpu_run(pts, 3, "simo", lam, mu, fb, ty, h)
+    F, P, reps, ep = gpu_run(pts, 3, "simo", lam, mu, fb, ty, h, compact=compact)
     assert_counts(reps, reps_ref, band)
     assert rel(F, F_ref) < 1e-9 and rel(P, P_ref) < 1e-9
     assert np.max(np.abs(ep - ep_ref)) < 1e-9 * max(1e-3, np.max(ep_ref))
     assert np.max(ep_ref) > 0.0  # the program yields
 
 
-def test_cube_simo16_matches_golden():
+@pytest.mark.parametrize("compact", [False, True])
+def test_cube_simo16_matches_golden(compact):
     """16^3 J2, ~100-300 CG iterations per pass: counts are checked against
     the oracle's envelope under six 1e-15-level parameter perturbations
     (tests/golden/make_golden.py simo16)."""
@@ -151,7 +153,7 @@ def test_cube_simo16_matches_golden():
     phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
               M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
     lam, mu, ty, h = M.bind_parameters(pg, phases)
-    F, P, reps, ep = gpu_run(pts, 3, "simo", lam, mu, M.simple_shear_program(0.02, 4, 3), ty, h)
+    F, P, reps, ep = gpu_run(pts, 3, "simo", lam, mu, M.simple_shear_program(0.02, 4, 3), ty, h, compact=compact)
     band = [_as_reps(bp, bc) for bp, bc in zip(g["band_passes"], g["band_cg_it"])]
     assert_counts(reps, _as_reps(g["passes"], g["cg_it"]), band)
     assert rel(F, g["F"]) < 1e-9 and rel(P, g["P"]) < 1e-9
@@ -171,7 +173,8 @@ def test_config0_matches_golden():
         assert rel(F, g["F"]) < 1e-9 and rel(P, g["P"]) < 1e-9
 
 
-def test_config1_matches_golden():
+@pytest.mark.parametrize("compact", [False, True])
+def test_config1_matches_golden(compact):
     """BASELINE config 1: 31^3 finite-strain J2, 20 increments to gamma 0.1."""
     path = os.path.join(GOLD, "config1.npz")
     if not os.path.exists(path):
@@ -182,7 +185,7 @@ def test_config1_matches_golden():
     phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
               M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
     lam, mu, ty, h = M.bind_parameters(pg, phases)
-    F, P, reps, ep = gpu_run(pts, 3, "simo", lam, mu, M.simple_shear_program(0.1, 20, 3), ty, h)
+    F, P, reps, ep = gpu_run(pts, 3, "simo", lam, mu, M.simple_shear_program(0.1, 20, 3), ty, h, compact=compact)
     as_reps = lambda z: [{"cg_it": [int(v) for v in z["cg_it"][t][:int(z["passes"][t])]],
                           "passes": int(z["passes"][t])} for t in range(len(z["passes"]))]
     band = [as_reps(np.load(os.path.join(GOLD, f"config1_band_{s}.npz"))) for s in ("p", "m")
