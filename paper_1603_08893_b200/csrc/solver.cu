@@ -101,7 +101,8 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
     return FM_OK;
   }
   const int64_t cap = max_cg > 0 ? max_cg : ctx->n_global * ctx->ncomp;  // :27-29 (int64: no overflow past 620^3)
-  FM_CUDA(ctx, cudaMemcpyAsync(ctx->r.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (b != ctx->r.d)  // the Newton driver builds its rhs in r directly (saves a field at 512^3)
+    FM_CUDA(ctx, cudaMemcpyAsync(ctx->r.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
   FM_CUDA(ctx, cudaMemcpyAsync(ctx->p.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
   double rr = ctx->h_scal[S_RR];
   for (int64_t it = 1; it <= cap; ++it) {
@@ -193,8 +194,12 @@ int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
   double* F = Ff->d;
   if (int st = ensure_field(ctx, ctx->Pw, nc)) return st;
   if (int st = ensure_field(ctx, ctx->dF, nc)) return st;
-  if (int st = ensure_field(ctx, ctx->rhs, nc)) return st;
-  if (int st = ensure_field(ctx, ctx->tmp, nc)) return st;
+  // rhs lives in the CG residual r and the scratch field in Ap: both are CG
+  // workspace that is free whenever the driver needs them.
+  for (fm_field* f : {&ctx->r, &ctx->p, &ctx->Ap})
+    if (int st = ensure_field(ctx, *f, nc)) return st;
+  double* rhs = ctx->r.d;
+  double* tmp = ctx->Ap.d;
   double* P = ctx->Pw.d;
   const auto finish = [&](bool conv) {
     rep->converged = conv ? 1 : 0;
@@ -217,12 +222,12 @@ int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
     double mean[9], dfbar[9];
     if (int st = mean_sync(ctx, F, mean)) return st;
     for (int c = 0; c < nc; ++c) dfbar[c] = fbar[c] - mean[c];
-    if (int st = fill_uniform_async(ctx, ctx->tmp.d, dfbar, nc, ctx->n)) return st;
-    if (int st = op_apply(ctx, op, ctx->tmp.d, ctx->rhs.d, -1.0)) return st;  // rhs = -G(K:dFbar^T)
+    if (int st = fill_uniform_async(ctx, tmp, dfbar, nc, ctx->n)) return st;
+    if (int st = op_apply(ctx, op, tmp, rhs, -1.0)) return st;  // rhs = -G(K:dFbar^T)
     rep->matvecs++;
     int32_t it = 0;
     double rel = 0.0;
-    if (int st = cg_run(ctx, op, ctx->rhs.d, prm.eta_cg, prm.max_cg, ctx->dF.d, &it, &rel)) {
+    if (int st = cg_run(ctx, op, rhs, prm.eta_cg, prm.max_cg, ctx->dF.d, &it, &rel)) {
       finish(false);
       return st;
     }
@@ -247,10 +252,10 @@ int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
                        "Newton did not converge within " + std::to_string(rep->n_passes) + " passes");
     }
     if (int st = model_evaluate(ctx, m, F, P)) return st;
-    if (int st = op_apply(ctx, Op{PRO_COPY}, P, ctx->rhs.d, -1.0)) return st;  // rhs = -G(P)
+    if (int st = op_apply(ctx, Op{PRO_COPY}, P, rhs, -1.0)) return st;  // rhs = -G(P)
     int32_t it = 0;
     double rel = 0.0;
-    if (int st = cg_run(ctx, op, ctx->rhs.d, prm.eta_cg, prm.max_cg, ctx->dF.d, &it, &rel)) {
+    if (int st = cg_run(ctx, op, rhs, prm.eta_cg, prm.max_cg, ctx->dF.d, &it, &rel)) {
       finish(false);
       return st;
     }
@@ -273,9 +278,9 @@ int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
   double pnorm;
   if (int st = norm_sync(ctx, P, count, &pnorm)) return st;
   if (pnorm > 0.0) {
-    if (int st = op_apply(ctx, Op{PRO_COPY}, P, ctx->tmp.d, 1.0)) return st;
+    if (int st = op_apply(ctx, Op{PRO_COPY}, P, tmp, 1.0)) return st;
     double gn;
-    if (int st = norm_sync(ctx, ctx->tmp.d, count, &gn)) return st;
+    if (int st = norm_sync(ctx, tmp, count, &gn)) return st;
     rep->equilibrium_rel_residual = gn / pnorm;
   }
   if (int st = model_commit(ctx, m, F)) return st;

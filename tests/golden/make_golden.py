@@ -113,3 +113,26 @@ if __name__ == "__main__":
         config0()
     if "1" in which:
         config1()
+
+
+def config3_reduced():
+    """Config 3's generator on a reduced grid (64^3, radius 2, seed 3, 10
+    increments to gamma 0.05) -- the parity case for the 512^3 J2 run."""
+    N, r = 64, 2
+    pg, frac, count = M.random_spheres(N, r, 0.25, 3)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    t = time.time()
+    F, P, reps, st, epsp = O.run_program((N, N, N), 3, 1, lam, mu, M.simple_shear_program(0.05, 10, 3),
+                                         ty0=ty, hard=h)
+    assert st == 0, st
+    pad = lambda rr: rr["cg_it"] + [0] * (64 - len(rr["cg_it"]))
+    np.savez_compressed(os.path.join(HERE, "config3_64.npz"), F=F, P=P, epsp=epsp,
+                        passes=np.array([rr["passes"] for rr in reps]), cg_it=np.array([pad(rr) for rr in reps]),
+                        fraction=frac, spheres=count)
+    print("config3_64", time.time() - t, frac, count, [rr["cg_it"] for rr in reps])
+
+
+if __name__ == "__main__" and "config3" in sys.argv[1:]:
+    config3_reduced()
