@@ -169,6 +169,88 @@ __global__ void __launch_bounds__(TW*(N / E)) k_x_fast2(Geo g, const double2* __
   }
 }
 
+// x pass, prefetching variant: the whole tile (3 components x N x TW) is
+// requested from HBM at once with cp.async (16 B per request, 8 lanes per
+// 128-byte row) so all of it is in flight together; the components are then
+// transformed one at a time out of shared memory, projected on the
+// thread-owned positions, transformed back and stored.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+template <int N, int TW, int E>
+__global__ void __launch_bounds__(TW*(N / E)) k_x_fast3(Geo g, const double2* __restrict__ tw,
+                                                       double2* __restrict__ spec) {
+  constexpr int T = N / E;
+  extern __shared__ double2 sm[];
+  const int l = threadIdx.x % TW, t = threadIdx.x / TW;
+  const int kz = blockIdx.x * TW + l;
+  const int y = blockIdx.y, i = blockIdx.z;
+  const int64_t xstride = int64_t(g.Ny) * g.nzh;
+  double2* tile = spec + int64_t(i * 3) * N * xstride + int64_t(y) * g.nzh + blockIdx.x * TW;
+  for (int w = threadIdx.x; w < 3 * N * TW; w += blockDim.x) {
+    const int row = w / TW, ll = w - row * TW;  // row = j * N + e
+    cp_async16(sm + w, tile + int64_t(row) * xstride + ll);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  double2* base = tile + l;
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    double2* S = sm + j * N * TW + l;
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = S[(t + T * m) * TW];
+    __syncthreads();
+    reg::fft<N, E, -1>(v, S, TW, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) S[(t + T * m) * TW] = v[m];
+  }
+  const int yg = g.y0 + y;
+  const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
+  const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+  const double xiy = qy * g.invL[1], xiz = (g.dim == 3) ? qz * g.invL[2] : 0.0;
+#pragma unroll 2
+  for (int m = 0; m < E; ++m) {  // own positions only: no barrier needed
+    const int kx = t + T * m;
+    double2* s0 = sm + kx * TW + l;
+    const double xix = freq_of(kx, N) * g.invL[0];
+    const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
+    const bool nyq = nyq_yz || (kx == N / 2);
+    double2 a0 = s0[0], a1 = s0[N * TW], a2 = s0[2 * N * TW];
+    if (norm2 == 0.0 || (nyq && g.mode == FM_NYQUIST_ZERO_COMPATIBLE)) {
+      a0 = a1 = a2 = make_double2(0.0, 0.0);
+    } else if (!nyq) {
+      const double sx = a0.x * xix + a1.x * xiy + a2.x * xiz;
+      const double sy = a0.y * xix + a1.y * xiy + a2.y * xiz;
+      const double inv = 1.0 / norm2;
+      const double f0 = xix * inv, f1 = xiy * inv, f2 = xiz * inv;
+      a0 = make_double2(sx * f0, sy * f0);
+      a1 = make_double2(sx * f1, sy * f1);
+      a2 = make_double2(sx * f2, sy * f2);
+    }
+    s0[0] = a0;
+    s0[N * TW] = a1;
+    s0[2 * N * TW] = a2;
+  }
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    double2 v[E];
+    double2* S = sm + j * N * TW + l;
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = S[(t + T * m) * TW];
+    __syncthreads();
+    reg::fft<N, E, +1>(v, S, TW, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
+  }
+}
+
 // --------------------------------------------------------------- z passes
 // HEAVY: K4 / SVK prologue (720 B read per voxel): larger E, ~144 threads and
 // ~40 KB per CTA so 4 CTAs per SM overlap their load and FFT phases.
@@ -191,18 +273,37 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
   using S = ZShape<M, PRO != PRO_COPY>;
   constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
   extern __shared__ double2 sm[];
-  double* smd = reinterpret_cast<double*>(sm);
   const int nxy = g.Nx * g.Ny;
   const int L0 = blockIdx.x * G;
   const int Gb = min(G, nxy - L0);
   // phase 1: prologue, one thread per voxel; z -> packed complex m = z/2
-  for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
-    const int gi = w / N, z = w - gi * N;
-    const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
-    double v[9];
-    prologue_voxel<3, PRO, DIR>(pa, g.n, node, v);
+  // voxel pairs (z, z+1) per thread: both voxels' loads in flight together,
+  // one 16-byte shared store per component (the packed complex z_m)
+  // light prologues (copy, SVK action): voxel pairs (z, z+1) per thread, both
+  // voxels' loads in flight together and one 16-byte shared store per
+  // component; heavy ones (K4, compact J2) one voxel per thread (registers)
+  constexpr bool PAIRS = (PRO == PRO_COPY || PRO == PRO_SVK);
+  if constexpr (PAIRS) {
+    constexpr int N2 = N / 2;
+    for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
+      const int gi = w / N2, m = w - gi * N2;
+      const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
+      double v0[9], v1[9];
+      prologue_voxel<3, PRO, DIR>(pa, g.n, node, v0);
+      prologue_voxel<3, PRO, DIR>(pa, g.n, node + 1, v1);
 #pragma unroll
-    for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] = v[c];
+      for (int c = 0; c < 9; ++c) sm[m * LSP + c * G + gi] = make_double2(v0[c], v1[c]);
+    }
+  } else {
+    double* smd = reinterpret_cast<double*>(sm);
+    for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
+      const int gi = w / N, z = w - gi * N;
+      const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
+      double v[9];
+      prologue_voxel<3, PRO, DIR>(pa, g.n, node, v);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] = v[c];
+    }
   }
   __syncthreads();
   // phase 2: M-point complex FFT of every line, lines fastest across lanes
@@ -240,7 +341,6 @@ __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const dou
   using S = ZShape<M>;
   constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
   extern __shared__ double2 sm[];
-  double* smd = reinterpret_cast<double*>(sm);
   const int nxy = g.Nx * g.Ny;
   const int L0 = blockIdx.x * G;
   const int Gb = min(G, nxy - L0);
@@ -282,15 +382,23 @@ __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const dou
     for (int m = 0; m < E; ++m) sm[(t + T * m) * LSP + l] = v[m];
   }
   __syncthreads();
+  // epilogue on z pairs: one 16-byte shared read and one 16-byte store per
+  // component (node is even: N, the slab offset and the slab stride are even)
   double dot = 0.0;
-  for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
-    const int gi = w / N, z = w - gi * N;
-    const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
+  constexpr int N2 = N / 2;
+  for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
+    const int gi = w / N2, m = w - gi * N2;
+    const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
-      const double val = smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] * scale;
-      out[c * g.n + node] = val;
-      if (epi.partial) dot += __ldg(epi.pdot + c * g.n + node) * val;
+      const double2 zz = sm[m * LSP + c * G + gi];
+      const double2 val = make_double2(zz.x * scale, zz.y * scale);
+      *reinterpret_cast<double2*>(out + c * g.n + node) = val;
+      if (epi.partial) {
+        const double2 pp = __ldg(reinterpret_cast<const double2*>(epi.pdot + c * g.n + node));
+        dot += pp.x * val.x;
+        dot += pp.y * val.y;
+      }
     }
   }
   if (epi.partial) {  // fused <p, Ap> partial (solver.cpp:37)
@@ -339,7 +447,7 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
 int x_variant() {
   static int v = [] {
     const char* e = getenv("FM_XPASS");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 5;
   }();
   return v;
 }
@@ -355,13 +463,27 @@ void x2_go(fm_ctx* ctx, const Geo& g, double2* spec) {
   k_x_fast2<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
 
+template <int N, int TW, int E>
+void x3_go(fm_ctx* ctx, const Geo& g, double2* spec) {
+  constexpr int T = N / E;
+  const size_t smem = size_t(3) * N * TW * 16;
+  static bool a = (allow(k_x_fast3<N, TW, E>, smem), true);
+  (void)a;
+  const dim3 grid(ctx->nzh / TW, g.Ny, 3);
+  k_x_fast3<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+}
+
 template <int N>
 bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   constexpr int TW = tw_x(N);
   constexpr int T = N / e_x(N);
   const size_t smem = size_t(N) * TW * 16;
   const int var = (N <= 512 && ctx->nzh % 8 == 0) ? x_variant() : 1;
-  if (var == 2) {
+  if (var == 4 && N <= 256) {
+    x3_go<N, 4, e_line(N)>(ctx, g, spec);
+  } else if (var == 5 && N <= 512) {
+    x3_go<N, 8, e_line(N)>(ctx, g, spec);
+  } else if (var == 2) {
     x2_go<N, e_line(N)>(ctx, g, spec);
   } else if (var == 3) {
     x2_go<N, e_x(N)>(ctx, g, spec);

@@ -11,7 +11,7 @@ rng = np.random.default_rng(0)
 K = ctx.field(81)
 abi.lib().fm_field_fill(ctx.h, K.h, 0.0)
 lam = np.full(n, 0.5769); mu = np.full(n, 0.3846)
-model = abi.Model(ctx, "hyper", lam, mu)
+model = abi.Model(ctx, "hyper", lam, mu, matrix_free=len(sys.argv) > 3 and sys.argv[3] == "mf")
 F0 = abi.identity_field((N, N, N), 3); F0[n:2 * n] = 0.1
 F = ctx.field(9, F0); P = ctx.field(9)
 model.evaluate(F, P)
