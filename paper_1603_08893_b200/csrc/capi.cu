@@ -167,6 +167,7 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
 int fm_ctx_destroy(fm_ctx* ctx) {
   if (!ctx) return FM_OK;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->cg_exec) cudaGraphExecDestroy(ctx->cg_exec);
   release_field(ctx->r);
   release_field(ctx->p);
   release_field(ctx->Ap);

@@ -95,6 +95,12 @@ struct fm_ctx {
   int64_t spec_rank_elems = 0;    // complex elements of one rank's spectral buffer
   void* nccl = nullptr;           // ncclComm_t when distributed over devices
   double* d_gather = nullptr;     // all-gather staging of per-rank scalars
+  // CG loop as one CUDA graph (a while-conditional node around the fused
+  // iteration): cached for the last (operator, vectors) it was built for
+  bool capturing = false;
+  cudaGraphExec_t cg_exec = nullptr;
+  int64_t cg_iter_launches = 0;   // kernels per graph iteration
+  std::vector<const void*> cg_key;
   // reductions
   int red_blocks = 0;
   double* d_partial = nullptr;  // red_blocks * 16

@@ -277,7 +277,7 @@ ZLaunch z_launch(const fm_ctx* ctx, const Geo& g) {
 }
 
 void prof_mark(fm_ctx* ctx) {
-  if (!ctx->prof.on) return;
+  if (!ctx->prof.on || ctx->capturing) return;
   cudaEvent_t e;
   if (!ctx->prof.pool.empty()) {
     e = ctx->prof.pool.back();
