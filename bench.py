@@ -316,6 +316,32 @@ def main():
                   "cg_iterations": rep["cg_it"], "matvecs": rep["matvecs"], "rel_update": rep["rel_update"]}
         model2.close()
 
+    # ---- Newton solve time of the latency-bound 31^3 configurations (0, 1)
+    small = None
+    if world == 1 and not args.no_e2e:
+        from paper_1603_08893_b200 import microstructure as M
+        small = {}
+        el = [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)]
+        pl = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+        for name, kind, phases, prog in [("config0", "hyper", el, M.simple_shear_program(0.1, 1, 3)),
+                                         ("config1", "simo", pl, M.simple_shear_program(0.1, 20, 3))]:
+            pts = (31, 31, 31)
+            lam31, mu31, ty31, h31 = M.bind_parameters(M.corner_cube(pts, 9), phases)
+            with abi.Context(pts, 3, device=local) as c31:
+                for rep_i in range(2):  # second run timed (first-use module loads excluded)
+                    m31 = abi.Model(c31, kind, lam31, mu31, ty31, h31)
+                    F31 = c31.field(9, abi.identity_field(pts, 3))
+                    c31.sync()
+                    t0 = time.perf_counter()
+                    reps31 = abi.run_program(m31, F31, prog)
+                    c31.sync()
+                    wall31 = time.perf_counter() - t0
+                    m31.close()
+            small[name] = {"solve_s": wall31, "increments": len(reps31),
+                           "newton": [r["passes"] for r in reps31],
+                           "cg_total": int(sum(sum(r["cg_it"]) for r in reps31))}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -340,6 +366,7 @@ def main():
                        "operator": "matrix-free SVK",
                        "l2": "inputs 12 GB > 126 MB L2, no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "newton_solve": newton,
+            "newton_solve_31": small,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line))

@@ -251,6 +251,84 @@ __global__ void __launch_bounds__(TW*(N / E)) k_x_fast3(Geo g, const double2* __
   }
 }
 
+// x pass, scalar-accumulating variant (ZeroCompatible mode only).  The
+// projection of row i is Bhat_ij = s xi_j / |xi|^2 with s = sum_q Ahat_iq xi_q,
+// so the three forward transforms only have to accumulate s in registers:
+// per thread E values of s plus E working values, instead of all 3 x E.
+// Component tiles (N x TW) are double-buffered in shared memory with cp.async
+// (component q+2 streams in while q is transformed) and each buffer doubles
+// as the transform's exchange scratch; the inverse transforms store straight
+// from registers.  64 KB per CTA at N = 256, TW = 8.
+template <int N, int TW, int E>
+__global__ void __launch_bounds__(TW*(N / E), E >= 16 ? 3 : 2) k_x_fast4(Geo g, const double2* __restrict__ tw,
+                                                       double2* __restrict__ spec) {
+  constexpr int T = N / E;
+  extern __shared__ double2 sm[];
+  const int l = threadIdx.x % TW, t = threadIdx.x / TW;
+  const int kz = blockIdx.x * TW + l;
+  const int y = blockIdx.y, i = blockIdx.z;
+  const int64_t xstride = int64_t(g.Ny) * g.nzh;
+  double2* tile = spec + int64_t(i * 3) * N * xstride + int64_t(y) * g.nzh + blockIdx.x * TW;
+  auto fetch = [&](int q, double2* buf) {
+    const double2* src = tile + int64_t(q) * N * xstride;
+    for (int w = threadIdx.x; w < N * TW; w += blockDim.x) {
+      const int row = w / TW, ll = w - row * TW;
+      cp_async16(buf + w, src + int64_t(row) * xstride + ll);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double2* buf0 = sm;
+  double2* buf1 = sm + N * TW;
+  fetch(0, buf0);
+  fetch(1, buf1);
+  const int yg = g.y0 + y;
+  const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
+  const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+  const double xiy = qy * g.invL[1], xiz = qz * g.invL[2];
+  double2 s[E], v[E];
+#pragma unroll 1
+  for (int q = 0; q < 3; ++q) {
+    double2* B = (q == 1) ? buf1 : buf0;
+    if (q < 2) asm volatile("cp.async.wait_group 1;\n" ::);
+    else asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = B[(t + T * m) * TW + l];
+    __syncthreads();
+    reg::fft<N, E, -1>(v, B + l, TW, t, tw);  // ends past a barrier: B is free again
+    if (q == 0) fetch(2, buf0);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const double xq = q == 0 ? freq_of(t + T * m, N) * g.invL[0] : (q == 1 ? xiy : xiz);
+      if (q == 0) s[m] = make_double2(v[m].x * xq, v[m].y * xq);
+      else s[m] = make_double2(fma(v[m].x, xq, s[m].x), fma(v[m].y, xq, s[m].y));
+    }
+  }
+  // s <- s / |xi|^2, zero at xi = 0 and on Nyquist planes (ZeroCompatible)
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int kx = t + T * m;
+    const double xix = freq_of(kx, N) * g.invL[0];
+    const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
+    const bool zero = norm2 == 0.0 || nyq_yz || kx == N / 2;
+    const double inv = zero ? 0.0 : 1.0 / norm2;
+    s[m] = make_double2(s[m].x * inv, s[m].y * inv);
+  }
+  double2* base = tile + l;
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    double2* B = (j == 1) ? buf0 : buf1;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const double f = j == 0 ? freq_of(t + T * m, N) * g.invL[0] : (j == 1 ? xiy : xiz);
+      v[m] = make_double2(s[m].x * f, s[m].y * f);
+    }
+    reg::fft<N, E, +1>(v, B + l, TW, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
+  }
+}
+
 // --------------------------------------------------------------- z passes
 // HEAVY: K4 / SVK prologue (720 B read per voxel): larger E, ~144 threads and
 // ~40 KB per CTA so 4 CTAs per SM overlap their load and FFT phases.
@@ -333,7 +411,7 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
 }
 
 template <int M>
-__global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const double2* __restrict__ twM,
+__global__ void __launch_bounds__(ZShape<M>::THREADS, 4) k_zi_fast(Geo g, const double2* __restrict__ twM,
                                                                 const double2* __restrict__ twN,
                                                                 const double2* __restrict__ spec,
                                                                 double* __restrict__ out, double scale,
@@ -350,32 +428,21 @@ __global__ void __launch_bounds__(ZShape<M>::THREADS) k_zi_fast(Geo g, const dou
     sm[k * LSP + c * G + gi] = spec[(int64_t(c) * nxy + L0 + gi) * M + k];
   }
   __syncthreads();
-  // Z[k] = (X[k] + X*[M-k]) + i W_N^-k (X[k] - X*[M-k]), X[M] = 0 (ZeroCompatible)
-  constexpr int H = M / 2 + 1;
-  for (int w = threadIdx.x; w < 9 * Gb * H; w += blockDim.x) {
-    const int c = w / (Gb * H), rem = w - c * (Gb * H);
-    const int gi = rem / H, k = rem - gi * H;
-    const int l = c * G + gi;
-    double2 xk = sm[k * LSP + l];
-    if (k == 0) xk.y = 0.0;  // Re(ifft): drop the round-off imaginary part of kz = 0
-    const double2 xm = k == 0 ? make_double2(0.0, 0.0) : sm[(M - k) * LSP + l];
-    {
-      const double2 b = cconj(xm);
-      const double2 t = cmulc(csub(xk, b), __ldg(&twN[k]));
-      sm[k * LSP + l] = make_double2(xk.x + b.x - t.y, xk.y + b.y + t.x);
-    }
-    if (k > 0 && k < M - k) {
-      const double2 b = cconj(xk);
-      const double2 t = cmulc(csub(xm, b), __ldg(&twN[M - k]));
-      sm[(M - k) * LSP + l] = make_double2(xm.x + b.x - t.y, xm.y + b.y + t.x);
-    }
-  }
-  __syncthreads();
+  // Z[k] = (X[k] + X*[M-k]) + i W_N^-k (X[k] - X*[M-k]), X[M] = 0 (ZeroCompatible),
+  // formed straight into the registers of the thread that transforms Z[k]
   {
     const int l = threadIdx.x % S::LSL, t = threadIdx.x / S::LSL;
     double2 v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = sm[(t + T * m) * LSP + l];
+    for (int m = 0; m < E; ++m) {
+      const int k = t + T * m;
+      double2 xk = sm[k * LSP + l];
+      double2 b = make_double2(0.0, 0.0);
+      if (k == 0) xk.y = 0.0;  // Re(ifft): drop the round-off imaginary part of kz = 0
+      else b = cconj(sm[(M - k) * LSP + l]);
+      const double2 tt = cmulc(csub(xk, b), __ldg(&twN[k]));
+      v[m] = make_double2(xk.x + b.x - tt.y, xk.y + b.y + tt.x);
+    }
     __syncthreads();
     reg::fft<M, E, +1>(v, sm + l, LSP, t, twM);
 #pragma unroll
@@ -447,7 +514,7 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
 int x_variant() {
   static int v = [] {
     const char* e = getenv("FM_XPASS");
-    return e ? atoi(e) : 5;
+    return e ? atoi(e) : 0;
   }();
   return v;
 }
@@ -473,13 +540,30 @@ void x3_go(fm_ctx* ctx, const Geo& g, double2* spec) {
   k_x_fast3<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
 
+template <int N, int TW, int E>
+void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
+  constexpr int T = N / E;
+  const size_t smem = size_t(2) * N * TW * 16;
+  static bool a = (allow(k_x_fast4<N, TW, E>, smem), true);
+  (void)a;
+  const dim3 grid(ctx->nzh / TW, g.Ny, 3);
+  k_x_fast4<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+}
+
 template <int N>
 bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   constexpr int TW = tw_x(N);
   constexpr int T = N / e_x(N);
   const size_t smem = size_t(N) * TW * 16;
-  const int var = (N <= 512 && ctx->nzh % 8 == 0) ? x_variant() : 1;
-  if (var == 4 && N <= 256) {
+  // default: scalar-accumulating variant up to 256 (3 CTAs/SM), whole-tile
+  // prefetch at 512 (measured, scripts/xvar.py)
+  const int vdef = (ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE && N <= 256) ? 6 : 5;
+  const int var = (N <= 512 && ctx->nzh % 8 == 0) ? (x_variant() ? x_variant() : vdef) : 1;
+  if (var >= 6 && N >= 64 && N <= 512 && ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE) {
+    if (var == 6) x4_go<N, 8, e_line(N)>(ctx, g, spec);
+    else if (var == 8) x4_go<N, 4, e_line(N)>(ctx, g, spec);
+    else x4_go<N, 8, 8>(ctx, g, spec);
+  } else if (var == 4 && N <= 256) {
     x3_go<N, 4, e_line(N)>(ctx, g, spec);
   } else if (var == 5 && N <= 512) {
     x3_go<N, 8, e_line(N)>(ctx, g, spec);
