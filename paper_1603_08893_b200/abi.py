@@ -280,6 +280,11 @@ class Context:
         self.check(lib().fm_norm(self.h, a.h, C.byref(r)))
         return r.value
 
+    def axpy(self, a, x, y):
+        """y += a x (device)."""
+        self.check(lib().fm_axpy(self.h, C.c_double(a), x.h, y.h))
+        return y
+
     def mean(self, a):
         out = np.zeros(a.ncomp)
         self.check(lib().fm_mean(self.h, a.h, out))

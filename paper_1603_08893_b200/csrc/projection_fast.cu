@@ -13,8 +13,10 @@
 //   x pass   : one thread holds all 3 components of its row, so the
 //              projection Bhat_i. = (Ahat_i . xi) xi / |xi|^2 is applied in
 //              registers between the forward and inverse x transforms.
+#include <algorithm>
 #include <cstdlib>
 
+#include "bulk.cuh"
 #include "proj_common.cuh"
 
 namespace fm {
@@ -332,17 +334,25 @@ __global__ void __launch_bounds__(TW*(N / E), E >= 16 ? 3 : 2) k_x_fast4(Geo g, 
 // --------------------------------------------------------------- z passes
 // HEAVY: K4 / SVK prologue (720 B read per voxel): larger E, ~144 threads and
 // ~40 KB per CTA so 4 CTAs per SM overlap their load and FFT phases.
-template <int M, bool HEAVY = false>
-struct ZShape {
-  static constexpr int E = HEAVY ? e_line(M) : reg::e_z(M);
+template <int M, int E_, int G_>
+struct ZS {
+  static constexpr int E = E_;
   static constexpr int T = M / E;
-  static constexpr int TT = HEAVY ? 16 : 32;
-  static constexpr int G = T >= TT ? 1 : TT / T;  // z-lines per CTA
+  static constexpr int G = G_;                     // z-lines per CTA
   static constexpr int LSL = 9 * G;                // smem lines (9 components x G)
   static constexpr int LSP = LSL | 1;              // odd pitch: conflict-free strided access
   static constexpr int THREADS = LSL * T;
   static constexpr size_t SMEM = size_t(M) * LSP * 16;
 };
+template <int M, bool HEAVY = false>
+struct ZShapeSel {
+  static constexpr int E = HEAVY ? e_line(M) : reg::e_z(M);
+  static constexpr int T = M / E;
+  static constexpr int TT = HEAVY ? 16 : 32;
+  using type = ZS<M, E, (T >= TT ? 1 : TT / T)>;
+};
+template <int M, bool HEAVY = false>
+using ZShape = typename ZShapeSel<M, HEAVY>::type;
 
 template <int M, int PRO, bool DIR>
 __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast(Geo g, const double2* __restrict__ twM,
@@ -410,23 +420,182 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
   }
 }
 
+// Pipelined z-forward pass for the light prologues (projection input copy,
+// matrix-free SVK action, optionally fused with the CG direction update):
+// a persistent CTA walks z-lines; one thread streams the next line's inputs
+// (contiguous N-voxel chunks of every input component: 9 / 20 / 29 of them)
+// into a shared staging area with TMA bulk copies while the CTA transforms
+// the current line, so HBM reads stay in flight through the FFT phases.
 template <int M>
-__global__ void __launch_bounds__(ZShape<M>::THREADS, 4) k_zi_fast(Geo g, const double2* __restrict__ twM,
-                                                                const double2* __restrict__ twN,
-                                                                const double2* __restrict__ spec,
-                                                                double* __restrict__ out, double scale,
-                                                                EpiArgs epi) {
-  using S = ZShape<M>;
+struct ZPipe {
+  static constexpr int E = reg::e_z(M), T = M / E;
+  static constexpr int LSP = 9;  // one line per CTA, 9 components (odd pitch)
+  static constexpr int THREADS = 9 * T;
+  static constexpr size_t FFT_SM = size_t(M) * LSP * 16;
+};
+template <int PRO, bool DIR>
+constexpr int pipe_chunks() {
+  return PRO == PRO_COPY ? 9 : (DIR ? 29 : 20);
+}
+template <int M, int PRO, bool DIR>
+constexpr size_t pipe_smem() {
+  return ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR>()) * 2 * M * 8;
+}
+
+template <int M, int PRO, bool DIR, int MINB, bool PAIRS = true>
+__global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, const double2* __restrict__ twM,
+                                                               const double2* __restrict__ twN, ProArgs pa,
+                                                               double2* __restrict__ spec) {
+  using S = ZPipe<M>;
+  constexpr int N = 2 * M, LSP = S::LSP, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR>();
+  extern __shared__ __align__(16) double2 sm[];
+  double* stage = reinterpret_cast<double*>(sm + M * LSP);  // NCH chunks of N doubles
+  __shared__ uint64_t bar;
+  const int nxy = g.Nx * g.Ny;
+  const int64_t n = g.n;
+  auto issue = [&](int L) {
+    const int64_t node0 = g.roff + int64_t(L) * N;
+    bulk::mbar_expect_tx(&bar, NCH * N * 8);
+    int q = 0;
+    auto cp = [&](const double* base) { bulk::g2s(stage + (q++) * N, base + node0, N * 8, &bar); };
+    if constexpr (PRO == PRO_COPY) {
+      for (int c = 0; c < 9; ++c) cp(pa.A + c * n);
+    } else {
+      if constexpr (DIR) {
+        for (int c = 0; c < 9; ++c) cp(pa.r + c * n);
+        for (int c = 0; c < 9; ++c) cp(pa.p + c * n);
+      } else {
+        for (int c = 0; c < 9; ++c) cp(pa.A + c * n);
+      }
+      for (int c = 0; c < 9; ++c) cp(pa.F + c * n);
+      cp(pa.lam);
+      cp(pa.mu);
+    }
+  };
+  if (threadIdx.x == 0) bulk::mbar_init(&bar, 1);
+  __syncthreads();
+  int L = blockIdx.x;
+  if (threadIdx.x == 0 && L < nxy) issue(L);
+  unsigned phase = 0;
+  for (; L < nxy; L += gridDim.x) {
+    bulk::mbar_wait(&bar, phase);
+    phase ^= 1;
+    if constexpr (!PAIRS && PRO == PRO_SVK) {  // one voxel per thread: fewer registers
+      double* smd = reinterpret_cast<double*>(sm);
+      for (int z = threadIdx.x; z < N; z += blockDim.x) {
+        double d[9], f[9], v[9];
+        if constexpr (DIR) {
+          const double beta = *pa.beta;
+#pragma unroll
+          for (int c = 0; c < 9; ++c) d[c] = __dadd_rn(__dmul_rn(stage[(9 + c) * N + z], beta), stage[c * N + z]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 9; ++c) d[c] = stage[c * N + z];
+        }
+        constexpr int FB = DIR ? 18 : 9;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) f[c] = stage[(FB + c) * N + z];
+        svk_action<3>(f, d, stage[(FB + 9) * N + z], stage[(FB + 10) * N + z], v);
+        if constexpr (DIR) {
+          const int64_t node = g.roff + int64_t(L) * N + z;
+#pragma unroll
+          for (int c = 0; c < 9; ++c) pa.p[c * n + node] = d[c];
+        }
+#pragma unroll
+        for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c) * 2 + (z & 1)] = v[c];
+      }
+    } else
+    // prologue on voxel pairs (z, z+1) out of the staging area
+    for (int m = threadIdx.x; m < N / 2; m += blockDim.x) {
+      double v0[9], v1[9];
+      if constexpr (PRO == PRO_COPY) {
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+          const double2 a = *reinterpret_cast<const double2*>(stage + c * N + 2 * m);
+          v0[c] = a.x;
+          v1[c] = a.y;
+        }
+      } else {
+        double d0[9], d1[9], f0[9], f1[9];
+        if constexpr (DIR) {
+          const double beta = *pa.beta;
+#pragma unroll
+          for (int c = 0; c < 9; ++c) {
+            const double2 r = *reinterpret_cast<const double2*>(stage + c * N + 2 * m);
+            const double2 p = *reinterpret_cast<const double2*>(stage + (9 + c) * N + 2 * m);
+            d0[c] = __dadd_rn(__dmul_rn(p.x, beta), r.x);
+            d1[c] = __dadd_rn(__dmul_rn(p.y, beta), r.y);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 9; ++c) {
+            const double2 a = *reinterpret_cast<const double2*>(stage + c * N + 2 * m);
+            d0[c] = a.x;
+            d1[c] = a.y;
+          }
+        }
+        constexpr int FB = DIR ? 18 : 9;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+          const double2 a = *reinterpret_cast<const double2*>(stage + (FB + c) * N + 2 * m);
+          f0[c] = a.x;
+          f1[c] = a.y;
+        }
+        const double2 lm = *reinterpret_cast<const double2*>(stage + (FB + 9) * N + 2 * m);
+        const double2 mu = *reinterpret_cast<const double2*>(stage + (FB + 10) * N + 2 * m);
+        svk_action<3>(f0, d0, lm.x, mu.x, v0);
+        svk_action<3>(f1, d1, lm.y, mu.y, v1);
+        if constexpr (DIR) {
+          const int64_t node = g.roff + int64_t(L) * N + 2 * m;
+#pragma unroll
+          for (int c = 0; c < 9; ++c)
+            *reinterpret_cast<double2*>(pa.p + c * n + node) = make_double2(d0[c], d1[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 9; ++c) sm[m * LSP + c] = make_double2(v0[c], v1[c]);
+    }
+    __syncthreads();  // staging consumed, packed line in sm
+    if (threadIdx.x == 0 && L + int(gridDim.x) < nxy) issue(L + gridDim.x);
+    {
+      const int l = threadIdx.x % 9, t = threadIdx.x / 9;
+      double2 v[E];
+#pragma unroll
+      for (int m = 0; m < E; ++m) v[m] = sm[(t + T * m) * LSP + l];
+      __syncthreads();
+      reg::fft<M, E, -1>(v, sm + l, LSP, t, twM);
+#pragma unroll
+      for (int m = 0; m < E; ++m) sm[(t + T * m) * LSP + l] = v[m];
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < 9 * M; w += blockDim.x) {
+      const int c = w / M, k = w - c * M;
+      const double2 a = sm[k * LSP + c];
+      const double2 b = cconj(sm[((M - k) & (M - 1)) * LSP + c]);
+      const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+      const double2 D = csub(a, b);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      spec[(int64_t(c) * nxy + L) * M + k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+    }
+    __syncthreads();  // sm free for the next line's prologue
+  }
+}
+
+template <int M, typename S = ZShape<M>>
+__global__ void __launch_bounds__(S::THREADS, 2048 / S::THREADS >= 4 ? 4 : 1)
+    k_zi_fast(Geo g, const double2* __restrict__ twM, const double2* __restrict__ twN,
+              const double2* __restrict__ spec, double* __restrict__ out, double scale, EpiArgs epi) {
   constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
   extern __shared__ double2 sm[];
   const int nxy = g.Nx * g.Ny;
   const int L0 = blockIdx.x * G;
   const int Gb = min(G, nxy - L0);
-  for (int w = threadIdx.x; w < 9 * Gb * M; w += blockDim.x) {
+  for (int w = threadIdx.x; w < 9 * Gb * M; w += blockDim.x) {  // all loads in flight at once
     const int c = w / (Gb * M), rem = w - c * (Gb * M);
     const int gi = rem / M, k = rem - gi * M;
-    sm[k * LSP + c * G + gi] = spec[(int64_t(c) * nxy + L0 + gi) * M + k];
+    cp_async16(sm + k * LSP + c * G + gi, spec + (int64_t(c) * nxy + L0 + gi) * M + k);
   }
+  cp_async_wait_all();
   __syncthreads();
   // Z[k] = (X[k] + X*[M-k]) + i W_N^-k (X[k] - X*[M-k]), X[M] = 0 (ZeroCompatible),
   // formed straight into the registers of the thread that transforms Z[k]
@@ -591,9 +760,58 @@ void zf_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   k_zf_fast<M, PRO, DIR><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
 }
 
+int zpipe_mode() {
+  static int v = [] {
+    const char* e = getenv("FM_ZPIPE");
+    return e ? atoi(e) : 3;
+  }();
+  return v;
+}
+
+template <int M, int PRO, bool DIR, int MINB, bool PAIRS = true>
+bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
+  constexpr size_t smem = pipe_smem<M, PRO, DIR>();
+  if constexpr (smem > 200 * 1024 || M < 16) {
+    return false;
+  } else {
+    static const int per_sm = [] {
+      allow(k_zf_pipe<M, PRO, DIR, MINB, PAIRS>, smem);
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MINB, PAIRS>, ZPipe<M>::THREADS,
+                                                    smem);
+      cudaGetLastError();
+      return b > 0 ? b : 1;
+    }();
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int nxy = g.Nx * g.Ny;
+    const int grid = std::min(nxy, std::max(sms, 1) * per_sm);
+    k_zf_pipe<M, PRO, DIR, MINB, PAIRS><<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
+    return true;
+  }
+}
+
 template <int M>
 bool zf_launch(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int* st) {
   const bool dir = pa.r != nullptr;
+  if (zpipe_mode() && (pa.kind == PRO_COPY || pa.kind == PRO_SVK)) {
+    bool ok = false;
+    if (pa.kind == PRO_COPY) ok = zpipe_go<M, PRO_COPY, false, 1>(ctx, g, pa, spec);
+    else if (zpipe_mode() == 3) ok = dir ? zpipe_go<M, PRO_SVK, true, 3>(ctx, g, pa, spec)
+                                         : zpipe_go<M, PRO_SVK, false, 3>(ctx, g, pa, spec);
+    else if (zpipe_mode() == 4) ok = dir ? zpipe_go<M, PRO_SVK, true, 4>(ctx, g, pa, spec)
+                                         : zpipe_go<M, PRO_SVK, false, 4>(ctx, g, pa, spec);
+    else if (zpipe_mode() == 5) ok = dir ? zpipe_go<M, PRO_SVK, true, 1, false>(ctx, g, pa, spec)
+                                         : zpipe_go<M, PRO_SVK, false, 1, false>(ctx, g, pa, spec);
+    else if (zpipe_mode() == 6) ok = dir ? zpipe_go<M, PRO_SVK, true, 3, false>(ctx, g, pa, spec)
+                                         : zpipe_go<M, PRO_SVK, false, 3, false>(ctx, g, pa, spec);
+    else ok = dir ? zpipe_go<M, PRO_SVK, true, 1>(ctx, g, pa, spec) : zpipe_go<M, PRO_SVK, false, 1>(ctx, g, pa, spec);
+    if (ok) {
+      *st = launched(ctx, "k_zf_pipe");
+      return true;
+    }
+  }
   if (pa.kind == PRO_COPY) zf_go<M, PRO_COPY, false>(ctx, g, pa, spec);
   else if (pa.kind == PRO_K4 && !dir) zf_go<M, PRO_K4, false>(ctx, g, pa, spec);
   else if (pa.kind == PRO_K4) zf_go<M, PRO_K4, true>(ctx, g, pa, spec);
@@ -605,15 +823,40 @@ bool zf_launch(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int*
   return true;
 }
 
-template <int M>
-bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
-               int* st) {
-  using S = ZShape<M>;
-  static bool a = (allow(k_zi_fast<M>, S::SMEM), true);
+template <int M, typename S>
+void zi_go(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi) {
+  static bool a = (allow(k_zi_fast<M, S>, S::SMEM), true);
   (void)a;
   const int nxy = g.Nx * g.Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
-  k_zi_fast<M><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+  k_zi_fast<M, S><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+}
+
+int zi_variant() {
+  static int v = [] {
+    const char* e = getenv("FM_ZI");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int M>
+using ZiShape = ZShape<M>;
+
+template <int M>
+bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
+               int* st) {
+  bool done = false;
+  if constexpr (M >= 64 && M <= 256) {
+    const int v = zi_variant();
+    done = true;
+    if (v == 1) zi_go<M, ZS<M, 8, 1>>(ctx, g, spec, out, scale, epi);
+    else if (v == 2) zi_go<M, ZS<M, 4, 1>>(ctx, g, spec, out, scale, epi);
+    else if (v == 3) zi_go<M, ZS<M, 16, 1>>(ctx, g, spec, out, scale, epi);
+    else if (v == 4 && M <= 128) zi_go<M, ZS<M, 4, 2>>(ctx, g, spec, out, scale, epi);
+    else done = false;
+  }
+  if (!done) zi_go<M, ZiShape<M>>(ctx, g, spec, out, scale, epi);
   *st = launched(ctx, "k_zi_fast");
   return true;
 }
@@ -673,16 +916,20 @@ bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double
 
 int zi_fast_blocks(const fm_ctx* ctx, const Geo& g) {
   const int nxy = g.Nx * g.Ny;
+  const int M = ctx->Nz / 2;
   int G = 0;
-  switch (ctx->Nz / 2) {
-    case 16: G = ZShape<16>::G; break;
-    case 32: G = ZShape<32>::G; break;
-    case 64: G = ZShape<64>::G; break;
-    case 128: G = ZShape<128>::G; break;
-    case 256: G = ZShape<256>::G; break;
-    case 512: G = ZShape<512>::G; break;
+  switch (M) {
+    case 16: G = ZiShape<16>::G; break;
+    case 32: G = ZiShape<32>::G; break;
+    case 64: G = ZiShape<64>::G; break;
+    case 128: G = ZiShape<128>::G; break;
+    case 256: G = ZiShape<256>::G; break;
+    case 512: G = ZiShape<512>::G; break;
     default: return 0;
   }
+  const int v = (M >= 64 && M <= 256) ? zi_variant() : 0;
+  if (v >= 1 && v <= 3) G = 1;
+  if (v == 4 && M <= 128) G = 2;
   return (nxy + G - 1) / G;
 }
 

@@ -236,7 +236,29 @@ def simple_shear_program(gamma: float, increments: int, tdim: int) -> np.ndarray
     return out
 
 
+def _host_lib():
+    import ctypes
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfftmech_host.so")
+    if not os.path.exists(path):
+        return None
+    try:
+        lib = ctypes.CDLL(path)
+    except OSError:
+        return None
+    lib.fmh_uniform_field.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p]
+    lib.fmh_uniform_field.restype = None
+    return lib
+
+
 def uniform_field(points, ncomp: int, seed: int) -> np.ndarray:
-    """Config 4: ncomp slabs i.i.d. U(-1,1) = 2u-1, slab by slab in node order."""
+    """Config 4: ncomp slabs i.i.d. U(-1,1) = 2u-1, slab by slab in node order.
+    Large fields use the host library's std::mt19937_64 (same stream)."""
     n = int(np.prod(points))
+    if ncomp * n >= (1 << 20):
+        lib = _host_lib()
+        if lib is not None:
+            out = np.empty(ncomp * n)
+            lib.fmh_uniform_field(seed, ncomp * n, out.ctypes.data)
+            return out
     return 2.0 * MT19937_64(seed).uniform(ncomp * n) - 1.0

@@ -26,16 +26,17 @@ if len(sys.argv) > 2:  # child: one variant
         model.apply(dF, out)
     ctx.sync()
     dt = (time.perf_counter() - t) / reps
-    np.save(f"/tmp/xvar_{sys.argv[2]}.npy", out.download())
+    np.save(f"/tmp/xvar_{sys.argv[2].replace('=', '_')}.npy", out.download())
     print(f"variant {sys.argv[2]} N={N} matvec {dt*1e3:.3f} ms")
 else:
     N = sys.argv[1] if len(sys.argv) > 1 else "256"
     import numpy as np
     vs = os.environ.get("VARIANTS", "5 6 7").split()
-    for v in vs:
-        env = dict(os.environ, FM_XPASS=v)
+    for v in vs:  # "6" -> FM_XPASS=6; "FM_ZPIPE=0" -> that variable
+        k, val = v.split("=") if "=" in v else ("FM_XPASS", v)
+        env = dict(os.environ, **{k: val})
         subprocess.run([sys.executable, __file__, N, v], env=env, check=True)
-    ref = np.load(f"/tmp/xvar_{vs[0]}.npy")
+    ref = np.load(f"/tmp/xvar_{vs[0].replace('=', '_')}.npy")
     for v in vs[1:]:
-        o = np.load(f"/tmp/xvar_{v}.npy")
+        o = np.load(f"/tmp/xvar_{v.replace('=', '_')}.npy")
         print(v, "max rel diff vs", vs[0], float(np.abs(o - ref).max() / np.abs(ref).max()))

@@ -157,3 +157,38 @@ def test_shape_mismatch_is_invalid():
         with pytest.raises(abi.FmError) as e:
             ctx.projection(bad, a)
         assert e.value.status == 1
+
+
+@pytest.mark.parametrize("N", [256, 512])
+def test_config4_properties_full_size(N):
+    """BASELINE.json config 4 at full size: seed 4 + N,
+    nine i.i.d. U(-1,1) slabs.  The oracle does not fit at these sizes, so the
+    check is by size-independent properties, all evaluated on the device:
+    G(G(x)) = G(x), zero mean, self-adjointness <x, G y> = <G x, y>."""
+    pts = (N, N, N)
+    with abi.Context(pts, 3) as ctx:
+        x = ctx.field(9, M.uniform_field(pts, 9, seed=4 + N))
+        y = ctx.field(9, M.uniform_field(pts, 9, seed=5 + N))
+        Gx = ctx.projection(x)
+        GGx = ctx.projection(Gx)
+        ngx = ctx.norm(Gx)
+        ctx.axpy(-1.0, Gx, GGx)
+        assert ctx.norm(GGx) < 1e-10 * ngx
+        assert np.all(np.abs(ctx.mean(Gx)) < 1e-12)
+        Gy = ctx.projection(y, out=GGx)
+        lhs, rhs = ctx.dot(x, Gy), ctx.dot(Gx, y)
+        assert abs(lhs - rhs) <= 1e-10 * abs(rhs)
+
+
+def test_config4_oracle_equality_128():
+    """Config 4 at N = 128 (largest size the oracle runs in seconds):
+    bitwise-close equality of G(x) against the CPU oracle."""
+    N = 128
+    pts = (N, N, N)
+    x = M.uniform_field(pts, 9, seed=4 + N)
+    from oracle import oracle as O
+    ref, st, _ = O.apply_projection(pts, 3, x)
+    assert st == 0
+    with abi.Context(pts, 3) as ctx:
+        got = ctx.projection(ctx.field(9, x)).download()
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
