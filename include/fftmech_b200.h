@@ -153,6 +153,18 @@ int fm_simo_evaluate(fm_ctx* ctx, const fm_field* F, const fm_field* F_old,
                      const fm_field* hardening, fm_field* P, fm_field* K, fm_field* be_trial,
                      fm_field* epsp_trial);
 
+/* ---- output measures -----------------------------------
+ * equivalent_stress, material.cpp:14-31, of
+ *   FM_EQ_TENSOR    : T = P itself (F unused, may be NULL);
+ *   FM_EQ_PK2       : S = F^-1 P   HyperelasticModel::equivalent_stress_field,
+ *                     hyperelastic.cpp:89-92 (FM_E_SINGULAR at the first node
+ *                     with |det F| < 1e-30, tensor_ops.cpp:257-266);
+ *   FM_EQ_KIRCHHOFF : tau = P F^T  SimoPlasticityModel::equivalent_stress_field,
+ *                     simo.cpp:225-228.
+ * out: 1-component field. */
+enum { FM_EQ_TENSOR = 0, FM_EQ_PK2 = 1, FM_EQ_KIRCHHOFF = 2 };
+int fm_equivalent_stress(fm_ctx* ctx, const fm_field* F, const fm_field* P, int kind, fm_field* out);
+
 /* ---- BLAS-1 / reductions (fields.cpp:14-67, tensor_ops.cpp:276-294) ------
  * Deterministic: fixed-order block partials then a fixed-order final sum. */
 int fm_dot(fm_ctx* ctx, const fm_field* a, const fm_field* b, double* out);

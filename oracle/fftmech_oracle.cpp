@@ -866,6 +866,77 @@ int or_simo_evaluate(int64_t n, const double* F, const double* Fold, const doubl
                        bad, bad_value);
 }
 
+// equivalent_stress (material.cpp:14-31) of P, of inv2(F).P (hyperelastic.cpp:
+// 89-92; inv2 = Tensor2::inverse with the kSingularDetTol check, tensor_ops.cpp:
+// 257-266, tensor2.hpp:63-113) or of P.F^T (simo.cpp:225-228; dot22 sums the
+// inner index in order, tensor_ops.cpp:138-153).  kind 0 / 1 / 2.
+int or_equivalent_stress(int64_t n, int tdim, int kind, const double* F, const double* P, double* out,
+                         int64_t* bad) {
+  const int d = tdim;
+  for (int64_t q = 0; q < n; ++q) {
+    double p[9], f[9], t[9];
+    for (int c = 0; c < d * d; ++c) p[c] = P[c * n + q];
+    if (kind == 0) {
+      for (int c = 0; c < d * d; ++c) t[c] = p[c];
+    } else {
+      for (int c = 0; c < d * d; ++c) f[c] = F[c * n + q];
+      if (kind == 1) {
+        double det, inv[9];
+        if (d == 2) {
+          det = f[0] * f[3] - f[1] * f[2];
+        } else {
+          det = f[0] * (f[4] * f[8] - f[5] * f[7]) - f[1] * (f[3] * f[8] - f[5] * f[6]) +
+                f[2] * (f[3] * f[7] - f[4] * f[6]);
+        }
+        if (std::fabs(det) < 1e-30) {
+          if (bad) *bad = q;
+          return E_SINGULAR;
+        }
+        if (d == 2) {
+          inv[0] = f[3] / det;
+          inv[1] = -f[1] / det;
+          inv[2] = -f[2] / det;
+          inv[3] = f[0] / det;
+        } else {
+          inv[0] = (f[4] * f[8] - f[5] * f[7]) / det;
+          inv[1] = (f[2] * f[7] - f[1] * f[8]) / det;
+          inv[2] = (f[1] * f[5] - f[2] * f[4]) / det;
+          inv[3] = (f[5] * f[6] - f[3] * f[8]) / det;
+          inv[4] = (f[0] * f[8] - f[2] * f[6]) / det;
+          inv[5] = (f[2] * f[3] - f[0] * f[5]) / det;
+          inv[6] = (f[3] * f[7] - f[4] * f[6]) / det;
+          inv[7] = (f[1] * f[6] - f[0] * f[7]) / det;
+          inv[8] = (f[0] * f[4] - f[1] * f[3]) / det;
+        }
+        for (int i = 0; i < d; ++i)
+          for (int k = 0; k < d; ++k) {
+            double s = 0.0;
+            for (int j = 0; j < d; ++j) s += inv[i * d + j] * p[j * d + k];
+            t[i * d + k] = s;
+          }
+      } else {
+        for (int i = 0; i < d; ++i)
+          for (int k = 0; k < d; ++k) {
+            double s = 0.0;
+            for (int j = 0; j < d; ++j) s += p[i * d + j] * f[k * d + j];
+            t[i * d + k] = s;
+          }
+      }
+    }
+    double tr = 0.0;
+    for (int i = 0; i < d; ++i) tr += t[i * d + i];
+    tr /= double(d);
+    double s = 0.0;
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) {
+        const double dv = t[i * d + j] - (i == j ? tr : 0.0);
+        s += dv * dv;
+      }
+    out[q] = std::sqrt(1.5 * s);
+  }
+  return OK;
+}
+
 int or_sym_eig3(const double* A, double* lam, double* V) {
   sym_eig3(A, lam, V);
   return OK;

@@ -54,6 +54,8 @@ def lib():
         L.or_fft.argtypes = [C.c_int, _ip, C.c_int, C.c_int, _dp]
         L.or_hyper_evaluate.argtypes = [C.c_int64, C.c_int, _dp, _dp, _dp, _dp, C.c_void_p,
                                         C.POINTER(C.c_int64)]
+        L.or_equivalent_stress.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_void_p, _dp, _dp,
+                                           C.POINTER(C.c_int64)]
         L.or_simo_evaluate.argtypes = [C.c_int64] + [_dp] * 8 + [_dp, C.c_void_p, _dp, _dp,
                                                                   C.POINTER(C.c_int64),
                                                                   C.POINTER(C.c_double)]
@@ -125,6 +127,17 @@ def hyper_evaluate(F, lam, mu, tdim=3, want_K=True):
                                  np.ascontiguousarray(mu, dtype=np.float64), P,
                                  K.ctypes.data if K is not None else None, C.byref(bad))
     return P, K, st, bad.value
+
+
+def equivalent_stress(F, P, n, tdim=3, kind=0):
+    """kind 0: of P; 1: of F^-1 P (hyperelastic); 2: of P F^T (Simo).
+    Returns (eq, status, bad_node)."""
+    out = np.empty(n)
+    bad = C.c_int64(-1)
+    Fp = np.ascontiguousarray(F, dtype=np.float64).reshape(-1) if F is not None else None
+    st = lib().or_equivalent_stress(n, tdim, kind, Fp.ctypes.data if Fp is not None else None,
+                                    np.ascontiguousarray(P, dtype=np.float64).reshape(-1), out, C.byref(bad))
+    return out, st, bad.value
 
 
 def simo_evaluate(F, Fold, be, epsp, lam, mu, ty0, hard, want_K=True):

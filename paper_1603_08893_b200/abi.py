@@ -90,6 +90,7 @@ _SIGS = {
     "fm_projected_tangent_apply": (C.c_int, [_P, _P, _P, _P]),
     "fm_hyper_evaluate": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "fm_simo_evaluate": (C.c_int, [_P] + [_P] * 12),
+    "fm_equivalent_stress": (C.c_int, [_P, _P, _P, C.c_int, _P]),
     "fm_dot": (C.c_int, [_P, _P, _P, C.POINTER(C.c_double)]),
     "fm_norm": (C.c_int, [_P, _P, C.POINTER(C.c_double)]),
     "fm_mean": (C.c_int, [_P, _P, _dp]),
@@ -296,6 +297,15 @@ class Context:
         rel = C.c_double()
         self.check(lib().fm_cg_solve(self.h, K.h, rhs.h, eta_cg, max_cg, x.h, C.byref(it), C.byref(rel)))
         return x, it.value, rel.value
+
+    EQ_TENSOR, EQ_PK2, EQ_KIRCHHOFF = 0, 1, 2
+
+    def equivalent_stress(self, F, P, kind, out=None):
+        """von Mises equivalent (material.cpp:14-31) of P (EQ_TENSOR),
+        F^-1 P (EQ_PK2, hyperelastic) or P F^T (EQ_KIRCHHOFF, Simo)."""
+        out = out or self.field(1)
+        self.check(lib().fm_equivalent_stress(self.h, F.h if F is not None else None, P.h, kind, out.h))
+        return out
 
     def hyper_evaluate(self, F, lam, mu, want_K=True):
         P = self.field()

@@ -398,6 +398,14 @@ int fm_simo_evaluate(fm_ctx* ctx, const fm_field* F, const fm_field* F_old,
   return check_bad(ctx);
 }
 
+int fm_equivalent_stress(fm_ctx* ctx, const fm_field* F, const fm_field* P, int kind, fm_field* out) {
+  if (!ctx || !P || !out || P->ncomp != ctx->ncomp || out->ncomp != 1 ||
+      (kind != FM_EQ_TENSOR && (!F || F->ncomp != ctx->ncomp)) || kind < FM_EQ_TENSOR || kind > FM_EQ_KIRCHHOFF)
+    return set_error(ctx, FM_E_INVALID, "equivalent_stress: field size mismatch");
+  if (int st = eq_stress_async(ctx, kind, F ? F->d : nullptr, P->d, out->d)) return st;
+  return check_bad(ctx);
+}
+
 // ------------------------------------------------------------------- BLAS
 static bool same(const fm_field* a, const fm_field* b) { return a && b && a->ncomp == b->ncomp && a->n == b->n; }
 

@@ -369,6 +369,86 @@ __global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restric
   }
 }
 
+// ---------------------------------------------------------- output measures
+// von Mises equivalent of a tensor field, equivalent_stress (material.cpp:
+// 14-31): sqrt(3/2 dev(T):dev(T)), dev taken with tr(T)/tdim.  T is
+//   FM_EQ_TENSOR    : the field itself;
+//   FM_EQ_PK2       : S = F^-1 P (HyperelasticModel, hyperelastic.cpp:89-92;
+//                     inv2 throws SingularTensor if |det F| < 1e-30,
+//                     tensor_ops.cpp:257-266);
+//   FM_EQ_KIRCHHOFF : tau = P F^T (SimoPlasticityModel, simo.cpp:225-228).
+// Products accumulate over the inner index in order (dot22, tensor_ops.cpp:
+// 138-153).  Reads 72 or 144 B and writes 8 B per voxel: one HBM sweep.
+template <int TD, int KIND>
+__global__ void __launch_bounds__(256) k_eq_stress(int64_t n, const double* __restrict__ F,
+                                                   const double* __restrict__ P, double* __restrict__ out,
+                                                   unsigned long long* bad, int64_t noff) {
+  constexpr int NC = TD * TD;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    double p[NC], t[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) p[c] = __ldg(P + c * n + q);
+    if constexpr (KIND == FM_EQ_TENSOR) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) t[c] = p[c];
+    } else {
+      double f[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) f[c] = __ldg(F + c * n + q);
+      if constexpr (KIND == FM_EQ_PK2) {
+        const double d = det_t<TD>(f);
+        if (fabs(d) < 1e-30) {  // detail::kSingularDetTol
+          report_bad(bad, nullptr, noff + q, FM_E_SINGULAR, 0.0);
+          out[q] = 0.0;
+          continue;
+        }
+        double fi[NC];
+        if constexpr (TD == 2) {
+          fi[0] = f[3] / d;
+          fi[1] = -f[1] / d;
+          fi[2] = -f[2] / d;
+          fi[3] = f[0] / d;
+        } else {
+          inv3(f, fi);
+        }
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+#pragma unroll
+          for (int k = 0; k < TD; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < TD; ++j) s += fi[i * TD + j] * p[j * TD + k];
+            t[i * TD + k] = s;
+          }
+      } else {  // tau = P F^T
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+#pragma unroll
+          for (int k = 0; k < TD; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < TD; ++j) s += p[i * TD + j] * f[k * TD + j];
+            t[i * TD + k] = s;
+          }
+      }
+    }
+    double tr = 0.0;
+#pragma unroll
+    for (int i = 0; i < TD; ++i) tr += t[i * TD + i];
+    tr /= double(TD);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        const double dv = t[i * TD + j] - (i == j ? tr : 0.0);
+        s += dv * dv;
+      }
+    out[q] = sqrt(1.5 * s);
+  }
+}
+
 // -------------------------------------------------------------------- host
 int reset_bad(fm_ctx* ctx) {
   FM_CUDA(ctx, cudaMemsetAsync(ctx->d_bad, 0xFF, sizeof(unsigned long long), ctx->stream));
@@ -407,6 +487,26 @@ int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const doub
     k_hyper<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
   else
     k_hyper<2><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
+template <int TD>
+static void eq_launch(fm_ctx* ctx, int kind, const double* F, const double* P, double* out, int blocks) {
+  if (kind == FM_EQ_TENSOR)
+    k_eq_stress<TD, FM_EQ_TENSOR><<<blocks, 256, 0, ctx->stream>>>(ctx->n, F, P, out, ctx->d_bad, ctx->node_offset);
+  else if (kind == FM_EQ_PK2)
+    k_eq_stress<TD, FM_EQ_PK2><<<blocks, 256, 0, ctx->stream>>>(ctx->n, F, P, out, ctx->d_bad, ctx->node_offset);
+  else
+    k_eq_stress<TD, FM_EQ_KIRCHHOFF><<<blocks, 256, 0, ctx->stream>>>(ctx->n, F, P, out, ctx->d_bad,
+                                                                      ctx->node_offset);
+}
+
+int eq_stress_async(fm_ctx* ctx, int kind, const double* F, const double* P, double* out) {
+  if (int st = reset_bad(ctx)) return st;
+  const int blocks = grid_for(ctx->n, 256);
+  if (ctx->tdim == 3) eq_launch<3>(ctx, kind, F, P, out, blocks);
+  else eq_launch<2>(ctx, kind, F, P, out, blocks);
   FM_LAUNCHED(ctx);
   return FM_OK;
 }

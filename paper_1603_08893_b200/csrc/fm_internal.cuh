@@ -191,6 +191,7 @@ int cg_pap_finalize_async(fm_ctx* ctx, int n_partials);
 // constitutive.cu -----------------------------------------------------------
 int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const double* mu, double* P,
                      double* K);
+int eq_stress_async(fm_ctx* ctx, int kind, const double* F, const double* P, double* out);
 int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const double* be_c,
                     const double* epsp_c, const double* lam, const double* mu,
                     const double* ty0, const double* hard, double* P, double* K, double* be_t,

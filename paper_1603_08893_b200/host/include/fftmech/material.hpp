@@ -53,4 +53,9 @@ class MaterialModel {
 
 ScalarField equivalent_stress(const Tensor2Field& T);
 
+// sqrt(2/3 dev(ln U):dev(ln U)) of the macroscopic stretch, U^2 = Fbar^T Fbar
+// (material.cpp:33-49; 2x2 inputs embedded as plane strain).  The eps_bar
+// column of report.csv.
+double macroscopic_equivalent_strain(const Tensor2& fbar);
+
 }  // namespace fftmech

@@ -1,6 +1,8 @@
 // Drop-in constitutive models backed by the sm_100a kernels (reference:
 // hyperelastic.cpp:10-92, simo.cpp:26-228, material.cpp:11-31).
+#include <algorithm>
 #include <cmath>
+#include <memory>
 #include <stdexcept>
 
 #include "device.hpp"
@@ -12,21 +14,69 @@ namespace fftmech {
 
 HistoryState::HistoryState(const GridShape& shape, int tdim) : be(identity2(shape, tdim)), eps_p(shape, 0.0) {}
 
-ScalarField equivalent_stress(const Tensor2Field& T) {
-  const int d = T.tdim();
-  ScalarField out(T.shape());
-  for (std::size_t q = 0; q < T.nodes(); ++q) {
-    const Tensor2 t = T.tensor(q);
-    const double m = t.trace() / d;
-    double s = 0.0;
-    for (int i = 0; i < d; ++i)
-      for (int j = 0; j < d; ++j) {
-        const double dev = t(i, j) - (i == j ? m : 0.0);
-        s += dev * dev;
-      }
-    out[q] = std::sqrt(1.5 * s);
+namespace {
+// Output measures on the device (fm_equivalent_stress): compat-mode upload of
+// the host fields, one kernel sweep, download of the scalar field.
+ScalarField device_equivalent_stress(const Tensor2Field* F, const Tensor2Field& P, int kind, const char* where) {
+  const int d = P.tdim();
+  auto dev = detail::device_for(P.shape(), d, 0);
+  detail::DevField p(dev, d * d), out(dev, 1);
+  p.upload(P.data());
+  std::unique_ptr<detail::DevField> f;
+  if (F) {
+    if (F->nodes() != P.nodes() || F->tdim() != d) throw std::invalid_argument(std::string(where) + ": size mismatch");
+    f = std::make_unique<detail::DevField>(dev, d * d);
+    f->upload(F->data());
   }
-  return out;
+  detail::check(dev->h, fm_equivalent_stress(dev->h, f ? f->get() : nullptr, p.get(), kind, out.get()), where);
+  ScalarField eq(P.shape());
+  out.download(eq.data());
+  return eq;
+}
+}  // namespace
+
+ScalarField equivalent_stress(const Tensor2Field& T) {
+  return device_equivalent_stress(nullptr, T, FM_EQ_TENSOR, "equivalent_stress");
+}
+
+double macroscopic_equivalent_strain(const Tensor2& fbar) {
+  double f[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int i = 0; i < fbar.dim; ++i)
+    for (int j = 0; j < fbar.dim; ++j) f[i][j] = fbar(i, j);
+  double c[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) c[i][j] = f[0][i] * f[0][j] + f[1][i] * f[1][j] + f[2][i] * f[2][j];
+  // cyclic Jacobi on the symmetric 3x3 (eigenvalues only)
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    const double off = c[0][1] * c[0][1] + c[0][2] * c[0][2] + c[1][2] * c[1][2];
+    const double dg = c[0][0] * c[0][0] + c[1][1] * c[1][1] + c[2][2] * c[2][2];
+    if (off == 0.0 || off < 1e-36 * dg) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (c[p][q] == 0.0) continue;
+        const double th = (c[q][q] - c[p][p]) / (2.0 * c[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < 3; ++k) {
+          const double a = c[k][p], b = c[k][q];
+          c[k][p] = cs * a - sn * b;
+          c[k][q] = sn * a + cs * b;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double a = c[p][k], b = c[q][k];
+          c[p][k] = cs * a - sn * b;
+          c[q][k] = sn * a + cs * b;
+        }
+      }
+  }
+  double lam[3] = {c[0][0], c[1][1], c[2][2]};
+  std::sort(lam, lam + 3);
+  double le[3];
+  for (int i = 0; i < 3; ++i) le[i] = 0.5 * std::log(lam[i]);
+  const double tr = (le[0] + le[1] + le[2]) / 3.0;
+  double s = 0.0;
+  for (int i = 0; i < 3; ++i) s += (le[i] - tr) * (le[i] - tr);
+  return std::sqrt(2.0 / 3.0 * s);
 }
 
 // ------------------------------------------------------------ hyperelastic
@@ -96,7 +146,7 @@ void HyperelasticModel::evaluate(const Tensor2Field& F, Tensor2Field& P, Tensor4
 }
 
 ScalarField HyperelasticModel::equivalent_stress_field(const Tensor2Field& F, const Tensor2Field& P) const {
-  return equivalent_stress(dot22(inv2(F), P));  // dev S, S = F^-1 P
+  return device_equivalent_stress(&F, P, FM_EQ_PK2, "equivalent_stress_field");  // S = F^-1 P
 }
 
 // -------------------------------------------------------------------- Simo
@@ -217,7 +267,7 @@ const HistoryState& SimoPlasticityModel::trial() const {
 const Tensor2Field& SimoPlasticityModel::reference_deformation() const { return f_old_; }
 
 ScalarField SimoPlasticityModel::equivalent_stress_field(const Tensor2Field& F, const Tensor2Field& P) const {
-  return equivalent_stress(dot22(P, trans2(F)));  // tau = P F^T
+  return device_equivalent_stress(&F, P, FM_EQ_KIRCHHOFF, "equivalent_stress_field");  // tau = P F^T
 }
 
 }  // namespace fftmech

@@ -8,6 +8,10 @@
 // every CHECK held.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <filesystem>
+#include <fstream>
+#include <sstream>
 #include <functional>
 #include <random>
 #include <string>
@@ -17,6 +21,7 @@
 #include "fftmech/microstructure.hpp"
 #include "fftmech/projection.hpp"
 #include "fftmech/simo.hpp"
+#include "fftmech/snapshot.hpp"
 #include "fftmech/solver.hpp"
 #include "fftmech/tensor_ops.hpp"
 
@@ -96,7 +101,120 @@ class HostSvk final : public MaterialModel {
   ElasticParams p_;
 };
 
-int main() {
+static std::string slurp(const std::filesystem::path& p) {
+  std::ifstream in(p, std::ios::binary);
+  std::ostringstream ss;
+  ss << in.rdbuf();
+  return ss.str();
+}
+
+static std::vector<std::vector<std::string>> csv_rows(const std::filesystem::path& p) {
+  std::vector<std::vector<std::string>> rows;
+  std::istringstream in(slurp(p));
+  std::string line;
+  while (std::getline(in, line)) {
+    std::vector<std::string> cells;
+    std::istringstream ls(line);
+    std::string c;
+    while (std::getline(ls, c, ',')) cells.push_back(c);
+    rows.push_back(cells);
+  }
+  return rows;
+}
+
+// One reference run (execute_run's loop, run_config.cpp:497-524) written
+// through SnapshotSink, then compared with the reference's own record
+// directory: meta_<k>.json and VTK byte-for-byte, report.csv on every column
+// but wall_ms (newton/cg exact, residual to 1e-6 relative -- the CG vectors'
+// round-off -- and eps_bar to 1e-14).
+static void check_run_against_record(const std::filesystem::path& golden, const std::string& rec,
+                                     const GridShape& s, const std::vector<double>& fractions,
+                                     const std::vector<ElasticParams>& phases, double gamma, int increments,
+                                     OutputOptions opts) {
+  namespace fs = std::filesystem;
+  const fs::path out = fs::temp_directory_path() / ("fftmech_b200_" + rec);
+  fs::remove_all(out);
+  opts.directory = out;
+  const PhaseGrid pg = make_laminate(s, fractions);
+  std::vector<ElasticParams> used(phases.begin(), phases.begin() + pg.phase_count);
+  const MaterialFields mf = bind_parameters(pg, used);
+  HyperelasticModel model(s, s.dim, mf.lambda, mf.mu);
+  const ProjectionOperator G = build_projection(s, s.dim);
+  Tensor2Field F = identity2(s, s.dim);
+  LoadProgram program;
+  for (int t = 1; t <= increments; ++t) {
+    Tensor2 f = Tensor2::identity(s.dim);
+    f(0, 1) = gamma * static_cast<double>(t) / increments;
+    program.push_back({f, std::to_string(t)});
+  }
+  SnapshotSink sink(opts);
+  run_program(F, model, G, program, SolverParams{}, sink);
+  sink.finish();
+  const fs::path ref = golden / rec;
+  for (const auto& e : fs::directory_iterator(ref)) {
+    const std::string name = e.path().filename().string();
+    if (name == "report.csv") continue;
+    const bool same = slurp(out / name) == slurp(e.path());
+    if (!same) std::printf("    %s/%s differs from the reference record\n", rec.c_str(), name.c_str());
+    CHECK(same);
+  }
+  const auto got = csv_rows(out / "report.csv"), want = csv_rows(ref / "report.csv");
+  CHECK(got.size() == want.size());
+  for (size_t r = 0; r < std::min(got.size(), want.size()); ++r) {
+    CHECK(got[r].size() == 6 && want[r].size() == 6);
+    if (got[r].size() != 6 || want[r].size() != 6) continue;
+    if (r == 0) {
+      for (int c = 0; c < 6; ++c) CHECK(got[r][c] == want[r][c]);
+      continue;
+    }
+    CHECK(got[r][0] == want[r][0] && got[r][1] == want[r][1] && got[r][2] == want[r][2]);
+    const double rg = std::stod(got[r][3]), rw = std::stod(want[r][3]);
+    CHECK(std::abs(rg - rw) <= 1e-6 * std::abs(rw));
+    const double eg = std::stod(got[r][5]), ew = std::stod(want[r][5]);
+    CHECK(std::abs(eg - ew) <= 1e-14 * std::abs(ew));
+  }
+  CHECK(list_snapshots(out).size() == size_t((increments) / opts.stride));
+}
+
+static void snapshot_round_trip(const std::filesystem::path& golden) {
+      namespace fs = std::filesystem;
+      const fs::path dir = fs::temp_directory_path() / "fftmech_b200_unit_snapshot_out";
+      fs::remove_all(dir);
+      Snapshot snap;
+      snap.increment = 7;
+      snap.label = "7";
+      snap.grid = grid_2d(3, 2);
+      snap.tensor_dim = 2;
+      snap.fbar = Tensor2::identity(2);
+      snap.fbar(0, 1) = 0.25;
+      SnapshotFieldData f;
+      f.components = 4;
+      for (int c = 0; c < 4; ++c)
+        for (int k = 0; k < 6; ++k) f.values.push_back(0.1 * c + 1e-13 * k + (c == 0 || c == 3));
+      snap.fields["F"] = f;
+      SnapshotFieldData eq;
+      eq.components = 1;
+      for (int k = 0; k < 6; ++k) eq.values.push_back(std::sqrt(2.0) * k);
+      snap.fields["eq"] = eq;
+      write_snapshot(dir, snap);
+      const Snapshot back = read_snapshot(dir, 7);
+      CHECK(back.label == "7" && back.tensor_dim == 2 && back.grid.points[0] == 3 && back.fbar(0, 1) == 0.25);
+      CHECK(back.fields.count("F") == 1 && back.fields.at("F").values == f.values);
+      CHECK(back.fields.at("eq").values == eq.values);
+      CHECK(list_snapshots(dir) == std::vector<int>{7});
+      CHECK(slurp(dir / "meta_7.json") == slurp(golden / "unit_snapshot_out" / "meta_7.json"));
+      const Tensor2Field T = snapshot_to_field(back, "F");
+      CHECK(T.at(5, 1, 1) == f.values[3 * 6 + 5]);
+    }
+
+int main(int argc, char** argv) {
+  const char* golden_env = std::getenv("FFTMECH_GOLDEN_RECORDS");
+  const std::filesystem::path golden = argc > 1 ? argv[1] : (golden_env ? golden_env : "");
+  if (argc > 2 && std::string(argv[2]) == "--no-device") {  // host-only cases (CPU test suite)
+    run("output: snapshot round trip, bit-exact (test_config_io.cpp:135-164)", [&] { snapshot_round_trip(golden); });
+    std::printf("%d checks, %d failed\n", g_checks, g_fail);
+    return g_fail == 0 ? 0 : 1;
+  }
   run("projection: constant fields project to zero", [] {
     const GridShape s = grid_3d(5, 5, 5);
     const ProjectionOperator G = build_projection(s, 3);
@@ -442,6 +560,47 @@ int main() {
     }
     CHECK(ok);
   });
+
+  if (!golden.empty()) {
+    run("output: homogeneous 4x4 run == proj/unit_run_out (meta, report)", [&] {
+      check_run_against_record(golden, "unit_run_out", grid_2d(4, 4), {1.0}, {{1.0, 0.3}}, 0.2, 2, OutputOptions{});
+    });
+    run("output: 3x3 run with VTK == proj/unit_vtk_out (meta, VTK bytes, report)", [&] {
+      OutputOptions o;
+      o.vtk = true;
+      check_run_against_record(golden, "unit_vtk_out", grid_2d(3, 3), {1.0}, {{1.0, 0.3}}, 0.05, 1, o);
+    });
+    run("output: laminate run == proj/unit_det_out1 (meta, report)", [&] {
+      OutputOptions o;
+      o.fields = {"F", "P", "eq"};
+      check_run_against_record(golden, "unit_det_out1", grid_2d(5, 4), {0.4, 0.6}, {{1.0, 0.3}, {5.0, 0.25}}, 0.15,
+                               3, o);
+    });
+    run("output: snapshot round trip, bit-exact (test_config_io.cpp:135-164)", [&] { snapshot_round_trip(golden); });
+    run("output: equivalent stress on the device == host restatement", [] {
+      const GridShape s = grid_3d(4, 3, 5);
+      std::mt19937 rng(3);
+      Tensor2Field F = random_field(s, 3, rng, 0.2);
+      F.add_uniform(Tensor2::identity(3));
+      const Tensor2Field P = random_field(s, 3, rng);
+      const ScalarField eq = HyperelasticModel(s, 3, ElasticParams{}).equivalent_stress_field(F, P);
+      const ScalarField eqs = equivalent_stress(dot22(P, trans2(F)));
+      const ScalarField tau = SimoPlasticityModel(s, PlasticParams{}).equivalent_stress_field(F, P);
+      double worst = 0.0;
+      for (std::size_t q = 0; q < s.node_count(); ++q) {
+        const Tensor2 S = dot(F.tensor(q).inverse(), P.tensor(q));
+        const double m = S.trace() / 3.0;
+        double ss = 0.0;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) ss += (S(i, j) - (i == j ? m : 0.0)) * (S(i, j) - (i == j ? m : 0.0));
+        worst = std::max(worst, std::abs(eq[q] - std::sqrt(1.5 * ss)) / std::max(1.0, eq[q]));
+        worst = std::max(worst, std::abs(eqs[q] - tau[q]) / std::max(1.0, tau[q]));
+      }
+      CHECK(worst < 1e-13);
+    });
+  } else {
+    std::printf("[SKIP] output records (pass the golden record directory as argv[1])\n");
+  }
 
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;

@@ -110,3 +110,35 @@ def test_simo_inverted_node():
             ctx.simo_evaluate(ctx.field(9, F), ctx.field(9, I), I, np.zeros(n), np.full(n, e.lame_lambda),
                               np.full(n, e.lame_mu), np.full(n, 0.01), np.full(n, 0.05))
     assert err.value.status == 4 and err.value.info["node"] == 9
+
+
+@pytest.mark.parametrize("tdim,kind", [(3, 0), (3, 1), (3, 2), (2, 0), (2, 1), (2, 2)])
+def test_equivalent_stress_matches_oracle(tdim, kind, oracle):
+    """fm_equivalent_stress against the restated
+    equivalent_stress / inv2 / dot22 (material.cpp:14-31)."""
+    pts = (6, 5, 7) if tdim == 3 else (9, 8)
+    n = int(np.prod(pts))
+    rng = np.random.default_rng(11 + kind)
+    F = rng.uniform(-0.2, 0.2, tdim * tdim * n)
+    for i in range(tdim):
+        F[(i * tdim + i) * n:(i * tdim + i + 1) * n] += 1.0
+    P = rng.uniform(-1, 1, tdim * tdim * n)
+    ref, st, _ = oracle.equivalent_stress(F, P, n, tdim, kind)
+    assert st == 0
+    with abi.Context(pts, tdim) as ctx:
+        got = ctx.equivalent_stress(ctx.field(tdim * tdim, F), ctx.field(tdim * tdim, P), kind).download()
+    assert np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref))) < 1e-14
+
+
+def test_equivalent_stress_singular_reports_first_node():
+    pts = (4, 4, 4)
+    n = 64
+    F = abi.identity_field(pts, 3)
+    for node in (37, 9):
+        for c in range(9):
+            F[c * n + node] = 0.0  # det F = 0 -> SingularTensor(first node)
+    P = np.ones(9 * n)
+    with abi.Context(pts, 3) as ctx:
+        with pytest.raises(abi.FmError) as e:
+            ctx.equivalent_stress(ctx.field(9, F), ctx.field(9, P), abi.Context.EQ_PK2)
+    assert e.value.status == 6 and e.value.info["node"] == 9

@@ -7,6 +7,7 @@ import pytest
 
 LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1603_08893_b200", "lib")
 BIN = os.path.join(LIB, "test_host_api")
+RECORDS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_records")
 
 
 def test_host_library_links_the_cuda_library():
@@ -24,7 +25,7 @@ def test_host_library_links_the_cuda_library():
 
 @pytest.mark.gpu
 def test_reference_style_cpp_client_passes_on_gpu():
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([BIN, RECORDS], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "[FAIL]" not in r.stdout
@@ -40,3 +41,11 @@ def test_native_config4_stream_matches_mt19937_64():
     b = 2.0 * M.MT19937_64(4 + 64).uniform(9 * 64 ** 3) - 1.0
     assert M._host_lib() is not None
     assert np.array_equal(a, b)
+
+
+def test_snapshot_writer_matches_reference_record_on_host():
+    """write_snapshot/read_snapshot round trip (test_config_io.cpp:135-164);
+    the emitted meta_7.json is byte-identical to proj/unit_snapshot_out's."""
+    r = subprocess.run([BIN, RECORDS, "--no-device"], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
