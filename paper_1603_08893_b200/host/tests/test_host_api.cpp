@@ -20,6 +20,7 @@
 #include "fftmech/hyperelastic.hpp"
 #include "fftmech/microstructure.hpp"
 #include "fftmech/projection.hpp"
+#include "fftmech/run_config.hpp"
 #include "fftmech/simo.hpp"
 #include "fftmech/snapshot.hpp"
 #include "fftmech/solver.hpp"
@@ -176,6 +177,107 @@ static void check_run_against_record(const std::filesystem::path& golden, const 
   CHECK(list_snapshots(out).size() == size_t((increments) / opts.stride));
 }
 
+// parse_config behaviour (proj/tests/unit/test_config_io.cpp:40-133); host only.
+static const char* kMinimalCube = R"({
+  "grid": {"points": [3, 3, 3]},
+  "microstructure": {"kind": "cube", "volume_fraction": 0.037},
+  "model": {"kind": "hyperelastic",
+            "phases": [{"youngs": 1.0, "poisson": 0.3},
+                       {"youngs": 10.0, "poisson": 0.3}]},
+  "loading": {"mode": "simple_shear", "gamma": 0.1, "increments": 1}
+})";
+
+static void config_cases() {
+  run("config: minimal config picks up the documented defaults", [] {
+    const RunConfig cfg = parse_config(kMinimalCube);
+    CHECK(cfg.solver.eta_newton == 1e-5 && cfg.solver.eta_cg == 1e-8 && cfg.solver.max_newton == 30);
+    CHECK(cfg.nyquist == NyquistMode::ZeroCompatible && cfg.snapshot_stride == 1 && cfg.tensor_dim() == 3);
+    CHECK(cfg.output_fields == (std::vector<std::string>{"F", "P", "eq"}));
+  });
+  run("config: poisson = 0.5 is flagged at its config path", [] {
+    std::string text = kMinimalCube;
+    text.replace(text.find("0.3"), 3, "0.5");
+    bool ok = false;
+    try {
+      parse_config(text);
+    } catch (const ConfigInvalid& e) {
+      ok = e.violations.size() == 1 && e.violations[0].find("model.phases[0].poisson") != std::string::npos;
+    }
+    CHECK(ok);
+  });
+  run("config: all violations are collected, not just the first", [] {
+    const char* broken = R"({
+      "grid": {"points": [3, 3, 3]},
+      "microstructure": {"kind": "cube", "volume_fraction": 1.5},
+      "model": {"kind": "hyperelastic",
+                "phases": [{"youngs": -1.0, "poisson": 0.7}, {"youngs": 10.0, "poisson": 0.3}]},
+      "loading": {"mode": "pure_shear", "lambda": -2.0, "increments": 0}
+    })";
+    size_t nv = 0;
+    try {
+      parse_config(broken);
+    } catch (const ConfigInvalid& e) {
+      nv = e.violations.size();
+    }
+    CHECK(nv >= 5);
+  });
+  run("config: pure shear expands to a uniform stretch ramp (plane strain Simo)", [] {
+    const RunConfig cfg = parse_config(R"({
+      "grid": {"points": [4, 4]},
+      "microstructure": {"kind": "laminate", "fractions": [0.5, 0.5]},
+      "model": {"kind": "simo", "contrast": 2.0,
+                "phases": [{"youngs": 1.0, "poisson": 0.3, "tau_y0": 0.003, "hardening": 0.01}]},
+      "loading": {"mode": "pure_shear", "lambda": 1.2, "increments": 250}
+    })");
+    CHECK(cfg.tensor_dim() == 3);
+    const LoadProgram prog = expand_loading(cfg);
+    CHECK(prog.size() == 250);
+    double worst = 0.0;
+    for (size_t t = 0; t < prog.size(); ++t) {
+      const double lam = 1.0 + 0.2 * double(t + 1) / 250.0;
+      worst = std::max({worst, std::abs(prog[t].fbar(0, 0) - lam) / lam,
+                        std::abs(prog[t].fbar(1, 1) - 1.0 / lam) * lam});
+      CHECK(prog[t].fbar(2, 2) == 1.0 && prog[t].label == std::to_string(t + 1));
+    }
+    CHECK(worst < 1e-14);
+  });
+  run("config: explicit loading lists are validated matrix by matrix", [] {
+    bool ok = false;
+    try {
+      parse_config(R"({
+        "grid": {"points": [3, 3]},
+        "microstructure": {"kind": "laminate", "fractions": [1.0]},
+        "model": {"kind": "hyperelastic", "phases": [{"youngs": 1.0, "poisson": 0.3}]},
+        "loading": {"mode": "explicit", "fbar": [[[1.0, 0.1], [0.0, 1.0]], [[-1.0, 0.0], [0.0, 1.0]]]}
+      })");
+    } catch (const ConfigInvalid& e) {
+      ok = e.violations.size() == 1 && e.violations[0].find("loading.fbar[1]") != std::string::npos;
+    }
+    CHECK(ok);
+  });
+  run("config: type errors, unknown kinds and cross-field checks", [] {
+    std::vector<std::string> v;
+    try {
+      parse_config(R"({
+        "grid": {"points": [4, "x"]},
+        "microstructure": {"kind": "sphere"},
+        "model": {"kind": "hyperelastic", "phases": [{"youngs": 1.0, "poisson": 0.3}]},
+        "loading": {"mode": "simple_shear", "gamma": 0.1, "increments": 1},
+        "output": {"fields": ["F", "epsp", "Q"], "stride": 0}
+      })");
+    } catch (const ConfigInvalid& e) {
+      v = e.violations;
+    }
+    auto has = [&](const char* s) {
+      for (const auto& x : v)
+        if (x.find(s) != std::string::npos) return true;
+      return false;
+    };
+    CHECK(has("grid.points: expected array of int") && has("microstructure.kind"));
+    CHECK(has("'epsp' requires the simo model") && has("unknown field 'Q'") && has("output.stride"));
+  });
+}
+
 static void snapshot_round_trip(const std::filesystem::path& golden) {
       namespace fs = std::filesystem;
       const fs::path dir = fs::temp_directory_path() / "fftmech_b200_unit_snapshot_out";
@@ -212,6 +314,7 @@ int main(int argc, char** argv) {
   const std::filesystem::path golden = argc > 1 ? argv[1] : (golden_env ? golden_env : "");
   if (argc > 2 && std::string(argv[2]) == "--no-device") {  // host-only cases (CPU test suite)
     run("output: snapshot round trip, bit-exact (test_config_io.cpp:135-164)", [&] { snapshot_round_trip(golden); });
+    config_cases();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
   }

@@ -15,6 +15,8 @@ RECORDS = {
     "unit_vtk_out": ["meta_1.json", "report.csv", "snapshot_1.vtk"],
     "unit_det_out1": ["meta_1.json", "meta_2.json", "meta_3.json", "report.csv"],
 }
+# the CLI smoke-test configurations (proj/tests/data)
+DATA = ["hyperelastic_cube_small.json", "bad_poisson.json"]
 
 if __name__ == "__main__":
     for d, files in RECORDS.items():
@@ -22,3 +24,7 @@ if __name__ == "__main__":
         for f in files:
             shutil.copyfile(os.path.join(SRC, d, f), os.path.join(DST, d, f))
             print("copied", d, f)
+    os.makedirs(os.path.join(DST, "data"), exist_ok=True)
+    for f in DATA:
+        shutil.copyfile(os.path.join(SRC, "tests", "data", f), os.path.join(DST, "data", f))
+        print("copied data", f)
