@@ -15,6 +15,7 @@
 //              registers between the forward and inverse x transforms.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "bulk.cuh"
 #include "proj_common.cuh"
@@ -726,11 +727,12 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   const size_t smem = size_t(N) * TW * 16;
   // default: scalar-accumulating variant up to 256 (3 CTAs/SM), whole-tile
   // prefetch at 512 (measured, scripts/xvar.py)
-  const int vdef = (ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE && N <= 256) ? 6 : 5;
+  const int vdef = ctx->mode != FM_NYQUIST_ZERO_COMPATIBLE ? 5 : (N <= 256 ? 6 : 8);
   const int var = (N <= 512 && ctx->nzh % 8 == 0) ? (x_variant() ? x_variant() : vdef) : 1;
   if (var >= 6 && N >= 64 && N <= 512 && ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE) {
     if (var == 6) x4_go<N, 8, e_line(N)>(ctx, g, spec);
     else if (var == 8) x4_go<N, 4, e_line(N)>(ctx, g, spec);
+    else if (var == 9) x4_go<N, 4, 8>(ctx, g, spec);
     else x4_go<N, 8, 8>(ctx, g, spec);
   } else if (var == 4 && N <= 256) {
     x3_go<N, 4, e_line(N)>(ctx, g, spec);
@@ -771,7 +773,7 @@ int zpipe_mode() {
 template <int M, int PRO, bool DIR, int MINB, bool PAIRS = true>
 bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   constexpr size_t smem = pipe_smem<M, PRO, DIR>();
-  if constexpr (smem > 200 * 1024 || M < 16) {
+  if constexpr (smem > 100 * 1024 || M < 16) {  // one CTA per SM does not pay (512^3: 2x slower)
     return false;
   } else {
     static const int per_sm = [] {
@@ -840,8 +842,10 @@ int zi_variant() {
   return v;
 }
 
+// z-inverse shape: 16 elements per thread, one z-line per CTA from M = 128 up
+// (measured: 643 -> 635 us at 256^3, 4.95 -> 4.67 ms at 512^3)
 template <int M>
-using ZiShape = ZShape<M>;
+using ZiShape = std::conditional_t<(M >= 128), ZS<M, 16, 1>, ZShape<M>>;
 
 template <int M>
 bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
