@@ -27,7 +27,6 @@ __device__ __forceinline__ double block_sum(double v) {
 }
 
 // Scalar slots in ctx->d_scal used by the CG driver (solver.cu).
-enum Slot { S_RR = 0, S_PAP = 1, S_RRNEW = 2, S_ALPHA = 3, S_BETA = 4, S_FLAG = 5, S_OUT = 8 };
 
 __global__ void __launch_bounds__(kRedThreads) k_dot_partial(const double* __restrict__ a,
                                                              const double* __restrict__ b,
@@ -88,6 +87,18 @@ __global__ void __launch_bounds__(kRedThreads) k_finalize(const double* __restri
     cg_scalar_op(scal, op, s);
 }
 
+// First level of a two-level finalisation: block b sums partials
+// [b*kFold, (b+1)*kFold) in a fixed order (deterministic).
+constexpr int kFold = 1024;
+__global__ void __launch_bounds__(kRedThreads) k_fold(const double* __restrict__ partial, int nb,
+                                                      double* __restrict__ out) {
+  const int lo = blockIdx.x * kFold, hi = min(nb, lo + kFold);
+  double s = 0.0;
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) s += partial[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 // distributed: the CG op applied after the cross-rank combination of scal[slot]
 __global__ void k_scalar_op(double* scal, int op, int slot) { cg_scalar_op(scal, op, scal[slot]); }
 
@@ -128,6 +139,15 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_update(double* __restrict__ 
   }
   s = block_sum(s);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// x += alpha p with the device alpha (the fused CG loop's last update)
+__global__ void k_cg_xfinal(double* __restrict__ x, const double* __restrict__ p, int64_t count,
+                            const double* scal) {
+  const double alpha = scal[S_ALPHA];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride)
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
 }
 
 // p = beta p + r   (solver.cpp:51-55, p *= beta; p += r)
@@ -180,6 +200,13 @@ static int ew_blocks(int64_t count) {
 // sum in scal[slot]; op 1/2 run the CG scalar step on it.  Distributed: the
 // local sum is combined across ranks (ordered) before the op is applied.
 static int finalize(fm_ctx* ctx, const double* partial, int nb, double* scal, int op, int slot) {
+  if (nb > 2 * kFold) {  // one block over 65536 partials costs ~60 us: fold first
+    const int nf = (nb + kFold - 1) / kFold;
+    k_fold<<<nf, kRedThreads, 0, ctx->stream>>>(partial, nb, ctx->d_fold);
+    FM_LAUNCHED(ctx);
+    partial = ctx->d_fold;
+    nb = nf;
+  }
   if (!distributed(ctx) || op == 0) {
     k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(partial, nb, scal, op, slot);
     FM_LAUNCHED(ctx);
@@ -256,10 +283,25 @@ int cg_update_async(fm_ctx* ctx, double* x, double* r, const double* p, const do
   return finalize(ctx, ctx->d_partial, ctx->red_blocks, ctx->d_scal, 2, 0);
 }
 
+int cg_final_x_async(fm_ctx* ctx, double* x, const double* p, int64_t count) {
+  k_cg_xfinal<<<ew_blocks(count), 256, 0, ctx->stream>>>(x, p, count, ctx->d_scal);
+  FM_LAUNCHED(ctx);
+  return FM_OK;
+}
+
 int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count) {
   k_cg_direction<<<ew_blocks(count), 256, 0, ctx->stream>>>(p, r, count, ctx->d_scal);
   FM_LAUNCHED(ctx);
   return FM_OK;
+}
+
+// alpha / curvature flag from arbitrary per-block partials of <p, Ap>
+int cg_pap_finalize_from(fm_ctx* ctx, const double* partials, int n) {
+  return finalize(ctx, partials, n, ctx->d_scal, 1, 0);
+}
+// beta / rr from per-block partials of <r, r> (fused z-inverse update)
+int cg_rr_finalize_from(fm_ctx* ctx, const double* partials, int n) {
+  return finalize(ctx, partials, n, ctx->d_scal, 2, 0);
 }
 
 // <p,Ap> from the partials the fused z-inverse epilogue wrote (solver.cpp:37-45)

@@ -155,6 +155,8 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
     return fail(FM_E_OOM);
   ctx->epi_cap = int64_t(ctx->Nx) * ctx->Ny + 64;
   if (cudaMalloc(&ctx->d_epi, sizeof(double) * ctx->epi_cap) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMalloc(&ctx->d_epi2, sizeof(double) * ctx->epi_cap) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMalloc(&ctx->d_fold, sizeof(double) * (ctx->epi_cap / 1024 + 64)) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMalloc(&ctx->d_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMemset(ctx->d_scal, 0, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_CUDA);
   if (cudaMallocHost(&ctx->h_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
@@ -179,6 +181,8 @@ int fm_ctx_destroy(fm_ctx* ctx) {
   if (ctx->spec) cudaFree(ctx->spec);
   if (ctx->d_partial) cudaFree(ctx->d_partial);
   if (ctx->d_epi) cudaFree(ctx->d_epi);
+  if (ctx->d_epi2) cudaFree(ctx->d_epi2);
+  if (ctx->d_fold) cudaFree(ctx->d_fold);
   if (ctx->spec2) cudaFree(ctx->spec2);
   if (ctx->d_gather) cudaFree(ctx->d_gather);
   dist_destroy(ctx);

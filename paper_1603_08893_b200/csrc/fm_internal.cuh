@@ -105,6 +105,9 @@ struct fm_ctx {
   int red_blocks = 0;
   double* d_partial = nullptr;  // red_blocks * 16
   double* d_epi = nullptr;      // per-block partials of the fused <p,Ap>
+  double* d_epi2 = nullptr;     // pass-1 partials of the fused-CG <p, K:p> (epi_cap)
+  double* d_fold = nullptr;     // first-level sums of a two-level finalisation (epi_cap / 1024 + 64)
+  int zf_partials = 0;          // partials the last pass 1 wrote
   int64_t epi_cap = 0;
   double* d_scal = nullptr;     // device scalars (64)
   double* h_scal = nullptr;     // pinned mirror (64)
@@ -119,6 +122,9 @@ struct fm_ctx {
 };
 
 namespace fm {
+
+// Device scalar slots of the CG driver (ctx->d_scal).
+enum Slot { S_RR = 0, S_PAP = 1, S_RRNEW = 2, S_ALPHA = 3, S_BETA = 4, S_FLAG = 5, S_IT = 6, S_THR = 7, S_OUT = 8 };
 
 // Launch/error helpers ------------------------------------------------------
 int set_error(fm_ctx* ctx, int status, const std::string& msg);
@@ -151,18 +157,41 @@ struct ProArgs {
   const double* r = nullptr;
   double* p = nullptr;
   const double* beta = nullptr;  // device scalar
+  // fused CG curvature: per-CTA partials of <p, dP> (= <p, G dP> = <p, Ap>
+  // since p lies in range(G) and G is self-adjoint), written by pass 1
+  double* pap_partial = nullptr;
+  // fused CG: x += alpha p_old with the previous iteration's alpha, applied
+  // where p_old is loaded anyway (pipelined SVK pass 1 only)
+  double* x = nullptr;
+  const double* alpha = nullptr;
 };
 // Epilogue of the last pass: per-block partial sums of <pdot, out>
 // (the CG curvature <p, Ap>, solver.cpp:37) written to `partial`.
 struct EpiArgs {
   const double* pdot = nullptr;
   double* partial = nullptr;
+  // fused CG update (solver.cpp:46-48) instead of storing Ap: with alpha and
+  // the curvature flag from `scal`, r -= alpha Ap, x += alpha p, and
+  // per-block partials of <r, r> into `partial`
+  double* r = nullptr;
+  double* x = nullptr;
+  const double* p = nullptr;
+  const double* scal = nullptr;
 };
 // out = scale * n * G(prologue(args)); scale = 1 gives the reference G.
 // Returns the number of partial sums written through epi (0 if none).
 int projection_run(fm_ctx* ctx, const ProArgs& args, double* out, double scale,
                    const EpiArgs& epi = EpiArgs{}, int* n_partials = nullptr);
 int profile_collect(fm_ctx* ctx);
+int cg_pap_finalize_from(fm_ctx* ctx, const double* partials, int n);
+int cg_rr_finalize_from(fm_ctx* ctx, const double* partials, int n);
+int cg_final_x_async(fm_ctx* ctx, double* x, const double* p, int64_t count);
+// True when passes 1 and 5 run the register-resident kernels that carry the
+// fused CG iteration (single device, pow2 z, ZeroCompatible, tdim 3).
+bool cg_fused_supported(const fm_ctx* ctx);
+// True when pass 1 of operator `kind` runs the pipelined kernel that can also
+// carry the CG x update (ProArgs::x).
+bool cg_xupd_supported(const fm_ctx* ctx, int kind);
 // dist.cu: the slab all-to-all (dir +1: packed B -> x-pass A, -1: back)
 int transpose(fm_ctx* ctx, int dir);
 // Ordered cross-rank sum of `count` device scalars (no-op unless distributed).

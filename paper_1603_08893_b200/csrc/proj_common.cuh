@@ -116,9 +116,10 @@ __device__ __forceinline__ void svk_action(const double* f, const double* d, dou
     }
 }
 
-template <int TD, int PRO, bool DIR = false>
+// PAP: also accumulate <dF, dP> of the voxel into *pap (fused CG curvature).
+template <int TD, int PRO, bool DIR = false, bool PAP = false>
 __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int64_t node,
-                                               double v[TD * TD]) {
+                                               double v[TD * TD], double* pap = nullptr) {
   constexpr int NC = TD * TD;
   if (PRO == PRO_COPY) {
 #pragma unroll
@@ -136,6 +137,10 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
         for (int kl = 0; kl < NC; ++kl) s += __ldg(pa.K + ((j * TD + i) * NC + kl) * n + node) * df[kl];
         v[i * TD + j] = s;
       }
+    if constexpr (PAP) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) *pap += df[c] * v[c];
+    }
     store_dir<NC, DIR>(pa, n, node, df);
   } else if (PRO == PRO_J2C) {
     // Compact J2 tangent action (constitutive.cu, simo.cpp:131-194 in the
@@ -181,6 +186,10 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
 #pragma unroll
         for (int j = 0; j < 3; ++j)
           v[i * 3 + j] = T[i * 3 + 0] * U[j * 3 + 0] + T[i * 3 + 1] * U[j * 3 + 1] + T[i * 3 + 2] * U[j * 3 + 2];
+      if constexpr (PAP) {
+#pragma unroll
+        for (int c = 0; c < 9; ++c) *pap += d[c] * v[c];
+      }
       store_dir<9, DIR>(pa, n, node, d);
     }
   } else {
@@ -190,6 +199,10 @@ __device__ __forceinline__ void prologue_voxel(const ProArgs& pa, int64_t n, int
 #pragma unroll
     for (int c = 0; c < NC; ++c) f[c] = __ldg(pa.F + c * n + node);
     svk_action<TD>(f, d, __ldg(pa.lam + node), __ldg(pa.mu + node), v);
+    if constexpr (PAP) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) *pap += d[c] * v[c];
+    }
     store_dir<NC, DIR>(pa, n, node, d);
   }
 }

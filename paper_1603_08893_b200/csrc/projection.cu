@@ -386,6 +386,8 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   prof_mark(ctx);
   for (int r = r0; r < r1; ++r)
     if (int st = pass_zf<TD>(ctx, geo_zy(ctx, r), pa, spec_a(ctx, r))) return st;
+  if (pa.pap_partial)  // fused CG: alpha from <p, K:p> before the remaining passes
+    if (int st = cg_pap_finalize_from(ctx, pa.pap_partial, ctx->zf_partials)) return st;
   prof_mark(ctx);
   for (int r = r0; r < r1; ++r)
     if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), -1, spec_a(ctx, r), spec_b(ctx, r))) return st;

@@ -355,7 +355,7 @@ struct ZShapeSel {
 template <int M, bool HEAVY = false>
 using ZShape = typename ZShapeSel<M, HEAVY>::type;
 
-template <int M, int PRO, bool DIR>
+template <int M, int PRO, bool DIR, bool PAP = false>
 __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast(Geo g, const double2* __restrict__ twM,
                                                                 const double2* __restrict__ twN,
                                                                 ProArgs pa, double2* __restrict__ spec) {
@@ -372,14 +372,15 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
   // voxels' loads in flight together and one 16-byte shared store per
   // component; heavy ones (K4, compact J2) one voxel per thread (registers)
   constexpr bool PAIRS = (PRO == PRO_COPY || PRO == PRO_SVK);
+  double pap = 0.0;  // fused CG: <p, dP> over this CTA's voxels
   if constexpr (PAIRS) {
     constexpr int N2 = N / 2;
     for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
       const int gi = w / N2, m = w - gi * N2;
       const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
       double v0[9], v1[9];
-      prologue_voxel<3, PRO, DIR>(pa, g.n, node, v0);
-      prologue_voxel<3, PRO, DIR>(pa, g.n, node + 1, v1);
+      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v0, &pap);
+      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node + 1, v1, &pap);
 #pragma unroll
       for (int c = 0; c < 9; ++c) sm[m * LSP + c * G + gi] = make_double2(v0[c], v1[c]);
     }
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
       const int gi = w / N, z = w - gi * N;
       const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
       double v[9];
-      prologue_voxel<3, PRO, DIR>(pa, g.n, node, v);
+      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v, &pap);
 #pragma unroll
       for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] = v[c];
     }
@@ -419,6 +420,10 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
     const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
     spec[(int64_t(c) * nxy + L0 + gi) * M + k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
   }
+  if constexpr (PAP) {
+    pap = block_sum_any(pap);
+    if (threadIdx.x == 0) pa.pap_partial[blockIdx.x] = pap;
+  }
 }
 
 // Pipelined z-forward pass for the light prologues (projection input copy,
@@ -434,21 +439,22 @@ struct ZPipe {
   static constexpr int THREADS = 9 * T;
   static constexpr size_t FFT_SM = size_t(M) * LSP * 16;
 };
-template <int PRO, bool DIR>
+template <int PRO, bool DIR, bool XUPD = false>
 constexpr int pipe_chunks() {
-  return PRO == PRO_COPY ? 9 : (DIR ? 29 : 20);
+  return PRO == PRO_COPY ? 9 : (DIR ? (XUPD ? 38 : 29) : 20);
 }
-template <int M, int PRO, bool DIR>
+template <int M, int PRO, bool DIR, bool XUPD = false>
 constexpr size_t pipe_smem() {
-  return ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR>()) * 2 * M * 8;
+  return ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR, XUPD>()) * 2 * M * 8;
 }
 
-template <int M, int PRO, bool DIR, int MINB, bool PAIRS = true>
+template <int M, int PRO, bool DIR, int MINB, bool PAIRS = true, bool PAP = false, bool XUPD = false>
 __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, const double2* __restrict__ twM,
                                                                const double2* __restrict__ twN, ProArgs pa,
                                                                double2* __restrict__ spec) {
   using S = ZPipe<M>;
-  constexpr int N = 2 * M, LSP = S::LSP, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR>();
+  constexpr int N = 2 * M, LSP = S::LSP, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR, XUPD>();
+  static_assert(!XUPD || (DIR && PAIRS && PRO == PRO_SVK), "x update rides on the pair-wise SVK direction prologue");
   extern __shared__ __align__(16) double2 sm[];
   double* stage = reinterpret_cast<double*>(sm + M * LSP);  // NCH chunks of N doubles
   __shared__ uint64_t bar;
@@ -465,6 +471,8 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
       if constexpr (DIR) {
         for (int c = 0; c < 9; ++c) cp(pa.r + c * n);
         for (int c = 0; c < 9; ++c) cp(pa.p + c * n);
+        if constexpr (XUPD)
+          for (int c = 0; c < 9; ++c) cp(pa.x + c * n);
       } else {
         for (int c = 0; c < 9; ++c) cp(pa.A + c * n);
       }
@@ -475,6 +483,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   };
   if (threadIdx.x == 0) bulk::mbar_init(&bar, 1);
   __syncthreads();
+  double pap = 0.0;  // fused CG: <p, dP> over this CTA's voxels
   int L = blockIdx.x;
   if (threadIdx.x == 0 && L < nxy) issue(L);
   unsigned phase = 0;
@@ -497,6 +506,10 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
 #pragma unroll
         for (int c = 0; c < 9; ++c) f[c] = stage[(FB + c) * N + z];
         svk_action<3>(f, d, stage[(FB + 9) * N + z], stage[(FB + 10) * N + z], v);
+        if constexpr (PAP) {
+#pragma unroll
+          for (int c = 0; c < 9; ++c) pap += d[c] * v[c];
+        }
         if constexpr (DIR) {
           const int64_t node = g.roff + int64_t(L) * N + z;
 #pragma unroll
@@ -520,12 +533,20 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
         double d0[9], d1[9], f0[9], f1[9];
         if constexpr (DIR) {
           const double beta = *pa.beta;
+          double alpha = 0.0;
+          if constexpr (XUPD) alpha = *pa.alpha;
 #pragma unroll
           for (int c = 0; c < 9; ++c) {
             const double2 r = *reinterpret_cast<const double2*>(stage + c * N + 2 * m);
             const double2 p = *reinterpret_cast<const double2*>(stage + (9 + c) * N + 2 * m);
             d0[c] = __dadd_rn(__dmul_rn(p.x, beta), r.x);
             d1[c] = __dadd_rn(__dmul_rn(p.y, beta), r.y);
+            if constexpr (XUPD) {  // x += alpha p_old (solver.cpp:46, k_cg_update rounding)
+              double2 xv = *reinterpret_cast<const double2*>(stage + (18 + c) * N + 2 * m);
+              xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, p.x));
+              xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, p.y));
+              *reinterpret_cast<double2*>(pa.x + c * n + g.roff + int64_t(L) * N + 2 * m) = xv;
+            }
           }
         } else {
 #pragma unroll
@@ -535,7 +556,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
             d1[c] = a.y;
           }
         }
-        constexpr int FB = DIR ? 18 : 9;
+        constexpr int FB = DIR ? (XUPD ? 27 : 18) : 9;
 #pragma unroll
         for (int c = 0; c < 9; ++c) {
           const double2 a = *reinterpret_cast<const double2*>(stage + (FB + c) * N + 2 * m);
@@ -546,6 +567,12 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
         const double2 mu = *reinterpret_cast<const double2*>(stage + (FB + 10) * N + 2 * m);
         svk_action<3>(f0, d0, lm.x, mu.x, v0);
         svk_action<3>(f1, d1, lm.y, mu.y, v1);
+        if constexpr (PAP) {
+#pragma unroll
+          for (int c = 0; c < 9; ++c) pap += d0[c] * v0[c];
+#pragma unroll
+          for (int c = 0; c < 9; ++c) pap += d1[c] * v1[c];
+        }
         if constexpr (DIR) {
           const int64_t node = g.roff + int64_t(L) * N + 2 * m;
 #pragma unroll
@@ -580,6 +607,10 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
     }
     __syncthreads();  // sm free for the next line's prologue
   }
+  if constexpr (PAP) {
+    pap = block_sum_any(pap);
+    if (threadIdx.x == 0) pa.pap_partial[blockIdx.x] = pap;
+  }
 }
 
 template <int M, typename S = ZShape<M>>
@@ -595,6 +626,15 @@ __global__ void __launch_bounds__(S::THREADS, 2048 / S::THREADS >= 4 ? 4 : 1)
     const int c = w / (Gb * M), rem = w - c * (Gb * M);
     const int gi = rem / M, k = rem - gi * M;
     cp_async16(sm + k * LSP + c * G + gi, spec + (int64_t(c) * nxy + L0 + gi) * M + k);
+  }
+  // fused CG: the residual lines the epilogue updates, staged next to the spectrum
+  double2* rs = sm + M * LSP;  // [gi][c][N/2] voxel pairs
+  if (epi.r) {
+    for (int w = threadIdx.x; w < 9 * Gb * (N / 2); w += blockDim.x) {
+      const int gc = w / (N / 2), m = w - gc * (N / 2);
+      const int gi = gc / 9, c = gc - gi * 9;
+      cp_async16(rs + w, epi.r + c * g.n + g.roff + int64_t(L0 + gi) * N + 2 * m);
+    }
   }
   cp_async_wait_all();
   __syncthreads();
@@ -623,6 +663,39 @@ __global__ void __launch_bounds__(S::THREADS, 2048 / S::THREADS >= 4 ? 4 : 1)
   // component (node is even: N, the slab offset and the slab stride are even)
   double dot = 0.0;
   constexpr int N2 = N / 2;
+  if (epi.r) {
+    // fused CG update, solver.cpp:46-48 with the rounding of k_cg_update:
+    // Ap stays on chip; r -= alpha Ap, x += alpha p, partial <r, r>
+    if (epi.scal[S_FLAG] == 0.0) {
+      const double alpha = epi.scal[S_ALPHA];
+      for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
+        const int gi = w / N2, m = w - gi * N2;
+        const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+          const double2 zz = sm[m * LSP + c * G + gi];
+          const double2 av = make_double2(zz.x * scale, zz.y * scale);
+          double2 rv = rs[(gi * 9 + c) * N2 + m];
+          if (epi.x) {  // else the next pass 1 applies x += alpha p (ProArgs::x)
+            double2* xp = reinterpret_cast<double2*>(epi.x + c * g.n + node);
+            const double2 pv = __ldg(reinterpret_cast<const double2*>(epi.p + c * g.n + node));
+            double2 xv = *xp;
+            xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+            xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+            *xp = xv;
+          }
+          rv.x = __dadd_rn(rv.x, __dmul_rn(-alpha, av.x));
+          rv.y = __dadd_rn(rv.y, __dmul_rn(-alpha, av.y));
+          *reinterpret_cast<double2*>(epi.r + c * g.n + node) = rv;
+          dot += rv.x * rv.x;
+          dot += rv.y * rv.y;
+        }
+      }
+    }
+    dot = block_sum_any(dot);
+    if (threadIdx.x == 0) epi.partial[blockIdx.x] = dot;
+    return;
+  }
   for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
     const int gi = w / N2, m = w - gi * N2;
     const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
@@ -662,8 +735,39 @@ int launched(fm_ctx* ctx, const char* what) {
   return e == cudaSuccess ? FM_OK : check_cuda(ctx, e, what);
 }
 
+int y_tw() {
+  static int v = [] {
+    const char* e = getenv("FM_YTW");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int N, int TW>
+void y_go(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out) {
+  constexpr int T = N / e_line(N);
+  const size_t smem = size_t(N) * TW * 16;
+  const dim3 grid(ctx->nzh / TW, g.Nx, ctx->ncomp);
+  if (sign < 0) {
+    static bool a = (allow(k_y_fast<N, TW, -1>, smem), true);
+    (void)a;
+    k_y_fast<N, TW, -1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
+  } else {
+    static bool a = (allow(k_y_fast<N, TW, +1>, smem), true);
+    (void)a;
+    k_y_fast<N, TW, +1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
+  }
+}
+
 template <int N>
 bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st) {
+  if constexpr (N >= 256 && N <= 512) {
+    if (y_tw() == 4 && ctx->nzh % 4 == 0) {
+      y_go<N, 4>(ctx, g, sign, in, out);
+      *st = launched(ctx, "k_y_fast");
+      return true;
+    }
+  }
   constexpr int TW = N >= 1024 ? 4 : 8;
   constexpr int T = N / e_line(N);
   const size_t smem = size_t(N) * TW * 16;
@@ -752,35 +856,37 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   return true;
 }
 
-template <int M, int PRO, bool DIR>
+template <int M, int PRO, bool DIR, bool PAP>
 void zf_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   using S = ZShape<M, PRO != PRO_COPY>;
-  static bool a = (allow(k_zf_fast<M, PRO, DIR>, S::SMEM), true);
+  static bool a = (allow(k_zf_fast<M, PRO, DIR, PAP>, S::SMEM), true);
   (void)a;
   const int nxy = g.Nx * g.Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
-  k_zf_fast<M, PRO, DIR><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
+  k_zf_fast<M, PRO, DIR, PAP><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
+  ctx->zf_partials = int(grid.x);
 }
 
-int zpipe_mode() {
+int zpipe_mode() {  // FM_ZPIPE=0 disables the pipelined z-forward pass
   static int v = [] {
     const char* e = getenv("FM_ZPIPE");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 1;
   }();
   return v;
 }
 
-template <int M, int PRO, bool DIR, int MINB, bool PAIRS = true>
+// 3 CTAs/SM register budget (measured best of 1..4 and single-voxel variants)
+template <int M, int PRO, bool DIR, bool PAP, bool XUPD = false>
 bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
-  constexpr size_t smem = pipe_smem<M, PRO, DIR>();
+  constexpr size_t smem = pipe_smem<M, PRO, DIR, XUPD>();
   if constexpr (smem > 100 * 1024 || M < 16) {  // one CTA per SM does not pay (512^3: 2x slower)
     return false;
   } else {
     static const int per_sm = [] {
-      allow(k_zf_pipe<M, PRO, DIR, MINB, PAIRS>, smem);
+      allow(k_zf_pipe<M, PRO, DIR, 3, true, PAP, XUPD>, smem);
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MINB, PAIRS>, ZPipe<M>::THREADS,
-                                                    smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, 3, true, PAP, XUPD>,
+                                                    ZPipe<M>::THREADS, smem);
       cudaGetLastError();
       return b > 0 ? b : 1;
     }();
@@ -789,49 +895,65 @@ bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int nxy = g.Nx * g.Ny;
     const int grid = std::min(nxy, std::max(sms, 1) * per_sm);
-    k_zf_pipe<M, PRO, DIR, MINB, PAIRS><<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
+    k_zf_pipe<M, PRO, DIR, 3, true, PAP, XUPD>
+        <<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
+    ctx->zf_partials = grid;
     return true;
   }
+}
+
+template <int M, int PRO, bool PAP>
+void zf_kind(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, bool dir, int* st) {
+  if constexpr (PRO == PRO_SVK) {
+    if (pa.x) {  // fused CG x update: only the pipelined kernel carries it (cg_xupd_supported)
+      if (dir && PAP && zpipe_go<M, PRO, true, PAP, true>(ctx, g, pa, spec)) {
+        *st = launched(ctx, "k_zf_pipe");
+      } else {
+        *st = set_error(ctx, FM_E_UNSUPPORTED, "fused x update without the pipelined z-forward pass");
+      }
+      return;
+    }
+    if (zpipe_mode() && (dir ? zpipe_go<M, PRO, true, PAP>(ctx, g, pa, spec)
+                             : zpipe_go<M, PRO, false, PAP>(ctx, g, pa, spec))) {
+      *st = launched(ctx, "k_zf_pipe");
+      return;
+    }
+  }
+  if (dir) zf_go<M, PRO, true, PAP>(ctx, g, pa, spec);
+  else zf_go<M, PRO, false, PAP>(ctx, g, pa, spec);
+  *st = launched(ctx, "k_zf_fast");
 }
 
 template <int M>
 bool zf_launch(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int* st) {
   const bool dir = pa.r != nullptr;
-  if (zpipe_mode() && (pa.kind == PRO_COPY || pa.kind == PRO_SVK)) {
-    bool ok = false;
-    if (pa.kind == PRO_COPY) ok = zpipe_go<M, PRO_COPY, false, 1>(ctx, g, pa, spec);
-    else if (zpipe_mode() == 3) ok = dir ? zpipe_go<M, PRO_SVK, true, 3>(ctx, g, pa, spec)
-                                         : zpipe_go<M, PRO_SVK, false, 3>(ctx, g, pa, spec);
-    else if (zpipe_mode() == 4) ok = dir ? zpipe_go<M, PRO_SVK, true, 4>(ctx, g, pa, spec)
-                                         : zpipe_go<M, PRO_SVK, false, 4>(ctx, g, pa, spec);
-    else if (zpipe_mode() == 5) ok = dir ? zpipe_go<M, PRO_SVK, true, 1, false>(ctx, g, pa, spec)
-                                         : zpipe_go<M, PRO_SVK, false, 1, false>(ctx, g, pa, spec);
-    else if (zpipe_mode() == 6) ok = dir ? zpipe_go<M, PRO_SVK, true, 3, false>(ctx, g, pa, spec)
-                                         : zpipe_go<M, PRO_SVK, false, 3, false>(ctx, g, pa, spec);
-    else ok = dir ? zpipe_go<M, PRO_SVK, true, 1>(ctx, g, pa, spec) : zpipe_go<M, PRO_SVK, false, 1>(ctx, g, pa, spec);
-    if (ok) {
+  const bool pap = pa.pap_partial != nullptr;
+  if (pa.kind == PRO_COPY) {
+    if (zpipe_mode() && zpipe_go<M, PRO_COPY, false, false>(ctx, g, pa, spec)) {
       *st = launched(ctx, "k_zf_pipe");
       return true;
     }
+    zf_go<M, PRO_COPY, false, false>(ctx, g, pa, spec);
+    *st = launched(ctx, "k_zf_fast");
+  } else if (pa.kind == PRO_K4) {
+    pap ? zf_kind<M, PRO_K4, true>(ctx, g, pa, spec, dir, st) : zf_kind<M, PRO_K4, false>(ctx, g, pa, spec, dir, st);
+  } else if (pa.kind == PRO_J2C) {
+    pap ? zf_kind<M, PRO_J2C, true>(ctx, g, pa, spec, dir, st) : zf_kind<M, PRO_J2C, false>(ctx, g, pa, spec, dir, st);
+  } else {
+    pap ? zf_kind<M, PRO_SVK, true>(ctx, g, pa, spec, dir, st) : zf_kind<M, PRO_SVK, false>(ctx, g, pa, spec, dir, st);
   }
-  if (pa.kind == PRO_COPY) zf_go<M, PRO_COPY, false>(ctx, g, pa, spec);
-  else if (pa.kind == PRO_K4 && !dir) zf_go<M, PRO_K4, false>(ctx, g, pa, spec);
-  else if (pa.kind == PRO_K4) zf_go<M, PRO_K4, true>(ctx, g, pa, spec);
-  else if (pa.kind == PRO_J2C && !dir) zf_go<M, PRO_J2C, false>(ctx, g, pa, spec);
-  else if (pa.kind == PRO_J2C) zf_go<M, PRO_J2C, true>(ctx, g, pa, spec);
-  else if (!dir) zf_go<M, PRO_SVK, false>(ctx, g, pa, spec);
-  else zf_go<M, PRO_SVK, true>(ctx, g, pa, spec);
-  *st = launched(ctx, "k_zf_fast");
   return true;
 }
 
 template <int M, typename S>
 void zi_go(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi) {
-  static bool a = (allow(k_zi_fast<M, S>, S::SMEM), true);
+  constexpr size_t kR = size_t(9) * S::G * 2 * M * 8;  // fused CG: staged residual lines
+  static bool a = (allow(k_zi_fast<M, S>, S::SMEM + kR), true);
   (void)a;
   const int nxy = g.Nx * g.Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
-  k_zi_fast<M, S><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+  const size_t smem = S::SMEM + (epi.r ? kR : 0);
+  k_zi_fast<M, S><<<grid, S::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
 }
 
 int zi_variant() {
@@ -916,6 +1038,18 @@ bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double
              int* st) {
   if (!fast_z_ok(ctx)) return false;
   FM_HALF_CASES(zi_launch, ctx->Nz / 2, ctx, g, spec, out, scale, epi, st)
+}
+
+bool cg_xupd_supported(const fm_ctx* ctx, int kind) {
+  const int M = ctx->Nz / 2;
+  return kind == PRO_SVK && zpipe_mode() && cg_fused_supported(ctx) &&
+         pipe_smem<128, PRO_SVK, true, true>() <= 100 * 1024 && M <= 128;
+}
+
+bool cg_fused_supported(const fm_ctx* ctx) {
+  const int M = ctx->Nz / 2;
+  const bool pow2 = M >= 16 && M <= 512 && (M & (M - 1)) == 0;
+  return fast_z_ok(ctx) && pow2 && ctx->P == 1 && !ctx->virt;
 }
 
 int zi_fast_blocks(const fm_ctx* ctx, const Geo& g) {

@@ -10,7 +10,6 @@
 
 namespace fm {
 
-enum Slot { S_RR = 0, S_PAP = 1, S_RRNEW = 2, S_ALPHA = 3, S_BETA = 4, S_FLAG = 5, S_IT = 6, S_THR = 7, S_OUT = 8 };
 
 // ---- CG loop as a CUDA graph --------------------------------------------
 // Body of the while-conditional node: one fused CG iteration, then this
@@ -28,6 +27,7 @@ __global__ void k_cg_control(cudaGraphConditionalHandle h, double* scal, double 
 // beta = 0 makes the fused p = beta p + r of the first iteration p = r = b.
 __global__ void k_cg_init(double* scal, double thr) {
   scal[S_BETA] = 0.0;
+  scal[S_ALPHA] = 0.0;  // fused x update of the first iteration adds 0 p
   scal[S_IT] = 0.0;
   scal[S_THR] = thr;
   scal[S_FLAG] = 0.0;
@@ -83,6 +83,67 @@ int op_apply_cg(fm_ctx* ctx, const Op& op, double* p, const double* r, bool firs
   epi.pdot = p;
   epi.partial = ctx->d_epi;
   return projection_run(ctx, pa, Ap, 1.0, epi, n_partials);
+}
+
+// Fused CG iteration (single device, register-resident passes): pass 1 forms
+// p = beta p + r, dP = K:p and the curvature <p, dP> = <p, G dP> = <p, Ap>
+// (p stays in range(G), G is a self-adjoint projector); alpha is finalised
+// before pass 2; pass 5 applies r -= alpha Ap, x += alpha p and writes the
+// <r, r> partials without ever storing Ap (1456 -> 1240 B/voxel per iteration).
+static bool cg_fused(const fm_ctx* ctx) {
+  static const int env = [] {
+    const char* e = getenv("FM_CG_FUSED");
+    return e ? atoi(e) : 1;
+  }();
+  return env != 0 && cg_fused_supported(ctx);
+}
+
+int op_apply_cg_fused(fm_ctx* ctx, const Op& op, double* p, double* r, bool first, double* x, int* n_partials) {
+  // SVK through the pipelined pass 1: x += alpha_prev p_old rides on pass 1
+  // (p_old is staged there anyway) and the final update follows the loop
+  const bool xupd = cg_xupd_supported(ctx, op.kind);
+  ProArgs pa;
+  pa.kind = op.kind;
+  pa.A = p;
+  pa.K = op.K;
+  pa.F = op.F;
+  pa.lam = op.lam;
+  pa.mu = op.mu;
+  pa.pap_partial = ctx->d_epi2;
+  if (!first) {
+    pa.r = r;
+    pa.p = p;
+    pa.beta = ctx->d_scal + S_BETA;
+    if (xupd) {
+      pa.x = x;
+      pa.alpha = ctx->d_scal + S_ALPHA;
+    }
+  }
+  EpiArgs epi;
+  epi.r = r;
+  epi.x = xupd ? nullptr : x;
+  epi.p = p;
+  epi.scal = ctx->d_scal;
+  epi.partial = ctx->d_epi;
+  return projection_run(ctx, pa, nullptr, 1.0, epi, n_partials);
+}
+
+// one CG iteration in either form; leaves S_FLAG / S_RRNEW / S_BETA / S_RR set
+static int cg_iteration(fm_ctx* ctx, const Op& op, double* x, int64_t count, bool first) {
+  int nparts = 0;
+  if (cg_fused(ctx)) {
+    if (int st = op_apply_cg_fused(ctx, op, ctx->p.d, ctx->r.d, first, x, &nparts)) return st;
+    return cg_rr_finalize_from(ctx, ctx->d_epi, nparts);
+  }
+  if (int st = op_apply_cg(ctx, op, ctx->p.d, ctx->r.d, first, ctx->Ap.d, &nparts)) return st;
+  if (int st = cg_pap_finalize_async(ctx, nparts)) return st;
+  return cg_update_async(ctx, x, ctx->r.d, ctx->p.d, ctx->Ap.d, count);  // :46-48
+}
+
+// Converged: the last iteration's x += alpha p that pass 1 would have applied.
+static int cg_finish_x(fm_ctx* ctx, const Op& op, double* x, int64_t count) {
+  if (!cg_fused(ctx) || !cg_xupd_supported(ctx, op.kind)) return FM_OK;
+  return cg_final_x_async(ctx, x, ctx->p.d, count);
 }
 
 Op model_op(fm_model* m) {
@@ -148,10 +209,7 @@ int cg_loop_graph(fm_ctx* ctx, const Op& op, double* x, int64_t count, int64_t c
     FM_CUDA(ctx, cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     ctx->capturing = true;
     const int64_t l0 = ctx->cnt.launches;
-    int nparts = 0;
-    int st = op_apply_cg(ctx, op, ctx->p.d, ctx->r.d, false, ctx->Ap.d, &nparts);
-    if (!st) st = cg_pap_finalize_async(ctx, nparts);
-    if (!st) st = cg_update_async(ctx, x, ctx->r.d, ctx->p.d, ctx->Ap.d, count);
+    int st = cg_iteration(ctx, op, x, count, false);
     if (!st) {
       k_cg_control<<<1, 1, 0, ctx->stream>>>(h, ctx->d_scal, double(cap));
       st = cudaGetLastError() == cudaSuccess ? FM_OK : set_error(ctx, FM_E_CUDA, "k_cg_control launch");
@@ -186,7 +244,7 @@ int cg_loop_graph(fm_ctx* ctx, const Op& op, double* x, int64_t count, int64_t c
   }
   if (std::sqrt(hs[S_RRNEW]) <= thr) {  // :49-50
     *rel = std::sqrt(hs[S_RRNEW]) / bnorm;
-    return FM_OK;
+    return cg_finish_x(ctx, op, x, count);
   }
   *rel = std::sqrt(hs[S_RR]) / bnorm;
   const int st = set_error(ctx, FM_E_CG_STALLED, "conjugate gradient stalled after " + std::to_string(cap) + " iterations");
@@ -200,7 +258,8 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
   const int64_t count = ctx->n * ctx->ncomp;
   if (int st = ensure_field(ctx, ctx->r, ctx->ncomp)) return st;
   if (int st = ensure_field(ctx, ctx->p, ctx->ncomp)) return st;
-  if (int st = ensure_field(ctx, ctx->Ap, ctx->ncomp)) return st;
+  if (!cg_fused(ctx))  // the fused iteration never stores Ap
+    if (int st = ensure_field(ctx, ctx->Ap, ctx->ncomp)) return st;
   FM_CUDA(ctx, cudaMemsetAsync(x, 0, sizeof(double) * count, ctx->stream));  // :22
   // bnorm = |b|; rr = <r,r> with r = b  (:24, :31-33)
   if (int st = dot_async(ctx, b, b, count, ctx->d_scal + S_RR)) return st;
@@ -219,10 +278,7 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
   if (cg_graph_enabled(ctx)) return cg_loop_graph(ctx, op, x, count, cap, eta_cg * bnorm, bnorm, iters, rel);
   for (int64_t it = 1; it <= cap; ++it) {
     // :36-37 with :51-55 of the previous iteration folded in (p = beta p + r)
-    int nparts = 0;
-    if (int st = op_apply_cg(ctx, op, ctx->p.d, ctx->r.d, it == 1, ctx->Ap.d, &nparts)) return st;
-    if (int st = cg_pap_finalize_async(ctx, nparts)) return st;
-    if (int st = cg_update_async(ctx, x, ctx->r.d, ctx->p.d, ctx->Ap.d, count)) return st;  // :46-48
+    if (int st = cg_iteration(ctx, op, x, count, it == 1)) return st;
     if (int st = fetch_scalars(ctx, S_FLAG + 1)) return st;
     if (ctx->h_scal[S_FLAG] != 0.0) {  // !(pAp > 0): return without updating x (:38-44)
       *iters = int32_t(it);
@@ -233,7 +289,7 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
     if (std::sqrt(rr_new) <= eta_cg * bnorm) {  // :49-50
       *iters = int32_t(it);
       *rel = std::sqrt(rr_new) / bnorm;
-      return FM_OK;
+      return cg_finish_x(ctx, op, x, count);
     }
     rr = rr_new;  // p *= beta; p += r happens in the next matvec's prologue
   }

@@ -244,3 +244,27 @@ def test_reversibility_2d():
     F, _, _, _ = gpu_run(pts, 2, "hyper", lam, mu, [fb, np.eye(2)], eta_newton=1e-9)
     I = abi.identity_field(pts, 2)
     assert np.linalg.norm(F - I) / np.linalg.norm(F) < 1e-8
+
+
+@pytest.mark.parametrize("N,kind,graph", [(32, "mf", "1"), (64, "mf", "0"), (64, "k4", "0"), (256, "mf", "0")])
+def test_fused_cg_matches_unfused(N, kind, graph):
+    """The fused CG iteration (curvature <p, K:p> from pass 1, r/x updates in
+    passes 5/1, Ap never stored) against the unfused one: the same Newton and
+    CG counts and the same converged F (1e-9); covers the partial-warp block
+    reductions of the 72/144-thread pass shapes and the graph-driven loop."""
+    import json
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = {}
+    for fused in ("0", "1"):
+        env = dict(os.environ, FM_CG_FUSED=fused, FM_CG_GRAPH=graph)
+        r = subprocess.run([sys.executable, os.path.join(here, "cg_variant_run.py"), str(N), kind],
+                           capture_output=True, text=True, env=env, timeout=600)
+        assert r.returncode == 0, r.stderr
+        out[fused] = json.loads(r.stdout.strip().splitlines()[-1])
+    a, b = out["0"], out["1"]
+    assert a["passes"] == b["passes"]
+    assert all(abs(x - y) <= 1 for x, y in zip(a["cg"], b["cg"])), (a["cg"], b["cg"])
+    fa, fb = np.array(a["F"]), np.array(b["F"])
+    assert np.linalg.norm(fa - fb) <= 1e-9 * np.linalg.norm(fa)
