@@ -342,6 +342,40 @@ def main():
                            "newton": [r["passes"] for r in reps31],
                            "cg_total": int(sum(sum(r["cg_it"]) for r in reps31))}
 
+    # ---- config 4: projection-operator microbenchmark G(x) at 128^3/256^3/512^3
+    # (seed 4 + N, nine i.i.d. U(-1,1) slabs), checked by idempotence
+    proj = None
+    if world == 1 and not args.no_e2e:
+        from paper_1603_08893_b200 import microstructure as M
+        proj = {}
+        for Np in (128, 256, 512):
+            pts = (Np, Np, Np)
+            npv = Np ** 3
+            with abi.Context(pts, 3, device=local) as cp:
+                xg = cp.field(9, M.uniform_field(pts, 9, seed=4 + Np))
+                gx = cp.field(9)
+                st = torch.cuda.ExternalStream(cp.stream, device=f"cuda:{local}")
+                for _ in range(2):
+                    cp.projection(xg, out=gx)
+                cp.sync()
+                reps = 10 if Np < 512 else 4
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(reps):
+                    cp.projection(xg, out=gx)
+                e1.record(st)
+                e1.synchronize()
+                ms_g = e0.elapsed_time(e1) / reps
+                ggx = cp.projection(gx)
+                ngx = cp.norm(gx)
+                cp.axpy(-1.0, gx, ggx)
+                idem = cp.norm(ggx) / ngx
+                b_g = 2 * 72 + 8 * 144 * (Np // 2) / Np  # B_G: 720 B/voxel, nzh = N/2
+                proj[f"{Np}^3"] = {"ms": ms_g, "voxel_per_s": npv / (ms_g * 1e-3),
+                                   "bytes_per_voxel": b_g,
+                                   "roofline_frac": b_g * npv / (ms_g * 1e-3) / 1e9 / hbm,
+                                   "idempotence": idem}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -367,6 +401,7 @@ def main():
                        "l2": "inputs 12 GB > 126 MB L2, no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "newton_solve": newton,
             "newton_solve_31": small,
+            "projection_G": proj,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line))

@@ -335,8 +335,9 @@ __global__ void __launch_bounds__(TW*(N / E), E >= 16 ? 3 : 2) k_x_fast4(Geo g, 
 // --------------------------------------------------------------- z passes
 // HEAVY: K4 / SVK prologue (720 B read per voxel): larger E, ~144 threads and
 // ~40 KB per CTA so 4 CTAs per SM overlap their load and FFT phases.
-template <int M, int E_, int G_>
+template <int M, int E_, int G_, int MINB_ = 4>
 struct ZS {
+  static constexpr int MINB = MINB_;  // CTAs per SM the register budget targets
   static constexpr int E = E_;
   static constexpr int T = M / E;
   static constexpr int G = G_;                     // z-lines per CTA
@@ -432,6 +433,11 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
 // (contiguous N-voxel chunks of every input component: 9 / 20 / 29 of them)
 // into a shared staging area with TMA bulk copies while the CTA transforms
 // the current line, so HBM reads stay in flight through the FFT phases.
+#ifndef FM_PIPE_COPY_MINB
+#define FM_PIPE_COPY_MINB 5
+#endif
+constexpr int kPipeCopyMinB = FM_PIPE_COPY_MINB;
+
 template <int M>
 struct ZPipe {
   static constexpr int E = reg::e_z(M), T = M / E;
@@ -614,7 +620,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
 }
 
 template <int M, typename S = ZShape<M>>
-__global__ void __launch_bounds__(S::THREADS, 2048 / S::THREADS >= 4 ? 4 : 1)
+__global__ void __launch_bounds__(S::THREADS, 2048 / S::THREADS >= S::MINB ? S::MINB : 1)
     k_zi_fast(Geo g, const double2* __restrict__ twM, const double2* __restrict__ twN,
               const double2* __restrict__ spec, double* __restrict__ out, double scale, EpiArgs epi) {
   constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
@@ -876,16 +882,22 @@ int zpipe_mode() {  // FM_ZPIPE=0 disables the pipelined z-forward pass
 }
 
 // 3 CTAs/SM register budget (measured best of 1..4 and single-voxel variants)
+template <int PRO, int M>
+constexpr int pipe_minb() {  // copy: fewer registers suffice up to M = 128 (512^3: 5 CTAs/SM is slower)
+  return (PRO == PRO_COPY && M <= 128) ? kPipeCopyMinB : 3;
+}
+
 template <int M, int PRO, bool DIR, bool PAP, bool XUPD = false>
 bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
+  constexpr int MB = pipe_minb<PRO, M>();
   constexpr size_t smem = pipe_smem<M, PRO, DIR, XUPD>();
   if constexpr (smem > 100 * 1024 || M < 16) {  // one CTA per SM does not pay (512^3: 2x slower)
     return false;
   } else {
     static const int per_sm = [] {
-      allow(k_zf_pipe<M, PRO, DIR, 3, true, PAP, XUPD>, smem);
+      allow(k_zf_pipe<M, PRO, DIR, MB, true, PAP, XUPD>, smem);
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, 3, true, PAP, XUPD>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, true, PAP, XUPD>,
                                                     ZPipe<M>::THREADS, smem);
       cudaGetLastError();
       return b > 0 ? b : 1;
@@ -895,7 +907,7 @@ bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int nxy = g.Nx * g.Ny;
     const int grid = std::min(nxy, std::max(sms, 1) * per_sm);
-    k_zf_pipe<M, PRO, DIR, 3, true, PAP, XUPD>
+    k_zf_pipe<M, PRO, DIR, MB, true, PAP, XUPD>
         <<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
     ctx->zf_partials = grid;
     return true;
@@ -964,10 +976,12 @@ int zi_variant() {
   return v;
 }
 
-// z-inverse shape: 16 elements per thread, one z-line per CTA from M = 128 up
-// (measured: 643 -> 635 us at 256^3, 4.95 -> 4.67 ms at 512^3)
+// z-inverse shape: 16 elements per thread, one z-line per CTA from M = 128 up,
+// registers budgeted for 6 CTAs/SM (measured at 256^3: E8/G2 643 us, E16/G1
+// 4 CTAs 636 us, 6 CTAs 580 us; 512^3: E8/G1 4.95 ms, E16/G1 4 CTAs 4.67 ms,
+// 6 CTAs spills)
 template <int M>
-using ZiShape = std::conditional_t<(M >= 128), ZS<M, 16, 1>, ZShape<M>>;
+using ZiShape = std::conditional_t<(M >= 128), ZS<M, 16, 1, (M == 128 ? 6 : 4)>, ZShape<M>>;
 
 template <int M>
 bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
@@ -980,6 +994,9 @@ bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, doub
     else if (v == 2) zi_go<M, ZS<M, 4, 1>>(ctx, g, spec, out, scale, epi);
     else if (v == 3) zi_go<M, ZS<M, 16, 1>>(ctx, g, spec, out, scale, epi);
     else if (v == 4 && M <= 128) zi_go<M, ZS<M, 4, 2>>(ctx, g, spec, out, scale, epi);
+    else if (v == 6) zi_go<M, ZS<M, 16, 1, 6>>(ctx, g, spec, out, scale, epi);
+    else if (v == 8) zi_go<M, ZS<M, 16, 1, 8>>(ctx, g, spec, out, scale, epi);
+    else if (v == 9) zi_go<M, ZS<M, 8, 1, 8>>(ctx, g, spec, out, scale, epi);
     else done = false;
   }
   if (!done) zi_go<M, ZiShape<M>>(ctx, g, spec, out, scale, epi);
@@ -1066,7 +1083,7 @@ int zi_fast_blocks(const fm_ctx* ctx, const Geo& g) {
     default: return 0;
   }
   const int v = (M >= 64 && M <= 256) ? zi_variant() : 0;
-  if (v >= 1 && v <= 3) G = 1;
+  if ((v >= 1 && v <= 3) || v >= 6) G = 1;
   if (v == 4 && M <= 128) G = 2;
   return (nxy + G - 1) / G;
 }
