@@ -99,6 +99,16 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
 
 
+def ncu_traffic(N):
+    """Per-pass DRAM bytes/voxel from the committed ncu --set full capture
+    (scripts/ncu_traffic.py -> profiles/r1_traffic_<N>.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"r1_traffic_{N}.json")) as f:
+            return json.load(f)["passes"]
+    except Exception:
+        return None
+
+
 def config2_inputs(N, seed=2):
     from paper_1603_08893_b200 import microstructure as M
     pg = M.bernoulli((N, N, N), 0.3, seed)
@@ -268,8 +278,13 @@ def main():
         dom = int(np.argmax(per_pass))
         ach = pb[dom] * n / (per_pass[dom] * 1e-3) / 1e9
         tot = sum(pb)
-        roof = {"bound": "hbm", "kernel": (PASS_NAMES_MF if matrix_free else PASS_NAMES)[dom], "achieved": ach,
-                "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": src,
+        dom_name = (PASS_NAMES_MF if matrix_free else PASS_NAMES)[dom]
+        tr = ncu_traffic(N)
+        traffic = tr[dom_name] * n if tr and dom_name in tr else None  # bytes per launch (ncu --set full)
+        roof = {"bound": "hbm", "kernel": dom_name, "achieved": ach,
+                "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                "traffic_source": "profiles/r1_traffic_%d.json (dram__bytes_read+write, one ncu --set full capture)" % N
+                if traffic else None, "peak_source": src,
                 "algorithmic_bytes_per_voxel": pb[dom],
                 "passes_ms": {k: float(v) for k, v in zip(PASS_NAMES_MF if matrix_free else PASS_NAMES, per_pass)},
                 "matvec": {"bytes_per_voxel": tot, "achieved": tot * n / (ms * 1e-3) / 1e9,
