@@ -107,71 +107,6 @@ __global__ void __launch_bounds__(TW*(N / e_x(N)), 2) k_x_fast(Geo g, const doub
     for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[j][m];
 }
 
-// x pass, shared-memory staged variant: the three components of a row are
-// transformed one at a time (E elements per thread in registers), parked in
-// shared memory at the positions the thread owns, projected there, and
-// transformed back -- trading one extra smem round trip for 1/3 of the
-// registers (more CTAs per SM).
-template <int N, int TW, int E>
-__global__ void __launch_bounds__(TW*(N / E)) k_x_fast2(Geo g, const double2* __restrict__ tw,
-                                                       double2* __restrict__ spec) {
-  constexpr int T = N / E;
-  extern __shared__ double2 sm[];
-  const int l = threadIdx.x % TW, t = threadIdx.x / TW;
-  const int kz = blockIdx.x * TW + l;
-  const int y = blockIdx.y, i = blockIdx.z;
-  const int64_t xstride = int64_t(g.Ny) * g.nzh;
-  double2* base = spec + int64_t(i * 3) * N * xstride + int64_t(y) * g.nzh + kz;
-#pragma unroll 1
-  for (int j = 0; j < 3; ++j) {
-    double2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = base[(int64_t(j) * N + t + T * m) * xstride];
-    double2* S = sm + j * N * TW + l;
-    reg::fft<N, E, -1>(v, S, TW, t, tw);
-#pragma unroll
-    for (int m = 0; m < E; ++m) S[(t + T * m) * TW] = v[m];
-  }
-  const int yg = g.y0 + y;  // global y (slab decomposition: y-slab of this rank)
-  const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
-  const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
-  const double xiy = qy * g.invL[1], xiz = (g.dim == 3) ? qz * g.invL[2] : 0.0;
-#pragma unroll 2
-  for (int m = 0; m < E; ++m) {  // own positions only: no barrier needed
-    const int kx = t + T * m;
-    double2* s0 = sm + kx * TW + l;
-    const double xix = freq_of(kx, N) * g.invL[0];
-    const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
-    const bool nyq = nyq_yz || (kx == N / 2);
-    double2 a0 = s0[0], a1 = s0[N * TW], a2 = s0[2 * N * TW];
-    if (norm2 == 0.0 || (nyq && g.mode == FM_NYQUIST_ZERO_COMPATIBLE)) {
-      a0 = a1 = a2 = make_double2(0.0, 0.0);
-    } else if (!nyq) {
-      const double sx = a0.x * xix + a1.x * xiy + a2.x * xiz;
-      const double sy = a0.y * xix + a1.y * xiy + a2.y * xiz;
-      const double inv = 1.0 / norm2;
-      const double f0 = xix * inv, f1 = xiy * inv, f2 = xiz * inv;
-      a0 = make_double2(sx * f0, sy * f0);
-      a1 = make_double2(sx * f1, sy * f1);
-      a2 = make_double2(sx * f2, sy * f2);
-    }
-    s0[0] = a0;
-    s0[N * TW] = a1;
-    s0[2 * N * TW] = a2;
-  }
-#pragma unroll 1
-  for (int j = 0; j < 3; ++j) {
-    double2 v[E];
-    double2* S = sm + j * N * TW + l;
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = S[(t + T * m) * TW];
-    __syncthreads();  // every thread has its inputs before the exchanges overwrite S
-    reg::fft<N, E, +1>(v, S, TW, t, tw);
-#pragma unroll
-    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
-  }
-}
-
 // x pass, prefetching variant: the whole tile (3 components x N x TW) is
 // requested from HBM at once with cp.async (16 B per request, 8 lanes per
 // 128-byte row) so all of it is in flight together; the components are then
@@ -454,13 +389,13 @@ constexpr size_t pipe_smem() {
   return ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR, XUPD>()) * 2 * M * 8;
 }
 
-template <int M, int PRO, bool DIR, int MINB, bool PAIRS = true, bool PAP = false, bool XUPD = false>
+template <int M, int PRO, bool DIR, int MINB, bool PAP = false, bool XUPD = false>
 __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, const double2* __restrict__ twM,
                                                                const double2* __restrict__ twN, ProArgs pa,
                                                                double2* __restrict__ spec) {
   using S = ZPipe<M>;
   constexpr int N = 2 * M, LSP = S::LSP, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR, XUPD>();
-  static_assert(!XUPD || (DIR && PAIRS && PRO == PRO_SVK), "x update rides on the pair-wise SVK direction prologue");
+  static_assert(!XUPD || (DIR && PRO == PRO_SVK), "x update rides on the SVK direction prologue");
   extern __shared__ __align__(16) double2 sm[];
   double* stage = reinterpret_cast<double*>(sm + M * LSP);  // NCH chunks of N doubles
   __shared__ uint64_t bar;
@@ -496,35 +431,6 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   for (; L < nxy; L += gridDim.x) {
     bulk::mbar_wait(&bar, phase);
     phase ^= 1;
-    if constexpr (!PAIRS && PRO == PRO_SVK) {  // one voxel per thread: fewer registers
-      double* smd = reinterpret_cast<double*>(sm);
-      for (int z = threadIdx.x; z < N; z += blockDim.x) {
-        double d[9], f[9], v[9];
-        if constexpr (DIR) {
-          const double beta = *pa.beta;
-#pragma unroll
-          for (int c = 0; c < 9; ++c) d[c] = __dadd_rn(__dmul_rn(stage[(9 + c) * N + z], beta), stage[c * N + z]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 9; ++c) d[c] = stage[c * N + z];
-        }
-        constexpr int FB = DIR ? 18 : 9;
-#pragma unroll
-        for (int c = 0; c < 9; ++c) f[c] = stage[(FB + c) * N + z];
-        svk_action<3>(f, d, stage[(FB + 9) * N + z], stage[(FB + 10) * N + z], v);
-        if constexpr (PAP) {
-#pragma unroll
-          for (int c = 0; c < 9; ++c) pap += d[c] * v[c];
-        }
-        if constexpr (DIR) {
-          const int64_t node = g.roff + int64_t(L) * N + z;
-#pragma unroll
-          for (int c = 0; c < 9; ++c) pa.p[c * n + node] = d[c];
-        }
-#pragma unroll
-        for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c) * 2 + (z & 1)] = v[c];
-      }
-    } else
     // prologue on voxel pairs (z, z+1) out of the staging area
     for (int m = threadIdx.x; m < N / 2; m += blockDim.x) {
       double v0[9], v1[9];
@@ -741,40 +647,9 @@ int launched(fm_ctx* ctx, const char* what) {
   return e == cudaSuccess ? FM_OK : check_cuda(ctx, e, what);
 }
 
-int y_tw() {
-  static int v = [] {
-    const char* e = getenv("FM_YTW");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-template <int N, int TW>
-void y_go(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out) {
-  constexpr int T = N / e_line(N);
-  const size_t smem = size_t(N) * TW * 16;
-  const dim3 grid(ctx->nzh / TW, g.Nx, ctx->ncomp);
-  if (sign < 0) {
-    static bool a = (allow(k_y_fast<N, TW, -1>, smem), true);
-    (void)a;
-    k_y_fast<N, TW, -1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
-  } else {
-    static bool a = (allow(k_y_fast<N, TW, +1>, smem), true);
-    (void)a;
-    k_y_fast<N, TW, +1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
-  }
-}
-
 template <int N>
 bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st) {
-  if constexpr (N >= 256 && N <= 512) {
-    if (y_tw() == 4 && ctx->nzh % 4 == 0) {
-      y_go<N, 4>(ctx, g, sign, in, out);
-      *st = launched(ctx, "k_y_fast");
-      return true;
-    }
-  }
-  constexpr int TW = N >= 1024 ? 4 : 8;
+  constexpr int TW = N >= 1024 ? 4 : 8;  // 4-column tiles measured slower at 256^3 and 512^3
   constexpr int T = N / e_line(N);
   const size_t smem = size_t(N) * TW * 16;
   const dim3 grid(ctx->nzh / TW, g.Nx, ctx->ncomp);
@@ -789,25 +664,6 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
   }
   *st = launched(ctx, "k_y_fast");
   return true;
-}
-
-int x_variant() {
-  static int v = [] {
-    const char* e = getenv("FM_XPASS");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-template <int N, int E>
-void x2_go(fm_ctx* ctx, const Geo& g, double2* spec) {
-  constexpr int TW = 8;
-  constexpr int T = N / E;
-  const size_t smem = size_t(3) * N * TW * 16;
-  static bool a = (allow(k_x_fast2<N, TW, E>, smem), true);
-  (void)a;
-  const dim3 grid(ctx->nzh / TW, g.Ny, 3);
-  k_x_fast2<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
 
 template <int N, int TW, int E>
@@ -835,23 +691,16 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   constexpr int TW = tw_x(N);
   constexpr int T = N / e_x(N);
   const size_t smem = size_t(N) * TW * 16;
-  // default: scalar-accumulating variant up to 256 (3 CTAs/SM), whole-tile
-  // prefetch at 512 (measured, scripts/xvar.py)
-  const int vdef = ctx->mode != FM_NYQUIST_ZERO_COMPATIBLE ? 5 : (N <= 256 ? 6 : 8);
-  const int var = (N <= 512 && ctx->nzh % 8 == 0) ? (x_variant() ? x_variant() : vdef) : 1;
-  if (var >= 6 && N >= 64 && N <= 512 && ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE) {
-    if (var == 6) x4_go<N, 8, e_line(N)>(ctx, g, spec);
-    else if (var == 8) x4_go<N, 4, e_line(N)>(ctx, g, spec);
-    else if (var == 9) x4_go<N, 4, 8>(ctx, g, spec);
-    else x4_go<N, 8, 8>(ctx, g, spec);
-  } else if (var == 4 && N <= 256) {
-    x3_go<N, 4, e_line(N)>(ctx, g, spec);
-  } else if (var == 5 && N <= 512) {
+  // Measured (scripts/xvar.py): ZeroCompatible -> scalar-accumulating k_x_fast4
+  // (8-column tiles up to 256, 4-column tiles at 512: 3 CTAs/SM); other modes
+  // -> whole-tile prefetch k_x_fast3; registers-only k_x_fast as the fallback.
+  const bool zc = ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE;
+  if (zc && N >= 64 && N <= 256 && ctx->nzh % 8 == 0) {
+    x4_go<N, 8, e_line(N)>(ctx, g, spec);
+  } else if (zc && N == 512 && ctx->nzh % 4 == 0) {
+    x4_go<N, 4, e_line(N)>(ctx, g, spec);
+  } else if (N <= 512 && ctx->nzh % 8 == 0 && !(zc && N < 64)) {
     x3_go<N, 8, e_line(N)>(ctx, g, spec);
-  } else if (var == 2) {
-    x2_go<N, e_line(N)>(ctx, g, spec);
-  } else if (var == 3) {
-    x2_go<N, e_x(N)>(ctx, g, spec);
   } else {
     static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
     (void)a;
@@ -895,9 +744,9 @@ bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
     return false;
   } else {
     static const int per_sm = [] {
-      allow(k_zf_pipe<M, PRO, DIR, MB, true, PAP, XUPD>, smem);
+      allow(k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD>, smem);
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, true, PAP, XUPD>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD>,
                                                     ZPipe<M>::THREADS, smem);
       cudaGetLastError();
       return b > 0 ? b : 1;
@@ -907,7 +756,7 @@ bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int nxy = g.Nx * g.Ny;
     const int grid = std::min(nxy, std::max(sms, 1) * per_sm);
-    k_zf_pipe<M, PRO, DIR, MB, true, PAP, XUPD>
+    k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD>
         <<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
     ctx->zf_partials = grid;
     return true;
@@ -968,14 +817,6 @@ void zi_go(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double s
   k_zi_fast<M, S><<<grid, S::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
 }
 
-int zi_variant() {
-  static int v = [] {
-    const char* e = getenv("FM_ZI");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 // z-inverse shape: 16 elements per thread, one z-line per CTA from M = 128 up,
 // registers budgeted for 6 CTAs/SM (measured at 256^3: E8/G2 643 us, E16/G1
 // 4 CTAs 636 us, 6 CTAs 580 us; 512^3: E8/G1 4.95 ms, E16/G1 4 CTAs 4.67 ms,
@@ -986,20 +827,7 @@ using ZiShape = std::conditional_t<(M >= 128), ZS<M, 16, 1, (M == 128 ? 6 : 4)>,
 template <int M>
 bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
                int* st) {
-  bool done = false;
-  if constexpr (M >= 64 && M <= 256) {
-    const int v = zi_variant();
-    done = true;
-    if (v == 1) zi_go<M, ZS<M, 8, 1>>(ctx, g, spec, out, scale, epi);
-    else if (v == 2) zi_go<M, ZS<M, 4, 1>>(ctx, g, spec, out, scale, epi);
-    else if (v == 3) zi_go<M, ZS<M, 16, 1>>(ctx, g, spec, out, scale, epi);
-    else if (v == 4 && M <= 128) zi_go<M, ZS<M, 4, 2>>(ctx, g, spec, out, scale, epi);
-    else if (v == 6) zi_go<M, ZS<M, 16, 1, 6>>(ctx, g, spec, out, scale, epi);
-    else if (v == 8) zi_go<M, ZS<M, 16, 1, 8>>(ctx, g, spec, out, scale, epi);
-    else if (v == 9) zi_go<M, ZS<M, 8, 1, 8>>(ctx, g, spec, out, scale, epi);
-    else done = false;
-  }
-  if (!done) zi_go<M, ZiShape<M>>(ctx, g, spec, out, scale, epi);
+  zi_go<M, ZiShape<M>>(ctx, g, spec, out, scale, epi);
   *st = launched(ctx, "k_zi_fast");
   return true;
 }
@@ -1082,9 +910,6 @@ int zi_fast_blocks(const fm_ctx* ctx, const Geo& g) {
     case 512: G = ZiShape<512>::G; break;
     default: return 0;
   }
-  const int v = (M >= 64 && M <= 256) ? zi_variant() : 0;
-  if ((v >= 1 && v <= 3) || v >= 6) G = 1;
-  if (v == 4 && M <= 128) G = 2;
   return (nxy + G - 1) / G;
 }
 
