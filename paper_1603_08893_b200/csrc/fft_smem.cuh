@@ -33,9 +33,13 @@ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -
 // result (a or b).  sign = -1 forward, +1 backward (unnormalised).
 // lfast: thread index maps to the line first (use when lines are
 // interleaved element-wise, ls == 1) so smem accesses are consecutive.
+// tws: shared-memory space for the N-entry twiddle table (staged here once;
+// latency-bound small grids otherwise wait on one L2 round trip per term).
 __device__ __forceinline__ double2* fft_smem(double2* a, double2* b, int nl, int ls, int es,
-                                             const AxisPlan& P, int sign, bool lfast) {
+                                             const AxisPlan& P, int sign, bool lfast, double2* tws) {
   const int N = P.N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) tws[i] = __ldg(&P.tw[i]);
+  __syncthreads();
   int Ns = 1;
   for (int s = 0; s < P.nst; ++s) {
     const int R = P.radix[s];
@@ -58,11 +62,14 @@ __device__ __forceinline__ double2* fft_smem(double2* a, double2* b, int nl, int
       const double2* src = a + l * ls + j * es;
       double2 acc = src[0];
       int ex = 0;
+      // unrolled: the loads of 4 terms are issued together (small grids are
+      // load-latency bound here); the accumulation order is unchanged
+#pragma unroll 4
       for (int r = 1; r < R; ++r) {
         ex += e0;
         if (ex >= N) ex -= N;
         const double2 v = src[r * NR * es];
-        const double2 t = __ldg(&P.tw[ex]);
+        const double2 t = tws[ex];
         acc = cadd(acc, sign < 0 ? cmul(v, t) : cmulc(v, t));
       }
       b[l * ls + o * es] = acc;

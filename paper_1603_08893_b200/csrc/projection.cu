@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double
     }
   }
   __syncthreads();
-  double2* R = fft_smem(A, B, NC * G, ls, 1, plan, -1, false);
+  double2* R = fft_smem(A, B, NC * G, ls, 1, plan, -1, false, sm + 2 * NC * G * ls);
   const int M = g.Lz;
   for (int w = threadIdx.x; w < NC * Gb * g.nzh; w += blockDim.x) {
     const int line = w / g.nzh, k = w - line * g.nzh;
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, const doubl
       A[w] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  double2* R = fft_smem(A, B, TW, 1, TW, plan, sign, true);
+  double2* R = fft_smem(A, B, TW, 1, TW, plan, sign, true, sm + 2 * Ny * TW);
   for (int w = threadIdx.x; w < Ny * TW; w += blockDim.x) {
     const int e = w / TW, t = w - e * TW;
     const int kz = kz0 + t;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __
                : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  double2* R = fft_smem(A, B, nl, 1, nl, plan, -1, true);
+  double2* R = fft_smem(A, B, nl, 1, nl, plan, -1, true, sm + 2 * Nx * nl);
   double2* S = (R == A) ? B : A;
   // Bhat_ij = sum_l Ahat_il ghat_lj, ghat = xi (x) xi / |xi|^2 (projection.cpp:87-104,139-152)
   const int yg = g.y0 + y;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __
     }  // Nyquist in IdentityEquilibrium mode: ghat = I, keep v
   }
   __syncthreads();
-  R = fft_smem(R, S, nl, 1, nl, plan, +1, true);
+  R = fft_smem(R, S, nl, 1, nl, plan, +1, true, sm + 2 * Nx * nl);
   for (int w = threadIdx.x; w < Nx * nl; w += blockDim.x) {
     const int t = w % TW, j = (w / TW) % TD, e = w / nl;
     const int kz = kz0 + t;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double
     B[(c * G + gi) * ls + k] = Z;
   }
   __syncthreads();
-  double2* R = fft_smem(B, A, NC * G, ls, 1, plan, +1, false);
+  double2* R = fft_smem(B, A, NC * G, ls, 1, plan, +1, false, sm + 2 * NC * G * ls);
   double dot = 0.0;
   for (int w = threadIdx.x; w < NC * Gb * g.Nz; w += blockDim.x) {
     const int line = w / g.Nz, z = w - line * g.Nz;
@@ -249,10 +249,10 @@ void allow_smem(K kernel) {
 
 int tile_width(int nzh, int N, int lines_per_col, int& TW, int64_t other_blocks) {
   TW = std::min(8, nzh);
-  while (TW > 1 && size_t(2) * N * TW * lines_per_col * 16 > size_t(kMaxSmem)) TW /= 2;
+  while (TW > 1 && size_t(2 * TW * lines_per_col + 1) * N * 16 > size_t(kMaxSmem)) TW /= 2;
   // small grids: prefer more CTAs (>= 2 per SM) over wider tiles
   while (TW > 2 && int64_t((nzh + TW - 1) / TW) * other_blocks < 2 * 148) TW /= 2;
-  return size_t(2) * N * TW * lines_per_col * 16 <= size_t(kMaxSmem) ? 0 : -1;
+  return size_t(2 * TW * lines_per_col + 1) * N * 16 <= size_t(kMaxSmem) ? 0 : -1;
 }
 
 // Launch shape of the generic z passes for a (slab) geometry.
@@ -275,7 +275,7 @@ ZLaunch z_launch(const fm_ctx* ctx, const Geo& g) {
   if (nxy <= 148 * 16) G = 1;
   L.G = std::min(G, nxy);
   L.threads = (L.G * NC * ctx->Nz >= 2048 || L.G * ctx->Nz >= 256) ? 256 : 128;
-  L.smem = size_t(2) * NC * L.G * L.ls * 16;
+  L.smem = size_t(2) * NC * L.G * L.ls * 16 + size_t((ctx->Nz % 2 == 0) ? ctx->pzh.N : ctx->pz.N) * 16;
   L.grid = dim3((nxy + L.G - 1) / L.G);
   return L;
 }
@@ -347,7 +347,7 @@ int pass_y(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out)
   if (tile_width(ctx->nzh, g.Ny, 1, TW, int64_t(g.Nx) * ctx->ncomp))
     return set_error(ctx, FM_E_UNSUPPORTED, "y line too long for the shared-memory FFT");
   const dim3 grid((ctx->nzh + TW - 1) / TW, g.Nx, ctx->ncomp);
-  k_ypass<<<grid, 256, size_t(2) * g.Ny * TW * 16, ctx->stream>>>(g, ctx->py, in, out, TW, sign);
+  k_ypass<<<grid, 256, size_t(2 * TW + 1) * g.Ny * 16, ctx->stream>>>(g, ctx->py, in, out, TW, sign);
   FM_LAUNCHED(ctx);
   return FM_OK;
 }
@@ -360,7 +360,7 @@ int pass_x(fm_ctx* ctx, const Geo& g, double2* T) {
   if (tile_width(ctx->nzh, g.Nx, TD, TW, int64_t(g.Ny) * TD))
     return set_error(ctx, FM_E_UNSUPPORTED, "x line too long for the shared-memory FFT");
   const dim3 grid((ctx->nzh + TW - 1) / TW, g.Ny, TD);
-  k_xpass<TD><<<grid, 256, size_t(2) * g.Nx * TD * TW * 16, ctx->stream>>>(g, ctx->px, T, TW);
+  k_xpass<TD><<<grid, 256, size_t(2 * TD * TW + 1) * g.Nx * 16, ctx->stream>>>(g, ctx->px, T, TW);
   FM_LAUNCHED(ctx);
   return FM_OK;
 }

@@ -8,7 +8,7 @@ pts = (31, 31, 31)
 lam, mu, ty, h = M.bind_parameters(M.corner_cube(pts, 9), [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
                                                           M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)])
 with abi.Context(pts, 3) as ctx:
-    m = abi.Model(ctx, "simo", lam, mu, ty, h)
+    m = abi.Model(ctx, "simo", lam, mu, ty, h, compact=os.environ.get("CFG1_COMPACT") == "1")
     F = ctx.field(9, abi.identity_field(pts, 3))
     t = time.perf_counter()
     reps = abi.run_program(m, F, M.simple_shear_program(0.1, 20, 3)[:incs])

@@ -1,4 +1,4 @@
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/kt_cfg1.csv python scripts/cfg1_short.py 3 > /dev/null 2>&1
+FM_CG_GRAPH=0 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/kt_cfg1.csv python scripts/cfg1_short.py 1 > /dev/null 2>&1
 python3 - <<'PY'
 import csv, collections
 rows = [r for r in csv.reader(open("gpurun_out/kt_cfg1.csv")) if len(r) > 10]
