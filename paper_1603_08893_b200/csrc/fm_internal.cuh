@@ -192,6 +192,13 @@ bool cg_fused_supported(const fm_ctx* ctx);
 // True when pass 1 of operator `kind` runs the pipelined kernel that can also
 // carry the CG x update (ProArgs::x).
 bool cg_xupd_supported(const fm_ctx* ctx, int kind);
+// Persistent cooperative CG for latency-bound generic grids (projection.cu).
+bool cg_small_supported(const fm_ctx* ctx);
+// Runs the CG iterations with x = 0, r = p = b already set; leaves S_IT,
+// S_RR, S_RRNEW, S_FLAG and S_OUT (1 curvature exit, 2 converged, 3 cap) in
+// d_scal.  FM_E_UNSUPPORTED: not applicable, nothing launched.
+int cg_small_run(fm_ctx* ctx, const ProArgs& op, double* x, double* r, double* p, int64_t cap, double thr,
+                 double rr0);
 // dist.cu: the slab all-to-all (dir +1: packed B -> x-pass A, -1: back)
 int transpose(fm_ctx* ctx, int dir);
 // Ordered cross-rank sum of `count` device scalars (no-op unless distributed).

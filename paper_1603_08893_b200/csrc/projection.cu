@@ -1,3 +1,4 @@
+#include <cstdio>
 #include <cstdlib>
 // Compatibility projection G and the projected tangent G(K : dF^T) on sm_100a.
 //
@@ -20,28 +21,34 @@
 // This file holds the generic kernels (any line length, tdim 2 or 3) and the
 // pass dispatcher; projection_fast.cu the register-resident ones.
 #include <algorithm>
+#include <cmath>
+
+#include <cooperative_groups.h>
 
 #include "proj_common.cuh"
 
 namespace fm {
 
 // ------------------------------------------------------------------ pass 1
-template <int TD, int PRO, bool DIR>
-__global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double2* __restrict__ twN,
-                                              ProArgs pa, double2* __restrict__ spec, int G, int ls) {
-  extern __shared__ double2 sm[];
+// Work item `bx` (G z-lines) of pass 1.  PAP: per-item partial of <dF, dP>
+// (fused CG curvature) into pa.pap_partial[bx].
+template <int TD, int PRO, bool DIR, bool PAP = false>
+__device__ __forceinline__ void zfwd_body(const Geo& g, const AxisPlan& plan, const double2* __restrict__ twN,
+                                          const ProArgs& pa, double2* __restrict__ spec, int G, int ls, int bx,
+                                          double2* sm) {
   constexpr int NC = TD * TD;
   const int nxy = g.Nx * g.Ny;
-  const int L0 = blockIdx.x * G;
+  const int L0 = bx * G;
   const int Gb = min(G, nxy - L0);
   double2* A = sm;
   double2* B = sm + NC * G * ls;
   const bool even = (g.Nz % 2 == 0);
+  double pap = 0.0;
   for (int w = threadIdx.x; w < Gb * g.Nz; w += blockDim.x) {
     const int gi = w / g.Nz, z = w - gi * g.Nz;
     const int64_t node = g.roff + int64_t(L0 + gi) * g.Nz + z;
     double v[NC];
-    prologue_voxel<TD, PRO, DIR>(pa, g.n, node, v);
+    prologue_voxel<TD, PRO, DIR, PAP>(pa, g.n, node, v, &pap);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       double2* line = A + (c * G + gi) * ls;
@@ -72,15 +79,26 @@ __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double
     }
     spec[(int64_t(c) * nxy + L0 + gi) * g.nzh + k] = X;
   }
+  if constexpr (PAP) {
+    pap = block_sum_any(pap);
+    if (threadIdx.x == 0) pa.pap_partial[bx] = pap;
+  }
+  __syncthreads();  // smem reusable by the next work item
+}
+
+template <int TD, int PRO, bool DIR>
+__global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double2* __restrict__ twN,
+                                              ProArgs pa, double2* __restrict__ spec, int G, int ls) {
+  extern __shared__ double2 sm[];
+  zfwd_body<TD, PRO, DIR>(g, plan, twN, pa, spec, G, ls, blockIdx.x, sm);
 }
 
 // -------------------------------------------------------------- pass 2 / 4
 // sign -1: std in -> packed out (forward); +1: packed in -> std out.
-__global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, const double2* in,
-                                               double2* out, int TW, int sign) {  // in == out when P = 1
-  extern __shared__ double2 sm[];
-  const int kz0 = blockIdx.x * TW;
-  const int x = blockIdx.y, c = blockIdx.z, NC = gridDim.z;
+__device__ __forceinline__ void ypass_body(const Geo& g, const AxisPlan& plan, const double2* in, double2* out,
+                                           int TW, int sign, int bx, int by, int bz, int NC, double2* sm) {
+  const int kz0 = bx * TW;
+  const int x = by, c = bz;
   const int Ny = g.Ny;
   double2* A = sm;
   double2* B = sm + Ny * TW;
@@ -99,15 +117,21 @@ __global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, const doubl
     const int kz = kz0 + t;
     if (kz < g.nzh) out[sign < 0 ? spec_packed(g, NC, c, x, e, kz) : spec_std(g, c, x, e, kz)] = R[w];
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, const double2* in,
+                                               double2* out, int TW, int sign) {  // in == out when P = 1
+  extern __shared__ double2 sm[];
+  ypass_body(g, plan, in, out, TW, sign, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, sm);
 }
 
 // ------------------------------------------------------------------ pass 3
 template <int TD>
-__global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __restrict__ spec,
-                                               int TW) {
-  extern __shared__ double2 sm[];
-  const int kz0 = blockIdx.x * TW;
-  const int y = blockIdx.y, i = blockIdx.z;
+__device__ __forceinline__ void xpass_body(const Geo& g, const AxisPlan& plan, double2* __restrict__ spec, int TW,
+                                           int bx, int by, int bz, double2* sm) {
+  const int kz0 = bx * TW;
+  const int y = by, i = bz;
   const int Nx = g.Nx;
   const int nl = TD * TW;
   double2* A = sm;
@@ -165,18 +189,27 @@ __global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __
     if (kz < g.nzh)
       spec[(int64_t(i * TD + j) * Nx + e) * xstride + int64_t(y) * g.nzh + kz] = R[w];
   }
+  __syncthreads();
+}
+
+template <int TD>
+__global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __restrict__ spec,
+                                               int TW) {
+  extern __shared__ double2 sm[];
+  xpass_body<TD>(g, plan, spec, TW, blockIdx.x, blockIdx.y, blockIdx.z, sm);
 }
 
 // ------------------------------------------------------------------ pass 5
+// Work item `bx` (G z-lines) of pass 5.  Epilogue: store out (and the <pdot,
+// out> partial), or -- fused CG, epi.r set -- r -= alpha Ap (x += alpha p when
+// epi.x) with the partial of <r, r>; partials go to epi.partial[bx].
 template <int TD>
-__global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double2* __restrict__ twN,
-                                              const double2* __restrict__ spec,
-                                              double* __restrict__ out, int G, int ls,
-                                              double scale, EpiArgs epi) {
-  extern __shared__ double2 sm[];
+__device__ __forceinline__ void zinv_body(const Geo& g, const AxisPlan& plan, const double2* __restrict__ twN,
+                                          const double2* __restrict__ spec, double* __restrict__ out, int G,
+                                          int ls, double scale, const EpiArgs& epi, int bx, double2* sm) {
   constexpr int NC = TD * TD;
   const int nxy = g.Nx * g.Ny;
-  const int L0 = blockIdx.x * G;
+  const int L0 = bx * G;
   const int Gb = min(G, nxy - L0);
   double2* A = sm;
   double2* B = sm + NC * G * ls;
@@ -224,12 +257,159 @@ __global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double
       v = Zl[z].x;
     }
     const int64_t idx = int64_t(c) * g.n + g.roff + int64_t(L0 + gi) * g.Nz + z;
+    if (epi.r) {  // fused CG update, solver.cpp:46-48 with k_cg_update's rounding
+      if (epi.scal[S_FLAG] == 0.0) {
+        const double alpha = epi.scal[S_ALPHA];
+        const double rv = __dadd_rn(epi.r[idx], __dmul_rn(-alpha, v * scale));
+        epi.r[idx] = rv;
+        if (epi.x) epi.x[idx] = __dadd_rn(epi.x[idx], __dmul_rn(alpha, epi.p[idx]));
+        dot += rv * rv;
+      }
+      continue;
+    }
     out[idx] = v * scale;
     if (epi.partial) dot += __ldg(epi.pdot + idx) * (v * scale);
   }
   if (epi.partial) {
     dot = block_sum_any(dot);
-    if (threadIdx.x == 0) epi.partial[blockIdx.x] = dot;
+    if (threadIdx.x == 0) epi.partial[bx] = dot;
+  }
+  __syncthreads();
+}
+
+template <int TD>
+__global__ void __launch_bounds__(256) k_zinv(Geo g, AxisPlan plan, const double2* __restrict__ twN,
+                                              const double2* __restrict__ spec,
+                                              double* __restrict__ out, int G, int ls,
+                                              double scale, EpiArgs epi) {
+  extern __shared__ double2 sm[];
+  zinv_body<TD>(g, plan, twN, spec, out, G, ls, scale, epi, blockIdx.x, sm);
+}
+
+// ------------------------------------------------- persistent small-grid CG
+// The whole CG loop (solver.cpp:19-58) of a latency-bound grid as ONE
+// cooperative launch: the five passes are phases over work items separated
+// by grid-wide barriers, the curvature / residual reductions are summed by
+// every block in the same fixed order (so every block takes the same branch),
+// and the iteration loop runs on the device.  Fused iteration as on the
+// register-resident path: <p, K:p> from pass 1, r -= alpha Ap and
+// x += alpha p in pass 5, Ap never stored.
+struct CgSmallArgs {
+  Geo gz, gx;
+  AxisPlan pz, py, px;
+  const double2* twN;
+  ProArgs op;
+  double2* spec;
+  double *x, *r, *p;
+  double* pap_part;
+  double* rr_part;
+  double* scal;
+  int G, ls, tw_y, tw_x, nz_items, ny_items, nx_items, ny_gx, nx_gx;
+  double rr0, thr, scale;
+  int64_t cap;
+  unsigned long long* tdbg;  // optional: block-0 phase timestamps of the first 8 iterations (FM_CG_SMALL_TIMING)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// sum of n per-item partials, identical in every block (fixed thread -> index map)
+__device__ __forceinline__ double items_sum(const double* part, int n, double* bcast) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = block_sum_any(s);
+  if (threadIdx.x == 0) *bcast = s;
+  __syncthreads();
+  s = *bcast;
+  __syncthreads();
+  return s;
+}
+
+template <int PRO>
+__global__ void __launch_bounds__(256) k_cg_small(CgSmallArgs a) {
+  namespace cgp = cooperative_groups;
+  extern __shared__ double2 sm[];
+  __shared__ double ssc[16];
+  cgp::grid_group grid = cgp::this_grid();
+  double rr = a.rr0, rr_new = 0.0, pap = 0.0, beta = 0.0;
+  int64_t it = 0;
+  int exit_kind = 3;  // 1: !(pAp > 0), 2: converged, 3: cap
+  auto mark = [&](int k) {
+    if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0 && it <= 8) a.tdbg[(it - 1) * 8 + k] = gtimer();
+  };
+  while (it < a.cap) {
+    ++it;
+    mark(0);
+    if (threadIdx.x == 0) ssc[S_BETA] = beta;  // 0 in the first iteration: p = r = b
+    __syncthreads();
+    ProArgs pa = a.op;
+    pa.A = a.p;
+    pa.r = a.r;
+    pa.p = a.p;
+    pa.beta = &ssc[S_BETA];
+    pa.pap_partial = a.pap_part;
+    for (int w = blockIdx.x; w < a.nz_items; w += gridDim.x)
+      zfwd_body<3, PRO, true, true>(a.gz, a.pz, a.twN, pa, a.spec, a.G, a.ls, w, sm);
+    mark(1);
+    grid.sync();
+    mark(2);
+    pap = items_sum(a.pap_part, a.nz_items, &ssc[8]);
+    if (!(pap > 0.0)) {  // :38-44, x not updated
+      exit_kind = 1;
+      break;
+    }
+    if (threadIdx.x == 0) {
+      ssc[S_ALPHA] = rr / pap;
+      ssc[S_FLAG] = 0.0;
+    }
+    __syncthreads();
+    for (int w = blockIdx.x; w < a.ny_items; w += gridDim.x) {
+      const int bx = w % a.ny_gx, rest = w / a.ny_gx;
+      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, -1, bx, rest % a.gz.Nx, rest / a.gz.Nx, 9, sm);
+    }
+    grid.sync();
+    mark(3);
+    for (int w = blockIdx.x; w < a.nx_items; w += gridDim.x) {
+      const int bx = w % a.nx_gx, rest = w / a.nx_gx;
+      xpass_body<3>(a.gx, a.px, a.spec, a.tw_x, bx, rest % a.gx.Ny, rest / a.gx.Ny, sm);
+    }
+    grid.sync();
+    mark(4);
+    for (int w = blockIdx.x; w < a.ny_items; w += gridDim.x) {
+      const int bx = w % a.ny_gx, rest = w / a.ny_gx;
+      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, +1, bx, rest % a.gz.Nx, rest / a.gz.Nx, 9, sm);
+    }
+    grid.sync();
+    mark(5);
+    EpiArgs e;
+    e.r = a.r;
+    e.x = a.x;
+    e.p = a.p;
+    e.scal = ssc;
+    e.partial = a.rr_part;
+    for (int w = blockIdx.x; w < a.nz_items; w += gridDim.x)
+      zinv_body<3>(a.gz, a.pz, a.twN, a.spec, nullptr, a.G, a.ls, a.scale, e, w, sm);
+    mark(6);
+    grid.sync();
+    rr_new = items_sum(a.rr_part, a.nz_items, &ssc[8]);
+    mark(7);
+    if (sqrt(rr_new) <= a.thr) {  // :49-50
+      exit_kind = 2;
+      break;
+    }
+    beta = rr_new / rr;  // :51-55
+    rr = rr_new;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.scal[S_IT] = double(it);
+    a.scal[S_RR] = rr;
+    a.scal[S_RRNEW] = rr_new;
+    a.scal[S_PAP] = pap;
+    a.scal[S_FLAG] = exit_kind == 1 ? 1.0 : 0.0;
+    a.scal[S_OUT] = double(exit_kind);
   }
 }
 
@@ -434,6 +614,128 @@ int profile_collect(fm_ctx* ctx) {
   for (cudaEvent_t e : pr.pending) pr.pool.push_back(e);
   pr.pending.clear();
   return FM_OK;
+}
+
+bool cg_small_supported(const fm_ctx* ctx) {
+  static const int env = [] {
+    const char* e = getenv("FM_CG_SMALL");
+    return e ? atoi(e) : 1;
+  }();
+  if (!env || ctx->tdim != 3 || ctx->P != 1 || ctx->virt || ctx->n_global > (int64_t(1) << 20)) return false;
+  if (cg_fused_supported(ctx)) return false;  // power-of-two grids run the register-resident passes
+  int dev = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  return coop != 0;
+}
+
+template <int PRO>
+static int cg_small_blocks(size_t smem);
+
+template <int PRO>
+static int cg_small_go(fm_ctx* ctx, CgSmallArgs& a, size_t smem, int items_max) {
+  const int co = cg_small_blocks<PRO>(smem);  // co-residency bound of the cooperative launch
+  if (co < 1) return FM_E_UNSUPPORTED;
+  const int grid = std::max(1, std::min(co, items_max));
+  void* args[] = {&a};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_cg_small<PRO>), dim3(grid), dim3(256),
+                                                    args, smem, ctx->stream);
+  ctx->cnt.launches++;
+  return e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_cg_small");
+}
+
+template <int PRO>
+static int cg_small_blocks(size_t smem) {
+  static bool attr = (cudaFuncSetAttribute(k_cg_small<PRO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                      cudaGetLastError(), true);
+  (void)attr;
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_small<PRO>, 256, smem);
+  cudaGetLastError();
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms;
+}
+
+int cg_small_run(fm_ctx* ctx, const ProArgs& op, double* x, double* r, double* p, int64_t cap, double thr,
+                 double rr0) {
+  init_generic<3>();
+  const Geo gz = geo_zy(ctx, 0), gx = geo_x(ctx, 0);
+  // every phase in ONE round of work items: the co-resident block count
+  // (estimated at 64 KB of shared memory) sets the z-line group and the
+  // y / x tile widths
+  const int blocks0 = op.kind == PRO_K4 ? cg_small_blocks<PRO_K4>(64 * 1024)
+                      : op.kind == PRO_J2C ? cg_small_blocks<PRO_J2C>(64 * 1024)
+                                           : cg_small_blocks<PRO_SVK>(64 * 1024);
+  if (blocks0 < 1) return FM_E_UNSUPPORTED;
+  const int nxy = gz.Nx * gz.Ny;
+  ZLaunch L = z_launch(ctx, gz);
+  L.G = std::max(1, (nxy + blocks0 - 1) / blocks0);
+  L.smem = size_t(2) * 9 * L.G * L.ls * 16 + size_t((ctx->Nz % 2 == 0) ? ctx->pzh.N : ctx->pz.N) * 16;
+  L.grid = dim3((nxy + L.G - 1) / L.G);
+  int twy = 1, twx = 1;
+  while (twy < ctx->nzh && int64_t((ctx->nzh + twy - 1) / twy) * gz.Nx * 9 > blocks0) twy *= 2;
+  while (twx < ctx->nzh && int64_t((ctx->nzh + twx - 1) / twx) * gx.Ny * 3 > blocks0) twx *= 2;
+  CgSmallArgs a;
+  a.gz = gz;
+  a.gx = gx;
+  a.pz = (ctx->Nz % 2 == 0) ? ctx->pzh : ctx->pz;
+  a.py = ctx->py;
+  a.px = ctx->px;
+  a.twN = ctx->pz.tw;
+  a.op = op;
+  a.spec = spec_a(ctx, 0);
+  a.x = x;
+  a.r = r;
+  a.p = p;
+  a.pap_part = ctx->d_epi2;
+  a.rr_part = ctx->d_epi;
+  a.scal = ctx->d_scal;
+  a.G = L.G;
+  a.ls = L.ls;
+  a.tw_y = twy;
+  a.tw_x = twx;
+  a.nz_items = int(L.grid.x);
+  a.ny_gx = (ctx->nzh + twy - 1) / twy;
+  a.ny_items = a.ny_gx * gz.Nx * ctx->ncomp;
+  a.nx_gx = (ctx->nzh + twx - 1) / twx;
+  a.nx_items = a.nx_gx * gx.Ny * 3;
+  a.rr0 = rr0;
+  a.thr = thr;
+  a.scale = 1.0 / double(ctx->n_global);
+  a.cap = cap;
+  a.tdbg = nullptr;
+  static const bool timing = getenv("FM_CG_SMALL_TIMING") != nullptr;
+  static unsigned long long* tdbg = nullptr;
+  if (timing) {
+    if (!tdbg) cudaMalloc(&tdbg, 64 * sizeof(unsigned long long));
+    cudaMemsetAsync(tdbg, 0, 64 * sizeof(unsigned long long), ctx->stream);
+    a.tdbg = tdbg;
+  }
+  const size_t smem = std::max({L.smem, size_t(2 * twy + 1) * gz.Ny * 16, size_t(2 * 3 * twx + 1) * gx.Nx * 16});
+  const int items = std::max({a.nz_items, a.ny_items, a.nx_items});
+  if (smem > size_t(64 * 1024) || a.nz_items > ctx->epi_cap) return FM_E_UNSUPPORTED;
+  int st = FM_E_UNSUPPORTED;
+  switch (op.kind) {
+    case PRO_K4: st = cg_small_go<PRO_K4>(ctx, a, smem, items); break;
+    case PRO_J2C: st = cg_small_go<PRO_J2C>(ctx, a, smem, items); break;
+    case PRO_SVK: st = cg_small_go<PRO_SVK>(ctx, a, smem, items); break;
+    default: break;
+  }
+  if (timing && st == FM_OK) {
+    unsigned long long h[64];
+    cudaMemcpyAsync(h, tdbg, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    fprintf(stderr, "cg_small G=%d twy=%d twx=%d items z/y/x=%d/%d/%d:", a.G, a.tw_y, a.tw_x, a.nz_items, a.ny_items,
+            a.nx_items);
+    for (int i = 1; i < 4; ++i) {
+      fprintf(stderr, " [it%d", i + 1);
+      for (int k = 1; k < 8; ++k) fprintf(stderr, " %.1f", (h[i * 8 + k] - h[i * 8 + k - 1]) * 1e-3);
+      fprintf(stderr, "]");
+    }
+    fprintf(stderr, "\n");
+  }
+  return st;
 }
 
 int projection_run(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiArgs& epi,

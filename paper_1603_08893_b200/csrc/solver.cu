@@ -275,6 +275,35 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
     FM_CUDA(ctx, cudaMemcpyAsync(ctx->r.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
   FM_CUDA(ctx, cudaMemcpyAsync(ctx->p.d, b, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
   double rr = ctx->h_scal[S_RR];
+  if (cg_small_supported(ctx)) {  // latency-bound generic grid: the whole loop in one cooperative launch
+    ProArgs pa;
+    pa.kind = op.kind;
+    pa.K = op.K;
+    pa.F = op.F;
+    pa.lam = op.lam;
+    pa.mu = op.mu;
+    const int st = cg_small_run(ctx, pa, x, ctx->r.d, ctx->p.d, cap, eta_cg * bnorm, rr);
+    if (st != FM_E_UNSUPPORTED) {
+      if (st) return st;
+      if (int s2 = fetch_scalars(ctx, S_OUT + 1)) return s2;
+      const double* hs = ctx->h_scal;
+      const int how = int(hs[S_OUT]);
+      *iters = int32_t(hs[S_IT]);
+      if (how == 1) {  // !(pAp > 0): x not updated in that iteration (:38-44)
+        *rel = std::sqrt(hs[S_RR]) / bnorm;
+        return FM_OK;
+      }
+      if (how == 2) {  // :49-50
+        *rel = std::sqrt(hs[S_RRNEW]) / bnorm;
+        return FM_OK;
+      }
+      *rel = std::sqrt(hs[S_RR]) / bnorm;
+      const int se = set_error(ctx, FM_E_CG_STALLED,
+                               "conjugate gradient stalled after " + std::to_string(cap) + " iterations");
+      ctx->last_info = fm_error_info{FM_E_CG_STALLED, int32_t(cap), -1, *rel};
+      return se;
+    }
+  }
   if (cg_graph_enabled(ctx)) return cg_loop_graph(ctx, op, x, count, cap, eta_cg * bnorm, bnorm, iters, rel);
   for (int64_t it = 1; it <= cap; ++it) {
     // :36-37 with :51-55 of the previous iteration folded in (p = beta p + r)
