@@ -101,8 +101,41 @@ def simo16():
     print("simo16", [r["cg_it"] for r in reps], [[r["cg_it"] for r in run[2]] for run in runs[1:]])
 
 
+def _simo32_run(args):
+    which, eps = args
+    pts = (32, 32, 32)
+    pg = M.corner_cube(pts, 8)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    if which == "lam":
+        lam = lam * (1.0 + eps)
+    elif which == "mu":
+        mu = mu * (1.0 + eps)
+    return O.run_program(pts, 3, 1, lam, mu, M.simple_shear_program(0.01, 2, 3), ty0=ty, hard=h)
+
+
+def simo32():
+    """32^3 J2 case (power-of-two grid: the register-resident passes, fused CG,
+    compact tangent) of tests/test_gpu_solver.py, with its CG-count envelope."""
+    from multiprocessing import Pool
+    with Pool(7) as pool:
+        runs = pool.map(_simo32_run, [("none", 0.0)] + PERTURB)
+    F, P, reps, st, epsp = runs[0]
+    assert st == 0
+    pad = lambda r: r["cg_it"] + [0] * (64 - len(r["cg_it"]))
+    np.savez_compressed(os.path.join(HERE, "simo32.npz"), F=F, P=P, epsp=epsp,
+                        passes=np.array([r["passes"] for r in reps]),
+                        cg_it=np.array([pad(r) for r in reps]),
+                        band_passes=np.array([[r["passes"] for r in run[2]] for run in runs[1:]]),
+                        band_cg_it=np.array([[pad(r) for r in run[2]] for run in runs[1:]]))
+    print("simo32", [r["cg_it"] for r in reps], [[r["cg_it"] for r in run[2]] for run in runs[1:]])
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["0", "1"]
+    if "simo32" in which:
+        simo32()
     if "simo16" in which:
         simo16()
     if "band+" in which:
@@ -117,21 +150,24 @@ if __name__ == "__main__":
 
 def config3_reduced():
     """Config 3's generator on a reduced grid (64^3, radius 2, seed 3, 10
-    increments to gamma 0.05) -- the parity case for the 512^3 J2 run."""
+    increments to gamma 0.05), first two increments.  The oracle (like the
+    GPU) converges increment 1 and stops with InvertedElement in increment 2
+    (DESIGN.md §7b); the run records are kept as the parity fixture."""
+    import json
     N, r = 64, 2
     pg, frac, count = M.random_spheres(N, r, 0.25, 3)
     phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
               M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
     lam, mu, ty, h = M.bind_parameters(pg, phases)
     t = time.time()
-    F, P, reps, st, epsp = O.run_program((N, N, N), 3, 1, lam, mu, M.simple_shear_program(0.05, 10, 3),
-                                         ty0=ty, hard=h)
-    assert st == 0, st
-    pad = lambda rr: rr["cg_it"] + [0] * (64 - len(rr["cg_it"]))
-    np.savez_compressed(os.path.join(HERE, "config3_64.npz"), F=F, P=P, epsp=epsp,
-                        passes=np.array([rr["passes"] for rr in reps]), cg_it=np.array([pad(rr) for rr in reps]),
-                        fraction=frac, spheres=count)
-    print("config3_64", time.time() - t, frac, count, [rr["cg_it"] for rr in reps])
+    _, _, reps, st, _ = O.run_program((N, N, N), 3, 1, lam, mu, M.simple_shear_program(0.05, 10, 3)[:2],
+                                      ty0=ty, hard=h)
+    rec = {"grid": N, "radius": r, "fraction": frac, "spheres": count, "status": st,
+           "increments": [{"passes": rr["passes"], "status": rr["status"], "cg_it": rr["cg_it"],
+                           "err_node": rr["err_node"], "converged": rr["converged"]} for rr in reps if rr["passes"]]}
+    with open(os.path.join(HERE, "config3_64.json"), "w") as f:
+        json.dump(rec, f, indent=1)
+    print("config3_64", time.time() - t, rec)
 
 
 if __name__ == "__main__" and "config3" in sys.argv[1:]:

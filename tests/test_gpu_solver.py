@@ -160,6 +160,25 @@ def test_cube_simo16_matches_golden(compact):
     assert np.max(np.abs(ep - g["epsp"])) < 1e-9 * np.max(g["epsp"])
 
 
+@pytest.mark.parametrize("compact", [False, True])
+def test_cube_simo32_matches_golden(compact):
+    """32^3 J2 (8^3 corner inclusion, gamma 0.01 in 2 increments): the power-
+    of-two path -- register-resident passes and the fused CG iteration -- with
+    the K4 and the compact eigenbasis tangent, against the oracle and its
+    1e-15-perturbation envelope (tests/golden/make_golden.py simo32)."""
+    g = np.load(os.path.join(GOLD, "simo32.npz"))
+    pts = (32, 32, 32)
+    pg = M.corner_cube(pts, 8)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    F, P, reps, ep = gpu_run(pts, 3, "simo", lam, mu, M.simple_shear_program(0.01, 2, 3), ty, h, compact=compact)
+    band = [_as_reps(bp, bc) for bp, bc in zip(g["band_passes"], g["band_cg_it"])]
+    assert_counts(reps, _as_reps(g["passes"], g["cg_it"]), band)
+    assert rel(F, g["F"]) < 1e-9 and rel(P, g["P"]) < 1e-9
+    assert np.max(np.abs(ep - g["epsp"])) < 1e-9 * np.max(g["epsp"])
+
+
 def test_config0_matches_golden():
     """BASELINE config 0: 31^3 SVK, 9^3 corner inclusion, gamma 0.1."""
     g = np.load(os.path.join(GOLD, "config0.npz"))
