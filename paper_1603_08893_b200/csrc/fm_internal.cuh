@@ -105,7 +105,8 @@ struct fm_ctx {
   int red_blocks = 0;
   double* d_partial = nullptr;  // red_blocks * 16
   double* d_epi = nullptr;      // per-block partials of the fused <p,Ap>
-  double* d_epi2 = nullptr;     // pass-1 partials of the fused-CG <p, K:p> (epi_cap)
+  double* d_epi2 = nullptr;     // pass-1 partials of the fused-CG <p, K:p> (epi2_cap)
+  int64_t epi2_cap = 0;
   double* d_fold = nullptr;     // first-level sums of a two-level finalisation (epi_cap / 1024 + 64)
   int zf_partials = 0;          // partials the last pass 1 wrote
   int64_t epi_cap = 0;

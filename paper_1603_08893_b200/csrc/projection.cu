@@ -568,10 +568,20 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   const int r1 = ctx->virt ? ctx->P : ctx->rank + 1;
   const double sc = scale / double(ctx->n_global);
   prof_mark(ctx);
-  for (int r = r0; r < r1; ++r)
-    if (int st = pass_zf<TD>(ctx, geo_zy(ctx, r), pa, spec_a(ctx, r))) return st;
-  if (pa.pap_partial)  // fused CG: alpha from <p, K:p> before the remaining passes
-    if (int st = cg_pap_finalize_from(ctx, pa.pap_partial, ctx->zf_partials)) return st;
+  int pap_total = 0;
+  for (int r = r0; r < r1; ++r) {
+    ProArgs par = pa;
+    if (par.pap_partial) {  // virtual ranks: partials side by side
+      const Geo gr = geo_zy(ctx, r);
+      const int64_t most = std::max<int64_t>(int64_t(gr.Nx) * gr.Ny, 148 * 32);  // line groups / resident CTAs
+      if (pap_total + most > ctx->epi2_cap) return set_error(ctx, FM_E_UNSUPPORTED, "fused CG: too many pass-1 partials");
+      par.pap_partial += pap_total;
+    }
+    if (int st = pass_zf<TD>(ctx, geo_zy(ctx, r), par, spec_a(ctx, r))) return st;
+    if (par.pap_partial) pap_total += ctx->zf_partials;
+  }
+  if (pa.pap_partial)  // fused CG: alpha from <p, K:p> (summed over ranks) before the remaining passes
+    if (int st = cg_pap_finalize_from(ctx, pa.pap_partial, pap_total)) return st;
   prof_mark(ctx);
   for (int r = r0; r < r1; ++r)
     if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), -1, spec_a(ctx, r), spec_b(ctx, r))) return st;

@@ -894,7 +894,10 @@ bool cg_xupd_supported(const fm_ctx* ctx, int kind) {
 bool cg_fused_supported(const fm_ctx* ctx) {
   const int M = ctx->Nz / 2;
   const bool pow2 = M >= 16 && M <= 512 && (M & (M - 1)) == 0;
-  return fast_z_ok(ctx) && pow2 && ctx->P == 1 && !ctx->virt;
+  // slab ranks: each rank's pass-1 partials are summed across ranks in rank
+  // order (combine_ranks) before alpha is formed
+  const int64_t lines = int64_t(ctx->Nx / ctx->P) * ctx->Ny * ctx->P;
+  return fast_z_ok(ctx) && pow2 && lines <= ctx->epi_cap;
 }
 
 int zi_fast_blocks(const fm_ctx* ctx, const Geo& g) {
