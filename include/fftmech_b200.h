@@ -104,25 +104,33 @@ int64_t fm_ctx_launch_count(const fm_ctx* ctx);
 
 /* ---- slab decomposition ---------------------------------
  * Rank r of P owns x-planes [r Nx/P, (r+1) Nx/P) of every field; the
- * projection runs its z/y passes on the x-slab and its x pass on the y-slab,
- * with two all-to-alls (grouped ncclSend/ncclRecv over NVLink) in between.
- * Nx and Ny must be divisible by P; CG scalars are combined across ranks in
- * rank order (deterministic). */
+ * projection runs its z/y passes on the x-slab and its x pass on the y-slab.
+ * The two slab transposes are fused into the passes that produce the data:
+ * the forward y pass and the x pass store every element straight into the
+ * buffer of the rank that owns it next (peer memory over NVLink / NVSwitch,
+ * mapped with CUDA IPC at context creation), with one cross-rank barrier
+ * after each.  Nx and Ny must be divisible by P (P <= 16); CG scalars are
+ * combined across ranks in rank order (deterministic). */
 /* One rank per device.  `points` is the GLOBAL grid; fields created on this
  * context hold the local slab (Nx/P * Ny * Nz nodes per component).
- * nccl_unique_id: the 128-byte id from fm_nccl_unique_id on rank 0. */
+ * nccl_unique_id: the 128-byte id from fm_nccl_unique_id on rank 0 (NCCL
+ * carries the IPC handle exchange, the barriers and the CG scalars). */
 int fm_ctx_create_dist(int dim, const int32_t* points, const double* lengths, int tdim, int nyquist_mode,
                        int device, int nranks, int rank, const void* nccl_unique_id, fm_ctx** out);
 int fm_nccl_unique_id(void* out, int bytes);
-/* Virtual ranks: run all P slab ranks on this one device (the all-to-all is
- * a device copy) -- validates the decomposition against P = 1 bit for bit. */
+/* Virtual ranks: run all P slab ranks on this one device (their buffers side
+ * by side, the same transpose-fused kernels storing across them) -- validates
+ * the decomposition against P = 1 bit for bit. */
 int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P);
 int fm_ctx_ranks(const fm_ctx* ctx, int* nranks, int* rank, int* virtual_mode);
-/* Transpose plan (host only, no device needed): complex-element offsets of
- * the (src -> dst, component) chunk in src's packed buffer B and in dst's
- * x-pass buffer A, and its length. */
-int fm_dist_chunk(int P, int Nx, int Ny, int nzh, int ncomp, int src, int dst, int comp, int64_t* b_off,
-                  int64_t* a_off, int64_t* count);
+/* Route of the fused transpose (host only, no device needed), the same
+ * function the kernels evaluate.  dir +1 (forward y pass of x-slab `src`):
+ * element (comp, xl = i0, y = i1, kz) -> rank *dst_rank, complex-element
+ * index *dst_index in its x-pass input [c][x][yl][kz].  dir -1 (x pass of
+ * y-slab `src`): element (comp, x = i0, yl = i1, kz) -> rank *dst_rank, index
+ * in its spectrum [c][xl][y][kz]. */
+int fm_dist_route(int P, int Nx, int Ny, int nzh, int ncomp, int dir, int src, int comp, int i0, int i1, int kz,
+                  int32_t* dst_rank, int64_t* dst_index);
 
 /* ---- fields -------------------------------------------------------------- */
 int fm_field_alloc(fm_ctx* ctx, int ncomp, fm_field** out);

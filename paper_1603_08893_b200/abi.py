@@ -116,8 +116,7 @@ _SIGS = {
     "fm_model_set_tangent_form": (C.c_int, [_P, _P, C.c_int]),
     "fm_ctx_set_virtual_ranks": (C.c_int, [_P, C.c_int]),
     "fm_ctx_ranks": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
-    "fm_dist_chunk": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                                C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "fm_dist_route": (C.c_int, [C.c_int] * 11 + [C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
 }
 
 
@@ -130,13 +129,16 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def dist_chunk(P, Nx, Ny, nzh, ncomp, src, dst, comp):
-    """Transpose plan of the slab decomposition (host only): (b_off, a_off, count)."""
-    b, a, n = C.c_int64(), C.c_int64(), C.c_int64()
-    st = lib().fm_dist_chunk(P, Nx, Ny, nzh, ncomp, src, dst, comp, C.byref(b), C.byref(a), C.byref(n))
+def dist_route(P, Nx, Ny, nzh, ncomp, direction, src, comp, i0, i1, kz):
+    """Route of the fused slab transpose (host only), the function the kernels
+    evaluate: (destination rank, complex-element index in its buffer).
+    direction +1: forward y pass of x-slab `src`, element (comp, xl=i0, y=i1, kz);
+    direction -1: x pass of y-slab `src`, element (comp, x=i0, yl=i1, kz)."""
+    d, o = C.c_int32(), C.c_int64()
+    st = lib().fm_dist_route(P, Nx, Ny, nzh, ncomp, direction, src, comp, i0, i1, kz, C.byref(d), C.byref(o))
     if st != FM_OK:
-        raise FmError(st, "fm_dist_chunk")
-    return b.value, a.value, n.value
+        raise FmError(st, "fm_dist_route")
+    return d.value, o.value
 
 
 def declared_symbols():

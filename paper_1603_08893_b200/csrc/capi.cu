@@ -204,6 +204,7 @@ int fm_ctx_destroy(fm_ctx* ctx) {
 static int setup_slabs(fm_ctx* ctx, int P) {
   if (P < 1 || ctx->Nx % P || ctx->Ny % P)
     return set_error(ctx, FM_E_UNSUPPORTED, "slab decomposition needs Nx and Ny divisible by the rank count");
+  if (P > kMaxRanks) return set_error(ctx, FM_E_UNSUPPORTED, "more slab ranks than kMaxRanks (16)");
   ctx->P = P;
   ctx->spec_rank_elems = int64_t(ctx->ncomp) * (ctx->Nx / P) * ctx->Ny * ctx->nzh;
   if (P > 1 && !ctx->spec2) {
@@ -211,7 +212,7 @@ static int setup_slabs(fm_ctx* ctx, int P) {
     FM_CUDA(ctx, cudaMalloc(&ctx->spec2, bytes));
   }
   if (!ctx->d_gather) FM_CUDA(ctx, cudaMalloc(&ctx->d_gather, sizeof(double) * 64 * size_t(P)));
-  return FM_OK;
+  return dist_setup_routes(ctx);
 }
 
 int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P) {

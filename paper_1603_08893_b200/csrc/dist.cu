@@ -1,19 +1,30 @@
 // Slab decomposition of the projection over P ranks.
 //
 // Rank r owns x-planes [r Xl, (r+1) Xl) of every real field (Xl = Nx/P).
-// Passes 1-2 run on that x-slab; pass 2 writes its spectrum pre-packed per
-// destination, B_r = [dst][c][xl][yl][kz] (Yl = Ny/P), so the block bound for
-// rank d and component c is one contiguous run of Xl*Yl*nzh complex values.
-// The all-to-all delivers it to A_d = [c][x][yl][kz] (global x), where the
-// block from source s is again contiguous (x in [s Xl, (s+1) Xl)) -- no pack
-// or unpack kernels on either side.  Pass 3 runs on the y-slab, the reverse
-// all-to-all returns the blocks, pass 4 reads the packed layout.
+// Passes 1-2 run on that x-slab, pass 3 on the y-slab [r Yl, (r+1) Yl)
+// (Yl = Ny/P), passes 4-5 on the x-slab again.  The two slab transposes are
+// not separate all-to-all steps: they are fused into the epilogues of the
+// passes that produce the data (route_yf / route_xb, proj_common.cuh):
 //
-//   virtual mode : all P ranks live on one device; the all-to-all is one
-//                  device copy kernel (validates the decomposition exactly
-//                  against P = 1 on a single B200).
-//   NCCL mode    : one rank per device; grouped ncclSend/ncclRecv per
-//                  (peer, component) chunk over NVLink / NVSwitch.
+//   pass 2 (forward y FFT) stores every element straight into the x-pass
+//          input B_d of the rank d that owns its y, at its global x;
+//   pass 3 (x FFT, ghat, inverse x FFT) stores every element straight into
+//          the spectrum A_s of the rank s that owns its x, at its global y;
+//          pass 4 then runs in place on A_s.
+//
+// On devices the stores go over NVLink / NVSwitch into peer memory mapped
+// with CUDA IPC, so the exchange overlaps the FFT arithmetic line by line
+// instead of following it; one cross-rank barrier after pass 2 and one after
+// pass 3 order the passes (rank_barrier).  In the virtual mode all P ranks'
+// buffers live side by side on one device and the same kernels store into
+// them -- the decomposition is validated exactly against P = 1 on one B200.
+//
+// Buffer hazards (why two barriers suffice): B_d is written by every rank's
+// pass 2 and read only by d's pass 3, which runs after barrier 1; the next
+// application's pass 2 writes B_d again only after barrier 2, i.e. after d's
+// pass 3.  A_s is read by s's pass 2 (before barrier 1) and written by the
+// pass 3 of every rank (after barrier 1); s's passes 4-5 and the next pass 1
+// run after barrier 2.
 #include <nccl.h>
 
 #include <cstring>
@@ -24,73 +35,76 @@
 
 namespace fm {
 
-// Offsets (complex elements) of the chunk (src -> dst, component c):
-// b_off inside B of rank src, a_off inside A of rank dst.
-struct Chunk {
-  int64_t b_off, a_off, count;
-};
-
-inline Chunk chunk_of(int P, int Nx, int Ny, int nzh, int NC, int src, int dst, int c) {
-  const int64_t Xl = Nx / P, Yl = Ny / P;
-  const int64_t cnt = Xl * Yl * nzh;
-  return Chunk{(int64_t(dst) * NC + c) * cnt, (int64_t(c) * Nx + int64_t(src) * Xl) * Yl * nzh, cnt};
-}
-
-// grid: (blocks over a chunk, NC, P*P); dir +1: B -> A, -1: A -> B
-__global__ void k_transpose_virtual(double2* __restrict__ A, double2* __restrict__ B, int P, int NC,
-                                    int Nx, int Ny, int nzh, int64_t rank_elems, int dir) {
-  const int s = blockIdx.z / P, r = blockIdx.z - s * P, c = blockIdx.y;
-  const int64_t Xl = Nx / P, Yl = Ny / P;
-  const int64_t cnt = Xl * Yl * nzh;
-  double2* b = B + int64_t(s) * rank_elems + (int64_t(r) * NC + c) * cnt;
-  double2* a = A + int64_t(r) * rank_elems + (int64_t(c) * Nx + int64_t(s) * Xl) * Yl * nzh;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < cnt; i += int64_t(gridDim.x) * blockDim.x) {
-    if (dir > 0)
-      a[i] = b[i];
-    else
-      b[i] = a[i];
-  }
-}
-
 static int nccl_check(fm_ctx* ctx, ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return FM_OK;
   return set_error(ctx, FM_E_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
 }
 
-int transpose(fm_ctx* ctx, int dir) {
-  const int P = ctx->P, NC = ctx->ncomp;
-  if (ctx->virt) {
-    const int64_t cnt = int64_t(ctx->Nx / P) * (ctx->Ny / P) * ctx->nzh;
-    const int bx = int(std::min<int64_t>(1024, (cnt + 255) / 256));
-    k_transpose_virtual<<<dim3(bx, NC, P * P), 256, 0, ctx->stream>>>(ctx->spec, ctx->spec2, P, NC, ctx->Nx,
-                                                                       ctx->Ny, ctx->nzh, ctx->spec_rank_elems, dir);
-    FM_LAUNCHED(ctx);
-    return FM_OK;
-  }
-  // one rank per device: grouped point-to-point over NVLink
+int rank_barrier(fm_ctx* ctx) {
+  if (!distributed(ctx)) return FM_OK;
+  // a one-element all-reduce on the library stream: it starts after this
+  // rank's transpose-fused kernel completed (its peer stores performed) and
+  // finishes only when every rank's has
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
-  const int me = ctx->rank;
-  if (int st = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart")) return st;
-  for (int peer = 0; peer < P; ++peer) {
-    for (int c = 0; c < NC; ++c) {
-      // forward: my packed block for `peer` -> peer's A; reverse: A block of `peer` -> its B
-      const Chunk out = dir > 0 ? chunk_of(P, ctx->Nx, ctx->Ny, ctx->nzh, NC, me, peer, c)
-                                : chunk_of(P, ctx->Nx, ctx->Ny, ctx->nzh, NC, peer, me, c);
-      const Chunk in = dir > 0 ? chunk_of(P, ctx->Nx, ctx->Ny, ctx->nzh, NC, peer, me, c)
-                               : chunk_of(P, ctx->Nx, ctx->Ny, ctx->nzh, NC, me, peer, c);
-      const double2* src = dir > 0 ? ctx->spec2 + out.b_off : ctx->spec + out.a_off;
-      double2* dst = dir > 0 ? ctx->spec + in.a_off : ctx->spec2 + in.b_off;
-      if (peer == me) {
-        FM_CUDA(ctx, cudaMemcpyAsync(dst, src, out.count * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+  double* flag = ctx->d_scal + 63;
+  return nccl_check(ctx, ncclAllReduce(flag, flag, 1, ncclDouble, ncclSum, comm, ctx->stream), "ncclAllReduce");
+}
+
+int dist_setup_routes(fm_ctx* ctx) {
+  const int P = ctx->P;
+  if (P > kMaxRanks) return set_error(ctx, FM_E_UNSUPPORTED, "more slab ranks than kMaxRanks");
+  if (!ctx->d_dst_a) FM_CUDA(ctx, cudaMalloc(&ctx->d_dst_a, sizeof(double2*) * kMaxRanks));
+  if (!ctx->d_dst_b) FM_CUDA(ctx, cudaMalloc(&ctx->d_dst_b, sizeof(double2*) * kMaxRanks));
+  std::vector<double2*> a(kMaxRanks, nullptr), b(kMaxRanks, nullptr);
+  if (!distributed(ctx)) {  // virtual ranks: side by side on this device
+    for (int r = 0; r < P; ++r) {
+      a[r] = ctx->spec + int64_t(r) * ctx->spec_rank_elems;
+      b[r] = ctx->spec2 ? ctx->spec2 + int64_t(r) * ctx->spec_rank_elems : nullptr;
+    }
+  } else {
+    // one rank per device: exchange IPC handles of A and B (all-gather over
+    // the communicator), map every peer's buffers into this process
+    struct Handles {
+      cudaIpcMemHandle_t a, b;
+    };
+    Handles mine;
+    FM_CUDA(ctx, cudaIpcGetMemHandle(&mine.a, ctx->spec));
+    FM_CUDA(ctx, cudaIpcGetMemHandle(&mine.b, ctx->spec2));
+    char* d_h = nullptr;
+    FM_CUDA(ctx, cudaMalloc(&d_h, sizeof(Handles) * P));
+    std::vector<Handles> all(P);
+    int st = FM_OK;
+    if (cudaMemcpy(d_h + sizeof(Handles) * ctx->rank, &mine, sizeof(Handles), cudaMemcpyHostToDevice) != cudaSuccess)
+      st = set_error(ctx, FM_E_CUDA, "IPC handle upload");
+    if (!st)
+      st = nccl_check(ctx,
+                      ncclAllGather(d_h + sizeof(Handles) * ctx->rank, d_h, sizeof(Handles), ncclChar,
+                                    static_cast<ncclComm_t>(ctx->nccl), ctx->stream),
+                      "ncclAllGather(IPC handles)");
+    if (!st && cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = set_error(ctx, FM_E_CUDA, "IPC exchange");
+    if (!st && cudaMemcpy(all.data(), d_h, sizeof(Handles) * P, cudaMemcpyDeviceToHost) != cudaSuccess)
+      st = set_error(ctx, FM_E_CUDA, "IPC handle download");
+    cudaFree(d_h);
+    if (st) return st;
+    for (int r = 0; r < P; ++r) {
+      if (r == ctx->rank) {
+        a[r] = ctx->spec;
+        b[r] = ctx->spec2;
         continue;
       }
-      if (int st = nccl_check(ctx, ncclSend(src, size_t(out.count) * 2, ncclDouble, peer, comm, ctx->stream), "ncclSend"))
-        return st;
-      if (int st = nccl_check(ctx, ncclRecv(dst, size_t(in.count) * 2, ncclDouble, peer, comm, ctx->stream), "ncclRecv"))
-        return st;
+      void* pa = nullptr;
+      void* pb = nullptr;
+      FM_CUDA(ctx, cudaIpcOpenMemHandle(&pa, all[r].a, cudaIpcMemLazyEnablePeerAccess));
+      ctx->ipc_open.push_back(pa);
+      FM_CUDA(ctx, cudaIpcOpenMemHandle(&pb, all[r].b, cudaIpcMemLazyEnablePeerAccess));
+      ctx->ipc_open.push_back(pb);
+      a[r] = static_cast<double2*>(pa);
+      b[r] = static_cast<double2*>(pb);
     }
   }
-  return nccl_check(ctx, ncclGroupEnd(), "ncclGroupEnd");
+  FM_CUDA(ctx, cudaMemcpy(ctx->d_dst_a, a.data(), sizeof(double2*) * kMaxRanks, cudaMemcpyHostToDevice));
+  FM_CUDA(ctx, cudaMemcpy(ctx->d_dst_b, b.data(), sizeof(double2*) * kMaxRanks, cudaMemcpyHostToDevice));
+  return FM_OK;
 }
 
 // Ordered sum of `count` per-rank values across the distributed ranks:
@@ -131,6 +145,11 @@ int dist_init_nccl(fm_ctx* ctx, const void* unique_id, int nranks, int rank) {
 }
 
 void dist_destroy(fm_ctx* ctx) {
+  for (void* p : ctx->ipc_open) cudaIpcCloseMemHandle(p);
+  ctx->ipc_open.clear();
+  if (ctx->d_dst_a) cudaFree(ctx->d_dst_a);
+  if (ctx->d_dst_b) cudaFree(ctx->d_dst_b);
+  ctx->d_dst_a = ctx->d_dst_b = nullptr;
   if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
   ctx->nccl = nullptr;
 }
@@ -149,15 +168,21 @@ int fm_nccl_unique_id(void* out, int bytes) {
   return FM_OK;
 }
 
-int fm_dist_chunk(int P, int Nx, int Ny, int nzh, int ncomp, int src, int dst, int comp, int64_t* b_off,
-                  int64_t* a_off, int64_t* count) {
-  if (P < 1 || Nx % P || Ny % P || src < 0 || src >= P || dst < 0 || dst >= P || comp < 0 || comp >= ncomp ||
-      !b_off || !a_off || !count)
+int fm_dist_route(int P, int Nx, int Ny, int nzh, int ncomp, int dir, int src, int comp, int i0, int i1, int kz,
+                  int32_t* dst_rank, int64_t* dst_index) {
+  if (P < 1 || P > kMaxRanks || Nx % P || Ny % P || src < 0 || src >= P || comp < 0 || comp >= ncomp || kz < 0 ||
+      kz >= nzh || !dst_rank || !dst_index || (dir != 1 && dir != -1))
     return FM_E_INVALID;
-  const Chunk ch = chunk_of(P, Nx, Ny, nzh, ncomp, src, dst, comp);
-  *b_off = ch.b_off;
-  *a_off = ch.a_off;
-  *count = ch.count;
+  const int Xl = Nx / P, Yl = Ny / P;
+  int d = 0;
+  if (dir > 0) {  // y pass of x-slab src: (comp, xl = i0, y = i1, kz)
+    if (i0 < 0 || i0 >= Xl || i1 < 0 || i1 >= Ny) return FM_E_INVALID;
+    *dst_index = route_yf(Nx, Xl, Yl, nzh, src, comp, i0, i1, kz, d);
+  } else {        // x pass of y-slab src: (comp, x = i0, yl = i1, kz)
+    if (i0 < 0 || i0 >= Nx || i1 < 0 || i1 >= Yl) return FM_E_INVALID;
+    *dst_index = route_xb(Ny, Xl, Yl, nzh, src, comp, i0, i1, kz, d);
+  }
+  *dst_rank = d;
   return FM_OK;
 }
 

@@ -19,6 +19,7 @@
 namespace fm {
 
 constexpr int kMaxStages = 24;
+constexpr int kMaxRanks = 16;  // slab ranks (devices of one node, or virtual ranks)
 
 // One axis of the 3-D transform: length N, radix plan, twiddle table
 // tw[k] = exp(-2 pi i k / N) (long-double accurate, device resident).
@@ -87,13 +88,19 @@ struct fm_ctx {
   fm::AxisPlan px, py, pz, pzh;  // pzh: half-length plan for even-Nz r2c
   double2* d_tw = nullptr;        // all twiddle tables
   double2* spec = nullptr;        // ncomp * Nx * Ny * nzh  (A: z/y side; also the x-pass buffer)
-  double2* spec2 = nullptr;       // packed all-to-all staging (B), only when P > 1
+  double2* spec2 = nullptr;       // x-pass input B (y-slab), only when P > 1
   // slab decomposition over P ranks; P = 1: single device
   int P = 1, rank = 0;
   bool virt = false;              // all P ranks emulated on this one device
   int64_t n_local_stride = 0;     // component stride of real fields (n, or n_local when distributed)
   int64_t spec_rank_elems = 0;    // complex elements of one rank's spectral buffer
   void* nccl = nullptr;           // ncclComm_t when distributed over devices
+  // destinations of the fused slab transpose (device arrays of P pointers):
+  // A (spectrum, x-slab) and B (x-pass input, y-slab) of every rank -- peer
+  // memory mapped through CUDA IPC when the ranks are devices
+  double2** d_dst_a = nullptr;
+  double2** d_dst_b = nullptr;
+  std::vector<void*> ipc_open;    // peer buffers opened with cudaIpcOpenMemHandle
   double* d_gather = nullptr;     // all-gather staging of per-rank scalars
   // CG loop as one CUDA graph (a while-conditional node around the fused
   // iteration): cached for the last (operator, vectors) it was built for
@@ -109,6 +116,7 @@ struct fm_ctx {
   int64_t epi2_cap = 0;
   double* d_fold = nullptr;     // first-level sums of a two-level finalisation (epi_cap / 1024 + 64)
   int zf_partials = 0;          // partials the last pass 1 wrote
+  int zi_partials = 0;          // partials the last fast pass 5 wrote
   int64_t epi_cap = 0;
   double* d_scal = nullptr;     // device scalars (64)
   double* h_scal = nullptr;     // pinned mirror (64)
@@ -200,8 +208,12 @@ bool cg_small_supported(const fm_ctx* ctx);
 // d_scal.  FM_E_UNSUPPORTED: not applicable, nothing launched.
 int cg_small_run(fm_ctx* ctx, const ProArgs& op, double* x, double* r, double* p, int64_t cap, double thr,
                  double rr0);
-// dist.cu: the slab all-to-all (dir +1: packed B -> x-pass A, -1: back)
-int transpose(fm_ctx* ctx, int dir);
+// dist.cu: cross-device barrier between the transpose-fused passes (the
+// peer stores of one pass complete on every rank before the next reads them);
+// no-op on one device and in the virtual mode (stream order suffices)
+int rank_barrier(fm_ctx* ctx);
+// route tables of the fused transpose: virtual ranks, or IPC-mapped peers
+int dist_setup_routes(fm_ctx* ctx);
 // Ordered cross-rank sum of `count` device scalars (no-op unless distributed).
 int combine_ranks(fm_ctx* ctx, double* d_vals, int count);
 int combine_min_u64(fm_ctx* ctx, unsigned long long* d_key);

@@ -14,19 +14,61 @@ struct Geo {
   int64_t n;     // component stride of real fields
   int64_t roff;  // node offset of this slab inside the real fields
   double invL[3];
-  int P, Yl;     // y passes: ranks and y per rank (packed transpose layout)
+  int P, Yl;     // ranks, y per rank
   int y0, Nyg;   // x pass: global y of local y = 0, global Ny (frequencies)
+  int rank, Xl, Nxg;  // slab rank of this pass, x per rank, global Nx
+  // P > 1: the slab transpose is fused into the forward y pass and the x pass,
+  // which store each element straight into the buffer of the rank that owns
+  // it next (device array of P pointers: peer memory over NVLink when the
+  // ranks are devices, the side-by-side rank buffers in the virtual mode)
+  double2* const* dst;
 };
 
-// Spectral layouts.  std: [c][x][y][kz].  packed (y-pass side of the
-// all-to-all): [dst][c][x][yl][kz], dst = y / Yl, so the block bound for
-// each destination rank is contiguous.  P = 1 makes both identical.
+// Spectral layout of every pass: std [c][x][y][kz] on the pass's own extents.
 __device__ __forceinline__ int64_t spec_std(const Geo& g, int c, int x, int y, int kz) {
   return ((int64_t(c) * g.Nx + x) * g.Ny + y) * g.nzh + kz;
 }
-__device__ __forceinline__ int64_t spec_packed(const Geo& g, int NC, int c, int x, int y, int kz) {
-  const int dst = y / g.Yl, yl = y - dst * g.Yl;
-  return (((int64_t(dst) * NC + c) * g.Nx + x) * g.Yl + yl) * g.nzh + kz;
+
+// Routes of the fused slab transpose (shared by the kernels and fm_dist_route).
+// Forward, epilogue of the y pass on the x-slab of rank s: element
+// (c, xl, y, kz) goes to rank d = y / Yl, into its x-pass input B_d =
+// [c][x = s Xl + xl][yl][kz] (all x, the y-slab of d).
+__host__ __device__ __forceinline__ int64_t route_yf(int Nxg, int Xl, int Yl, int nzh, int s, int c, int xl, int y,
+                                                     int kz, int& d) {
+  d = y / Yl;
+  const int yl = y - d * Yl;
+  return ((int64_t(c) * Nxg + int64_t(s) * Xl + xl) * Yl + yl) * nzh + kz;
+}
+// Backward, epilogue of the x pass on the y-slab of rank d: element
+// (c, x, yl, kz) goes to rank s = x / Xl, into its spectrum A_s =
+// [c][xl][y = d Yl + yl][kz] (the x-slab of s, all y), where the inverse y
+// pass continues in place.
+__host__ __device__ __forceinline__ int64_t route_xb(int Nyg, int Xl, int Yl, int nzh, int d, int c, int x, int yl,
+                                                     int kz, int& s) {
+  s = x / Xl;
+  const int xl = x - s * Xl;
+  return ((int64_t(c) * Xl + xl) * Nyg + int64_t(d) * Yl + yl) * nzh + kz;
+}
+// Store of the forward y pass: in place on one device, routed when P > 1.
+__device__ __forceinline__ void store_yf(const Geo& g, double2* out, int c, int x, int y, int kz, double2 v) {
+  if (g.P == 1) {
+    out[spec_std(g, c, x, y, kz)] = v;
+  } else {
+    int d;
+    const int64_t o = route_yf(g.Nxg, g.Nx, g.Yl, g.nzh, g.rank, c, x, y, kz, d);
+    g.dst[d][o] = v;
+  }
+}
+// Store of the x pass: in place on one device (`local` = the element's
+// address), routed to the owning x-slab when P > 1.
+__device__ __forceinline__ void store_xb(const Geo& g, double2* local, int c, int x, int y, int kz, double2 v) {
+  if (g.P == 1) {
+    *local = v;
+  } else {
+    int s;
+    const int64_t o = route_xb(g.Nyg, g.Xl, g.Ny, g.nzh, g.rank, c, x, y, kz, s);
+    g.dst[s][o] = v;
+  }
 }
 
 __device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) ? i : i - n; }
@@ -223,22 +265,30 @@ inline Geo make_geo(const fm_ctx* ctx) {
   g.Yl = ctx->Ny;
   g.y0 = 0;
   g.Nyg = ctx->Ny;
+  g.rank = 0;
+  g.Xl = ctx->Nx;
+  g.Nxg = ctx->Nx;
+  g.dst = nullptr;
   return g;
 }
-// z and y passes of slab rank r: local x-slab, all y and z.
+// z and y passes of slab rank r: local x-slab, all y and z.  The forward y
+// pass stores into the x-pass inputs B of the destination ranks.
 inline Geo geo_zy(const fm_ctx* ctx, int r) {
   Geo g = make_geo(ctx);
   g.P = ctx->P;
   g.Nx = ctx->Nx / ctx->P;
+  g.Xl = g.Nx;
   g.Yl = ctx->Ny / ctx->P;
+  g.rank = r;
   g.roff = ctx->virt ? int64_t(r) * g.Nx * ctx->Ny * ctx->Nz : 0;
   g.n = ctx->n_local_stride;
+  g.dst = ctx->d_dst_b;
   return g;
 }
-// Spectral buffers of slab rank r: A (z/y side, reused in place by the x pass,
-// [c][x][yl][kz] after the transpose) and B (packed all-to-all staging).  One
-// rank per device when distributed; all P ranks side by side in the virtual
-// mode.  P = 1: B == A (the y passes run in place).
+// Spectral buffers of slab rank r: A (z / y side, std layout on the x-slab)
+// and B (the x-pass input, std layout on the y-slab), one rank per device
+// when distributed, all P ranks side by side in the virtual mode.  P = 1:
+// B == A (every pass runs in place).
 inline double2* spec_a(fm_ctx* ctx, int r) {
   return ctx->spec + (ctx->virt ? int64_t(r) * ctx->spec_rank_elems : 0);
 }
@@ -246,11 +296,17 @@ inline double2* spec_b(fm_ctx* ctx, int r) {
   if (ctx->P == 1) return ctx->spec;
   return ctx->spec2 + (ctx->virt ? int64_t(r) * ctx->spec_rank_elems : 0);
 }
-// x pass of slab rank r: all x, local y-slab.
+// x pass of slab rank r: all x, local y-slab; stores into the spectra A of
+// the x-slab owners.
 inline Geo geo_x(const fm_ctx* ctx, int r) {
   Geo g = make_geo(ctx);
+  g.P = ctx->P;
   g.Ny = ctx->Ny / ctx->P;
+  g.Yl = g.Ny;
+  g.Xl = ctx->Nx / ctx->P;
   g.y0 = r * g.Ny;
+  g.rank = r;
+  g.dst = ctx->d_dst_a;
   return g;
 }
 
@@ -262,6 +318,5 @@ bool y_fast(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out
 bool x_fast(fm_ctx* ctx, const Geo& g, double2* spec, int* st);
 bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
              int* st);
-int zi_fast_blocks(const fm_ctx* ctx, const Geo& g);  // partial sums the fast z-inverse writes
 
 }  // namespace fm

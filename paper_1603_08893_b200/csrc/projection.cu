@@ -94,9 +94,10 @@ __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double
 }
 
 // -------------------------------------------------------------- pass 2 / 4
-// sign -1: std in -> packed out (forward); +1: packed in -> std out.
+// In place on one device; P > 1 the forward pass (sign -1) stores into the
+// x-pass inputs of the y-slab owners (store_yf, the fused slab transpose).
 __device__ __forceinline__ void ypass_body(const Geo& g, const AxisPlan& plan, const double2* in, double2* out,
-                                           int TW, int sign, int bx, int by, int bz, int NC, double2* sm) {
+                                           int TW, int sign, int bx, int by, int bz, double2* sm) {
   const int kz0 = bx * TW;
   const int x = by, c = bz;
   const int Ny = g.Ny;
@@ -106,7 +107,7 @@ __device__ __forceinline__ void ypass_body(const Geo& g, const AxisPlan& plan, c
     const int e = w / TW, t = w - e * TW;
     const int kz = kz0 + t;
     if (kz < g.nzh)
-      A[w] = in[sign < 0 ? spec_std(g, c, x, e, kz) : spec_packed(g, NC, c, x, e, kz)];
+      A[w] = in[spec_std(g, c, x, e, kz)];
     else
       A[w] = make_double2(0.0, 0.0);
   }
@@ -115,7 +116,9 @@ __device__ __forceinline__ void ypass_body(const Geo& g, const AxisPlan& plan, c
   for (int w = threadIdx.x; w < Ny * TW; w += blockDim.x) {
     const int e = w / TW, t = w - e * TW;
     const int kz = kz0 + t;
-    if (kz < g.nzh) out[sign < 0 ? spec_packed(g, NC, c, x, e, kz) : spec_std(g, c, x, e, kz)] = R[w];
+    if (kz >= g.nzh) continue;
+    if (sign < 0) store_yf(g, out, c, x, e, kz, R[w]);
+    else out[spec_std(g, c, x, e, kz)] = R[w];
   }
   __syncthreads();
 }
@@ -123,12 +126,12 @@ __device__ __forceinline__ void ypass_body(const Geo& g, const AxisPlan& plan, c
 __global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, const double2* in,
                                                double2* out, int TW, int sign) {  // in == out when P = 1
   extern __shared__ double2 sm[];
-  ypass_body(g, plan, in, out, TW, sign, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, sm);
+  ypass_body(g, plan, in, out, TW, sign, blockIdx.x, blockIdx.y, blockIdx.z, sm);
 }
 
 // ------------------------------------------------------------------ pass 3
 template <int TD>
-__device__ __forceinline__ void xpass_body(const Geo& g, const AxisPlan& plan, double2* __restrict__ spec, int TW,
+__device__ __forceinline__ void xpass_body(const Geo& g, const AxisPlan& plan, double2* spec, int TW,
                                            int bx, int by, int bz, double2* sm) {
   const int kz0 = bx * TW;
   const int y = by, i = bz;
@@ -187,13 +190,14 @@ __device__ __forceinline__ void xpass_body(const Geo& g, const AxisPlan& plan, d
     const int t = w % TW, j = (w / TW) % TD, e = w / nl;
     const int kz = kz0 + t;
     if (kz < g.nzh)
-      spec[(int64_t(i * TD + j) * Nx + e) * xstride + int64_t(y) * g.nzh + kz] = R[w];
+      store_xb(g, spec + (int64_t(i * TD + j) * Nx + e) * xstride + int64_t(y) * g.nzh + kz, i * TD + j, e, y, kz,
+               R[w]);
   }
   __syncthreads();
 }
 
 template <int TD>
-__global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* __restrict__ spec,
+__global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* spec,
                                                int TW) {
   extern __shared__ double2 sm[];
   xpass_body<TD>(g, plan, spec, TW, blockIdx.x, blockIdx.y, blockIdx.z, sm);
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(256) k_cg_small(CgSmallArgs a) {
     __syncthreads();
     for (int w = blockIdx.x; w < a.ny_items; w += gridDim.x) {
       const int bx = w % a.ny_gx, rest = w / a.ny_gx;
-      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, -1, bx, rest % a.gz.Nx, rest / a.gz.Nx, 9, sm);
+      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, -1, bx, rest % a.gz.Nx, rest / a.gz.Nx, sm);
     }
     grid.sync();
     mark(3);
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(256) k_cg_small(CgSmallArgs a) {
     mark(4);
     for (int w = blockIdx.x; w < a.ny_items; w += gridDim.x) {
       const int bx = w % a.ny_gx, rest = w / a.ny_gx;
-      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, +1, bx, rest % a.gz.Nx, rest / a.gz.Nx, 9, sm);
+      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, +1, bx, rest % a.gz.Nx, rest / a.gz.Nx, sm);
     }
     grid.sync();
     mark(5);
@@ -550,7 +554,7 @@ int pass_zi(fm_ctx* ctx, const Geo& g, const double2* A, double* out, double sca
             int* nparts) {
   int st = FM_OK;
   if (TD == 3 && zi_fast(ctx, g, A, out, scale, epi, &st)) {
-    if (nparts) *nparts = zi_fast_blocks(ctx, g);
+    if (nparts) *nparts = ctx->zi_partials;  // partial sums the fast z-inverse wrote
     return st;
   }
   const ZLaunch L = z_launch(ctx, g);
@@ -583,18 +587,18 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   if (pa.pap_partial)  // fused CG: alpha from <p, K:p> (summed over ranks) before the remaining passes
     if (int st = cg_pap_finalize_from(ctx, pa.pap_partial, pap_total)) return st;
   prof_mark(ctx);
+  // P > 1: the forward y pass stores into the ranks' x-pass inputs B, the x
+  // pass into the ranks' spectra A (the fused slab transposes, dist.cu)
   for (int r = r0; r < r1; ++r)
-    if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), -1, spec_a(ctx, r), spec_b(ctx, r))) return st;
-  prof_mark(ctx);
-  if (ctx->P > 1)
-    if (int st = transpose(ctx, +1)) return st;
-  for (int r = r0; r < r1; ++r)
-    if (int st = pass_x<TD>(ctx, geo_x(ctx, r), spec_a(ctx, r))) return st;
-  if (ctx->P > 1)
-    if (int st = transpose(ctx, -1)) return st;
+    if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), -1, spec_a(ctx, r), spec_a(ctx, r))) return st;
+  if (int st = rank_barrier(ctx)) return st;
   prof_mark(ctx);
   for (int r = r0; r < r1; ++r)
-    if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), +1, spec_b(ctx, r), spec_a(ctx, r))) return st;
+    if (int st = pass_x<TD>(ctx, geo_x(ctx, r), spec_b(ctx, r))) return st;
+  if (int st = rank_barrier(ctx)) return st;
+  prof_mark(ctx);
+  for (int r = r0; r < r1; ++r)
+    if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), +1, spec_a(ctx, r), spec_a(ctx, r))) return st;
   prof_mark(ctx);
   int total = 0;
   for (int r = r0; r < r1; ++r) {

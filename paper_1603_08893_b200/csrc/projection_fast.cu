@@ -26,32 +26,36 @@ using reg::e_line;
 using reg::e_x;
 
 // ------------------------------------------------------------------ y pass
-// SIGN -1: std layout in, packed (all-to-all) layout out; +1: the reverse.
-// With P = 1 both layouts coincide and in == out (in place).
-template <int N, int TW, int SIGN>
+// In place on one device.  P > 1: SIGN -1 stores each element into the x-pass
+// input of the rank that owns its y (the fused forward slab transpose,
+// store_yf); SIGN +1 runs in place on the spectrum of the x-slab.
+template <int N, int TW, int SIGN, bool RT = false>
 __global__ void __launch_bounds__(TW*(N / e_line(N))) k_y_fast(Geo g, const double2* __restrict__ tw,
                                                                const double2* in, double2* out) {
   constexpr int E = e_line(N), T = N / E;
   extern __shared__ double2 sm[];
   const int l = threadIdx.x % TW, t = threadIdx.x / TW;
   const int kz = blockIdx.x * TW + l;
-  const int x = blockIdx.y, c = blockIdx.z, NC = gridDim.z;
+  const int x = blockIdx.y, c = blockIdx.z;
   double2 v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const int y = t + T * m;
-    v[m] = in[SIGN < 0 ? spec_std(g, c, x, y, kz) : spec_packed(g, NC, c, x, y, kz)];
-  }
+  for (int m = 0; m < E; ++m) v[m] = in[spec_std(g, c, x, t + T * m, kz)];
   reg::fft<N, E, SIGN>(v, sm + l, TW, t, tw);
+  if constexpr (!RT) {
 #pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const int y = t + T * m;
-    out[SIGN < 0 ? spec_packed(g, NC, c, x, y, kz) : spec_std(g, c, x, y, kz)] = v[m];
+    for (int m = 0; m < E; ++m) out[spec_std(g, c, x, t + T * m, kz)] = v[m];
+  } else {
+#pragma unroll
+    for (int m = 0; m < E; ++m) store_yf(g, out, c, x, t + T * m, kz, v[m]);
   }
 }
 
 // ------------------------------------------------------------------ x pass
-template <int N, int TW, int TD>
+// All x passes: in place on one device; P > 1 they read the y-slab input B
+// (disjoint from every destination, so __restrict__ holds in both cases)
+// and store each element into the spectrum of the rank that owns its x (the
+// fused backward slab transpose, store_xb).
+template <int N, int TW, int TD, bool RT = false>
 __global__ void __launch_bounds__(TW*(N / e_x(N)), 2) k_x_fast(Geo g, const double2* __restrict__ tw,
                                                             double2* __restrict__ spec) {
   constexpr int E = e_x(N), T = N / E;
@@ -101,10 +105,17 @@ __global__ void __launch_bounds__(TW*(N / e_x(N)), 2) k_x_fast(Geo g, const doub
   }
 #pragma unroll
   for (int j = 0; j < TD; ++j) reg::fft<N, E, +1>(v[j], sm + l, TW, t, tw);
+  if constexpr (!RT) {
 #pragma unroll
-  for (int j = 0; j < TD; ++j)
+    for (int j = 0; j < TD; ++j)
 #pragma unroll
-    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[j][m];
+      for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[j][m];
+  } else {
+#pragma unroll
+    for (int j = 0; j < TD; ++j)
+#pragma unroll
+      for (int m = 0; m < E; ++m) store_xb(g, nullptr, i * TD + j, t + T * m, y, kz, v[j][m]);
+  }
 }
 
 // x pass, prefetching variant: the whole tile (3 components x N x TW) is
@@ -121,7 +132,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-template <int N, int TW, int E>
+template <int N, int TW, int E, bool RT = false>
 __global__ void __launch_bounds__(TW*(N / E)) k_x_fast3(Geo g, const double2* __restrict__ tw,
                                                        double2* __restrict__ spec) {
   constexpr int T = N / E;
@@ -184,8 +195,13 @@ __global__ void __launch_bounds__(TW*(N / E)) k_x_fast3(Geo g, const double2* __
     for (int m = 0; m < E; ++m) v[m] = S[(t + T * m) * TW];
     __syncthreads();
     reg::fft<N, E, +1>(v, S, TW, t, tw);
+    if constexpr (!RT) {
 #pragma unroll
-    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
+      for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
+    } else {
+#pragma unroll
+      for (int m = 0; m < E; ++m) store_xb(g, nullptr, i * 3 + j, t + T * m, y, kz, v[m]);
+    }
   }
 }
 
@@ -197,7 +213,7 @@ __global__ void __launch_bounds__(TW*(N / E)) k_x_fast3(Geo g, const double2* __
 // (component q+2 streams in while q is transformed) and each buffer doubles
 // as the transform's exchange scratch; the inverse transforms store straight
 // from registers.  64 KB per CTA at N = 256, TW = 8.
-template <int N, int TW, int E>
+template <int N, int TW, int E, bool RT = false>
 __global__ void __launch_bounds__(TW*(N / E), E >= 16 ? 3 : 2) k_x_fast4(Geo g, const double2* __restrict__ tw,
                                                        double2* __restrict__ spec) {
   constexpr int T = N / E;
@@ -262,8 +278,13 @@ __global__ void __launch_bounds__(TW*(N / E), E >= 16 ? 3 : 2) k_x_fast4(Geo g, 
       v[m] = make_double2(s[m].x * f, s[m].y * f);
     }
     reg::fft<N, E, +1>(v, B + l, TW, t, tw);
+    if constexpr (!RT) {
 #pragma unroll
-    for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
+      for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
+    } else {
+#pragma unroll
+      for (int m = 0; m < E; ++m) store_xb(g, nullptr, i * 3 + j, t + T * m, y, kz, v[m]);
+    }
   }
 }
 
@@ -653,7 +674,11 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
   constexpr int T = N / e_line(N);
   const size_t smem = size_t(N) * TW * 16;
   const dim3 grid(ctx->nzh / TW, g.Nx, ctx->ncomp);
-  if (sign < 0) {
+  if (sign < 0 && g.P > 1) {  // forward pass with the fused slab transpose
+    static bool a = (allow(k_y_fast<N, TW, -1, true>, smem), true);
+    (void)a;
+    k_y_fast<N, TW, -1, true><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
+  } else if (sign < 0) {
     static bool a = (allow(k_y_fast<N, TW, -1>, smem), true);
     (void)a;
     k_y_fast<N, TW, -1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
@@ -666,24 +691,33 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
   return true;
 }
 
-template <int N, int TW, int E>
-void x3_go(fm_ctx* ctx, const Geo& g, double2* spec) {
+// RT: the slab-transpose-fused instantiation (P > 1); P = 1 runs the plain one
+template <int N, int TW, int E, bool RT>
+void x3_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   constexpr int T = N / E;
   const size_t smem = size_t(3) * N * TW * 16;
-  static bool a = (allow(k_x_fast3<N, TW, E>, smem), true);
+  static bool a = (allow(k_x_fast3<N, TW, E, RT>, smem), true);
   (void)a;
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
-  k_x_fast3<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+  k_x_fast3<N, TW, E, RT><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+}
+template <int N, int TW, int E>
+void x3_go(fm_ctx* ctx, const Geo& g, double2* spec) {
+  g.P > 1 ? x3_rt<N, TW, E, true>(ctx, g, spec) : x3_rt<N, TW, E, false>(ctx, g, spec);
 }
 
-template <int N, int TW, int E>
-void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
+template <int N, int TW, int E, bool RT>
+void x4_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   constexpr int T = N / E;
   const size_t smem = size_t(2) * N * TW * 16;
-  static bool a = (allow(k_x_fast4<N, TW, E>, smem), true);
+  static bool a = (allow(k_x_fast4<N, TW, E, RT>, smem), true);
   (void)a;
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
-  k_x_fast4<N, TW, E><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+  k_x_fast4<N, TW, E, RT><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+}
+template <int N, int TW, int E>
+void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
+  g.P > 1 ? x4_rt<N, TW, E, true>(ctx, g, spec) : x4_rt<N, TW, E, false>(ctx, g, spec);
 }
 
 template <int N>
@@ -702,10 +736,16 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   } else if (N <= 512 && ctx->nzh % 8 == 0 && !(zc && N < 64)) {
     x3_go<N, 8, e_line(N)>(ctx, g, spec);
   } else {
-    static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
-    (void)a;
     const dim3 grid(ctx->nzh / TW, g.Ny, 3);
-    k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+    if (g.P > 1) {
+      static bool a = (allow(k_x_fast<N, TW, 3, true>, smem), true);
+      (void)a;
+      k_x_fast<N, TW, 3, true><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+    } else {
+      static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
+      (void)a;
+      k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+    }
   }
   *st = launched(ctx, "k_x_fast");
   return true;
@@ -828,6 +868,7 @@ template <int M>
 bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
                int* st) {
   zi_go<M, ZiShape<M>>(ctx, g, spec, out, scale, epi);
+  ctx->zi_partials = (g.Nx * g.Ny + ZiShape<M>::G - 1) / ZiShape<M>::G;
   *st = launched(ctx, "k_zi_fast");
   return true;
 }
@@ -898,22 +939,6 @@ bool cg_fused_supported(const fm_ctx* ctx) {
   // order (combine_ranks) before alpha is formed
   const int64_t lines = int64_t(ctx->Nx / ctx->P) * ctx->Ny * ctx->P;
   return fast_z_ok(ctx) && pow2 && lines <= ctx->epi_cap;
-}
-
-int zi_fast_blocks(const fm_ctx* ctx, const Geo& g) {
-  const int nxy = g.Nx * g.Ny;
-  const int M = ctx->Nz / 2;
-  int G = 0;
-  switch (M) {
-    case 16: G = ZiShape<16>::G; break;
-    case 32: G = ZiShape<32>::G; break;
-    case 64: G = ZiShape<64>::G; break;
-    case 128: G = ZiShape<128>::G; break;
-    case 256: G = ZiShape<256>::G; break;
-    case 512: G = ZiShape<512>::G; break;
-    default: return 0;
-  }
-  return (nxy + G - 1) / G;
 }
 
 }  // namespace fm

@@ -1,5 +1,6 @@
 """Slab decomposition validated on one B200: P slab ranks
-emulated on the device ("virtual ranks", the all-to-all is a device copy)
+emulated on the device ("virtual ranks": the transpose-fused y and x passes
+store across the side-by-side rank buffers)
 must reproduce the P = 1 projection bit for bit -- the z / y / x passes
 compute the same lines in the same order, only the layouts between them
 change -- and the Newton solve must match the single-rank run."""
