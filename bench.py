@@ -219,7 +219,7 @@ def main():
     n_global = N ** 3
     lam_g, mu_g = config2_inputs(N)
     # N > 1: slab decomposition of the one config-2 grid over the GPUs (strong
-    # scaling, NCCL all-to-all inside every matvec); --replicas: independent copies.
+    # scaling, transpose-fused peer stores inside every matvec); --replicas: independent copies.
     slab = world > 1 and not args.replicas
     note = None
     ctx = None
@@ -410,7 +410,7 @@ def main():
             "config": {"workload": f"config2: {N}^3 SVK Bernoulli(0.3) seed 2, contrast 10, "
                                    "G:K4:dF matvec (K4 at F_bar)",
                        "grid": [N, N, N],
-                       "parallelism": (f"slab x{world} (x-slabs, NCCL all-to-all per matvec)" if slab
+                       "parallelism": (f"slab x{world} (x-slabs, transposes fused into the y/x passes as NVLink peer stores)" if slab
                                        else f"replicas x{world}") + (f"; {note}" if note else ""),
                        "operator": "matrix-free SVK",
                        "l2": "inputs 12 GB > 126 MB L2, no flush"},
