@@ -351,6 +351,14 @@ class Field:
         self.ctx.check(lib().fm_field_download(self.ctx.h, self.h, out, out.size))
         return out
 
+    @property
+    def __cuda_array_interface__(self):
+        """Zero-copy view of the device slabs ([ncomp * n] fp64) for callers that
+        fill or check huge fields on the device (e.g. torch.as_tensor(field,
+        device="cuda")); the library's stream must be synchronised around it."""
+        return {"shape": (self.size,), "typestr": "<f8", "data": (int(self.ptr), False), "version": 3,
+                "strides": None}
+
     def free(self):
         if self.h:
             lib().fm_field_free(self.ctx.h, self.h)

@@ -153,13 +153,14 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
   ctx->red_blocks = int(rb < 1 ? 1 : (rb > 148 * 4 ? 148 * 4 : rb));
   if (cudaMalloc(&ctx->d_partial, sizeof(double) * (ctx->red_blocks + 16) * 16) != cudaSuccess)
     return fail(FM_E_OOM);
-  ctx->epi_cap = int64_t(ctx->Nx) * ctx->Ny + 64;
+  // pass-5 partials: one per z-line group (9 components x Nx Ny lines at most)
+  ctx->epi_cap = int64_t(9) * ctx->Nx * ctx->Ny + 64;
   if (cudaMalloc(&ctx->d_epi, sizeof(double) * ctx->epi_cap) != cudaSuccess) return fail(FM_E_OOM);
   // pass-1 partials: one per z-line group, or one per resident CTA of the
   // persistent pass 1 (<= 148 SMs x 32) for each of up to 16 virtual ranks
   ctx->epi2_cap = ctx->epi_cap + int64_t(148) * 32 * 16;
   if (cudaMalloc(&ctx->d_epi2, sizeof(double) * ctx->epi2_cap) != cudaSuccess) return fail(FM_E_OOM);
-  if (cudaMalloc(&ctx->d_fold, sizeof(double) * (ctx->epi_cap / 1024 + 64)) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMalloc(&ctx->d_fold, sizeof(double) * (ctx->epi2_cap / 1024 + 64)) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMalloc(&ctx->d_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMemset(ctx->d_scal, 0, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_CUDA);
   if (cudaMallocHost(&ctx->h_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);

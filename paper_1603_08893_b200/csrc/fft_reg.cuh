@@ -88,9 +88,21 @@ __device__ __forceinline__ double2 tw_mul(double2 x, double2 w, int sign) {
                   : make_double2(x.x * w.x + x.y * w.y, x.y * w.x - x.x * w.y);
 }
 
+// Exchange-buffer address of element p.  SW = 0: lines interleaved,
+// sm[p*LS + l] (the lanes of a warp are lines).  SW = log2(E) > 0: one line
+// per contiguous region with an XOR swizzle p ^ ((p >> SW) & 7), for lanes
+// that are the T threads of a line: every group of 8 lanes that a 16-byte
+// access serves in one phase then hits 8 distinct bank groups, both for the
+// strided Stockham writes (p = E j + k) and the unit-stride reads.
+template <int SW>
+__device__ __forceinline__ int xaddr(int p, int LS) {
+  if constexpr (SW == 0) return p * LS;
+  else return p ^ ((p >> SW) & 7);
+}
+
 // One Stockham stage of radix R (Ns = product of earlier radices).
 // tw: table W_N^e, e < N (global or shared).  sml = sm + line offset.
-template <int N, int E, int R, int Ns, int SIGN>
+template <int N, int E, int R, int Ns, int SIGN, int SW = 0>
 __device__ __forceinline__ void stage(double2 (&v)[E], double2* sml, int LS, int t,
                                       const double2* __restrict__ tw) {
   constexpr int T = N / E;
@@ -116,28 +128,29 @@ __device__ __forceinline__ void stage(double2 (&v)[E], double2* sml, int LS, int
     } else {
       const int base = (j / Ns) * Ns * R + jm;
 #pragma unroll
-      for (int k = 0; k < R; ++k) sml[(base + k * Ns) * LS] = a[k];
+      for (int k = 0; k < R; ++k) sml[xaddr<SW>(base + k * Ns, LS)] = a[k];
     }
   }
   if constexpr (!last) {
-    __syncthreads();
+    // SW > 0: a line's T threads are lanes of one warp and own its region
+    if constexpr (SW > 0) __syncwarp(); else __syncthreads();
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = sml[(t + T * m) * LS];
-    __syncthreads();
+    for (int m = 0; m < E; ++m) v[m] = sml[xaddr<SW>(t + T * m, LS)];
+    if constexpr (SW > 0) __syncwarp(); else __syncthreads();
   }
 }
 
-template <int N, int E, int Ns, int SIGN>
+template <int N, int E, int Ns, int SIGN, int SW>
 struct Stages {
   static constexpr int R = (N / Ns >= E) ? E : N / Ns;
   __device__ __forceinline__ static void run(double2 (&v)[E], double2* sml, int LS, int t,
                                              const double2* __restrict__ tw) {
-    stage<N, E, R, Ns, SIGN>(v, sml, LS, t, tw);
-    Stages<N, E, Ns * R, SIGN>::run(v, sml, LS, t, tw);
+    stage<N, E, R, Ns, SIGN, SW>(v, sml, LS, t, tw);
+    Stages<N, E, Ns * R, SIGN, SW>::run(v, sml, LS, t, tw);
   }
 };
-template <int N, int E, int SIGN>
-struct Stages<N, E, N, SIGN> {
+template <int N, int E, int SIGN, int SW>
+struct Stages<N, E, N, SIGN, SW> {
   __device__ __forceinline__ static void run(double2 (&)[E], double2*, int, int, const double2*) {}
 };
 
@@ -146,7 +159,19 @@ template <int N, int E, int SIGN>
 __device__ __forceinline__ void fft(double2 (&v)[E], double2* sml, int LS, int t,
                                     const double2* __restrict__ tw) {
   static_assert(N % E == 0, "E must divide N");
-  Stages<N, E, 1, SIGN>::run(v, sml, LS, t, tw);
+  Stages<N, E, 1, SIGN, 0>::run(v, sml, LS, t, tw);
+}
+
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
+
+// Same transform for lanes that are the T threads of one line (T | 32, so a
+// line never straddles a warp and warp-level syncs suffice), exchanging
+// through the line's own swizzled region of N elements (sml = sm + line * N).
+// Every lane of the warp must call it.
+template <int N, int E, int SIGN>
+__device__ __forceinline__ void fft_swz(double2 (&v)[E], double2* sml, int t, const double2* __restrict__ tw) {
+  static_assert(N % E == 0 && E >= 8, "E must divide N; the swizzle needs E >= 8");
+  Stages<N, E, 1, SIGN, ilog2(E)>::run(v, sml, 1, t, tw);
 }
 
 // Elements per thread used by each pass for a line length N.

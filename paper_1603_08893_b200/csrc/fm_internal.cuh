@@ -114,7 +114,7 @@ struct fm_ctx {
   double* d_epi = nullptr;      // per-block partials of the fused <p,Ap>
   double* d_epi2 = nullptr;     // pass-1 partials of the fused-CG <p, K:p> (epi2_cap)
   int64_t epi2_cap = 0;
-  double* d_fold = nullptr;     // first-level sums of a two-level finalisation (epi_cap / 1024 + 64)
+  double* d_fold = nullptr;     // first-level sums of a two-level finalisation (epi2_cap / 1024 + 64)
   int zf_partials = 0;          // partials the last pass 1 wrote
   int zi_partials = 0;          // partials the last fast pass 5 wrote
   int64_t epi_cap = 0;

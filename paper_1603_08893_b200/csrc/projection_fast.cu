@@ -288,6 +288,22 @@ __global__ void __launch_bounds__(TW*(N / E), E >= 16 ? 3 : 2) k_x_fast4(Geo g, 
   }
 }
 
+// r2c / c2r untangling pairs element k of a z-line with M - k.  With the
+// line's elements spread as k = t + T m over its T lanes (T | 32), the partner
+// of (t, m) sits in lane (T - t) mod T of the same warp:
+// Value the mirror partner of this lane wants in round m (see above): lane t
+// of a line hands out element (M - k') of its receiver's k' = (T - t) + T m.
+template <int E>
+__device__ __forceinline__ double2 mirror_give(const double2 (&v)[E], int t, int m) {
+  return t == 0 ? v[(E - m) & (E - 1)] : v[E - 1 - m];
+}
+template <int T>
+__device__ __forceinline__ double2 mirror_take(double2 give, int t) {
+  const int lane = threadIdx.x & 31;
+  const int src = lane - t + ((T - t) & (T - 1));
+  return make_double2(__shfl_sync(0xffffffffu, give.x, src), __shfl_sync(0xffffffffu, give.y, src));
+}
+
 // --------------------------------------------------------------- z passes
 // HEAVY: K4 / SVK prologue (720 B read per voxel): larger E, ~144 threads and
 // ~40 KB per CTA so 4 CTAs per SM overlap their load and FFT phases.
@@ -397,7 +413,7 @@ constexpr int kPipeCopyMinB = FM_PIPE_COPY_MINB;
 template <int M>
 struct ZPipe {
   static constexpr int E = reg::e_z(M), T = M / E;
-  static constexpr int LSP = 9;  // one line per CTA, 9 components (odd pitch)
+  static constexpr int LSP = 9;  // one line per CTA: 9 component lines (line-major, swizzled)
   static constexpr int THREADS = 9 * T;
   static constexpr size_t FFT_SM = size_t(M) * LSP * 16;
 };
@@ -415,10 +431,12 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
                                                                const double2* __restrict__ twN, ProArgs pa,
                                                                double2* __restrict__ spec) {
   using S = ZPipe<M>;
-  constexpr int N = 2 * M, LSP = S::LSP, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR, XUPD>();
+  constexpr int N = 2 * M, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR, XUPD>();
+  constexpr int SW = reg::ilog2(E);  // line-major swizzled line buffer (reg::fft_swz)
+  static_assert(32 % T == 0, "a component line must not straddle a warp");
   static_assert(!XUPD || (DIR && PRO == PRO_SVK), "x update rides on the SVK direction prologue");
   extern __shared__ __align__(16) double2 sm[];
-  double* stage = reinterpret_cast<double*>(sm + M * LSP);  // NCH chunks of N doubles
+  double* stage = reinterpret_cast<double*>(sm + M * S::LSP);  // NCH chunks of N doubles
   __shared__ uint64_t bar;
   const int nxy = g.Nx * g.Ny;
   const int64_t n = g.n;
@@ -514,29 +532,31 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
         }
       }
 #pragma unroll
-      for (int c = 0; c < 9; ++c) sm[m * LSP + c] = make_double2(v0[c], v1[c]);
+      for (int c = 0; c < 9; ++c) sm[c * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
     }
     __syncthreads();  // staging consumed, packed line in sm
     if (threadIdx.x == 0 && L + int(gridDim.x) < nxy) issue(L + gridDim.x);
     {
-      const int l = threadIdx.x % 9, t = threadIdx.x / 9;
+      // component c's line in the T lanes of one warp: swizzled exchange with
+      // warp syncs, untangling by shuffle, spectrum stored from registers
+      const int c = threadIdx.x / T, t = threadIdx.x % T;
+      double2* line = sm + c * M;
       double2 v[E];
 #pragma unroll
-      for (int m = 0; m < E; ++m) v[m] = sm[(t + T * m) * LSP + l];
-      __syncthreads();
-      reg::fft<M, E, -1>(v, sm + l, LSP, t, twM);
+      for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
+      __syncwarp();
+      reg::fft_swz<M, E, -1>(v, line, t, twM);
+      double2* dst = spec + (int64_t(c) * nxy + L) * M;
 #pragma unroll
-      for (int m = 0; m < E; ++m) sm[(t + T * m) * LSP + l] = v[m];
-    }
-    __syncthreads();
-    for (int w = threadIdx.x; w < 9 * M; w += blockDim.x) {
-      const int c = w / M, k = w - c * M;
-      const double2 a = sm[k * LSP + c];
-      const double2 b = cconj(sm[((M - k) & (M - 1)) * LSP + c]);
-      const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
-      const double2 D = csub(a, b);
-      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
-      spec[(int64_t(c) * nxy + L) * M + k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+      for (int m = 0; m < E; ++m) {
+        const int k = t + T * m;
+        const double2 a = v[m];
+        const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
+        const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+        const double2 D = csub(a, b);
+        const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+        dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+      }
     }
     __syncthreads();  // sm free for the next line's prologue
   }
@@ -647,6 +667,133 @@ __global__ void __launch_bounds__(S::THREADS, 2048 / S::THREADS >= S::MINB ? S::
   if (epi.partial) {  // fused <p, Ap> partial (solver.cpp:37)
     dot = block_sum_any(dot);
     if (threadIdx.x == 0) epi.partial[blockIdx.x] = dot;
+  }
+}
+
+// ----------------------------------------------- z passes, lines in registers
+// One component z-line per T = M/E lanes (T | 32), LPC lines per CTA.  The
+// line goes from HBM straight into registers and back (16-byte accesses, T
+// lanes per contiguous run), the r2c / c2r untangling pairs k with M - k by
+// warp shuffle (the partner element sits in lane (T - t) mod T), and the FFT
+// exchanges through the line's own swizzled shared-memory region with
+// warp-level syncs only -- two shared-memory accesses per element and
+// exchange instead of the staged passes' six to eight.  Components are
+// independent here, so this is the shape of the z-inverse (every operator)
+// and of the z-forward of G (no per-voxel prologue coupling the components).
+
+template <int M, int E, int LPC, int MINB>
+__global__ void __launch_bounds__(LPC*(M / E), MINB)
+    k_zi_reg(Geo g, const double2* __restrict__ twM, const double2* __restrict__ twN,
+             const double2* __restrict__ spec, double* __restrict__ out, double scale, EpiArgs epi) {
+  constexpr int T = M / E, N = 2 * M;
+  static_assert(32 % T == 0, "a line must not straddle a warp");
+  extern __shared__ double2 sm[];
+  const int t = threadIdx.x % T, w = threadIdx.x / T;
+  const int nxy = g.Nx * g.Ny;
+  const int64_t nl = int64_t(9) * nxy;
+  int64_t gl = int64_t(blockIdx.x) * LPC + w;
+  const bool live = gl < nl;
+  if (!live) gl = nl - 1;  // tail lanes transform a valid line (warp-synchronous) and store nothing
+  const int c = int(gl / nxy);
+  const int L = int(gl - int64_t(c) * nxy);
+  const double2* X = spec + gl * M;
+  double2 xk[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) xk[m] = X[t + T * m];
+  // Z[k] = (X[k] + X*[M-k]) + i W_N^-k (X[k] - X*[M-k]), X[M] = 0 (ZeroCompatible)
+  double2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const double2 xm = mirror_take<T>(mirror_give<E>(xk, t, m), t);
+    const int k = t + T * m;
+    double2 a = xk[m];
+    double2 b = make_double2(0.0, 0.0);
+    if (k == 0) a.y = 0.0;  // Re(ifft): drop the round-off imaginary part of kz = 0
+    else b = cconj(xm);
+    const double2 tt = cmulc(csub(a, b), __ldg(&twN[k]));
+    v[m] = make_double2(a.x + b.x - tt.y, a.y + b.y + tt.x);
+  }
+  reg::fft_swz<M, E, +1>(v, sm + w * M, t, twM);
+  // v[m] = z[n], n = t + T m: the real voxel pair (2n, 2n + 1)
+  const int64_t base = int64_t(c) * g.n + g.roff + int64_t(L) * N;
+  double dot = 0.0;
+  if (epi.r) {
+    // fused CG update, solver.cpp:46-48 with the rounding of k_cg_update:
+    // Ap stays on chip; r -= alpha Ap, x += alpha p, partial <r, r>
+    if (live && epi.scal[S_FLAG] == 0.0) {
+      const double alpha = epi.scal[S_ALPHA];
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const int64_t o = base + 2 * (t + T * m);
+        const double2 av = make_double2(v[m].x * scale, v[m].y * scale);
+        double2 rv = *reinterpret_cast<const double2*>(epi.r + o);
+        if (epi.x) {  // else the next pass 1 applies x += alpha p (ProArgs::x)
+          double2* xp = reinterpret_cast<double2*>(epi.x + o);
+          const double2 pv = __ldg(reinterpret_cast<const double2*>(epi.p + o));
+          double2 xv = *xp;
+          xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+          xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+          *xp = xv;
+        }
+        rv.x = __dadd_rn(rv.x, __dmul_rn(-alpha, av.x));
+        rv.y = __dadd_rn(rv.y, __dmul_rn(-alpha, av.y));
+        *reinterpret_cast<double2*>(epi.r + o) = rv;
+        dot += rv.x * rv.x;
+        dot += rv.y * rv.y;
+      }
+    }
+  } else if (live) {
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int64_t o = base + 2 * (t + T * m);
+      const double2 val = make_double2(v[m].x * scale, v[m].y * scale);
+      *reinterpret_cast<double2*>(out + o) = val;
+      if (epi.partial) {
+        const double2 pp = __ldg(reinterpret_cast<const double2*>(epi.pdot + o));
+        dot += pp.x * val.x;
+        dot += pp.y * val.y;
+      }
+    }
+  }
+  if (epi.partial) {  // fused <p, Ap> or <r, r> partial (solver.cpp:37, 48)
+    dot = block_sum_any(dot);
+    if (threadIdx.x == 0) epi.partial[blockIdx.x] = dot;
+  }
+}
+
+// z-forward of G (PRO_COPY): real pairs straight into registers, M-point FFT,
+// r2c untangling with the mirror partner by shuffle, spectrum stored from
+// registers.  Same arithmetic as the staged z-forward passes.
+template <int M, int E, int LPC, int MINB>
+__global__ void __launch_bounds__(LPC*(M / E), MINB)
+    k_zf_reg(Geo g, const double2* __restrict__ twM, const double2* __restrict__ twN, const double* __restrict__ A,
+             double2* __restrict__ spec) {
+  constexpr int T = M / E, N = 2 * M;
+  static_assert(32 % T == 0, "a line must not straddle a warp");
+  extern __shared__ double2 sm[];
+  const int t = threadIdx.x % T, w = threadIdx.x / T;
+  const int nxy = g.Nx * g.Ny;
+  const int64_t nl = int64_t(9) * nxy;
+  int64_t gl = int64_t(blockIdx.x) * LPC + w;
+  const bool live = gl < nl;
+  if (!live) gl = nl - 1;
+  const int c = int(gl / nxy);
+  const int L = int(gl - int64_t(c) * nxy);
+  const double* src = A + int64_t(c) * g.n + g.roff + int64_t(L) * N;
+  double2 v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = __ldg(reinterpret_cast<const double2*>(src + 2 * (t + T * m)));
+  reg::fft_swz<M, E, -1>(v, sm + w * M, t, twM);
+  double2* dst = spec + gl * M;
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int k = t + T * m;
+    const double2 a = v[m];
+    const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
+    const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+    const double2 D = csub(a, b);
+    const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+    if (live) dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
   }
 }
 
@@ -825,10 +972,69 @@ void zf_kind(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, bool d
   *st = launched(ctx, "k_zf_fast");
 }
 
+// Register-resident z passes (k_zi_reg / k_zf_reg): E elements per lane,
+// 128 threads per CTA, MINB CTAs/SM for the register budget.  FM_ZREG=0
+// selects the staged passes instead (A/B measurements).
+int zreg_mode() {
+  static int v = [] {
+    const char* e = getenv("FM_ZREG");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+template <int M>
+struct ZReg {
+  static constexpr int E = M >= 128 ? 16 : 8;
+  static constexpr int T = M / E;
+  static constexpr int LPC = 128 / T;
+  static constexpr int THREADS = LPC * T;
+  static constexpr int MINB = 4;
+  static constexpr size_t SMEM = size_t(LPC) * M * 16;
+  static constexpr bool OK = M >= 16 && 32 % T == 0;
+};
+
+template <int M>
+bool zf_reg_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
+  using S = ZReg<M>;
+  if constexpr (!S::OK) {
+    return false;
+  } else {
+    static bool a = (allow(k_zf_reg<M, S::E, S::LPC, S::MINB>, S::SMEM), true);
+    (void)a;
+    const int64_t nl = int64_t(9) * g.Nx * g.Ny;
+    const dim3 grid(unsigned((nl + S::LPC - 1) / S::LPC));
+    k_zf_reg<M, S::E, S::LPC, S::MINB>
+        <<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa.A, spec);
+    ctx->zf_partials = 0;
+    return true;
+  }
+}
+
+template <int M>
+bool zi_reg_go(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi) {
+  using S = ZReg<M>;
+  if constexpr (!S::OK) {
+    return false;
+  } else {
+    static bool a = (allow(k_zi_reg<M, S::E, S::LPC, S::MINB>, S::SMEM), true);
+    (void)a;
+    const int64_t nl = int64_t(9) * g.Nx * g.Ny;
+    const dim3 grid(unsigned((nl + S::LPC - 1) / S::LPC));
+    k_zi_reg<M, S::E, S::LPC, S::MINB>
+        <<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+    ctx->zi_partials = int(grid.x);
+    return true;
+  }
+}
+
 template <int M>
 bool zf_launch(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int* st) {
   const bool dir = pa.r != nullptr;
   const bool pap = pa.pap_partial != nullptr;
+  if (pa.kind == PRO_COPY && zreg_mode() && zf_reg_go<M>(ctx, g, pa, spec)) {
+    *st = launched(ctx, "k_zf_reg");
+    return true;
+  }
   if (pa.kind == PRO_COPY) {
     if (zpipe_mode() && zpipe_go<M, PRO_COPY, false, false>(ctx, g, pa, spec)) {
       *st = launched(ctx, "k_zf_pipe");
@@ -867,6 +1073,10 @@ using ZiShape = std::conditional_t<(M >= 128), ZS<M, 16, 1, (M == 128 ? 6 : 4)>,
 template <int M>
 bool zi_launch(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
                int* st) {
+  if (zreg_mode() && zi_reg_go<M>(ctx, g, spec, out, scale, epi)) {
+    *st = launched(ctx, "k_zi_reg");
+    return true;
+  }
   zi_go<M, ZiShape<M>>(ctx, g, spec, out, scale, epi);
   ctx->zi_partials = (g.Nx * g.Ny + ZiShape<M>::G - 1) / ZiShape<M>::G;
   *st = launched(ctx, "k_zi_fast");
