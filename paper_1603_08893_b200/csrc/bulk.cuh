@@ -45,5 +45,11 @@ __device__ __forceinline__ void g2s(void* dst, const void* src, unsigned bytes, 
                : "memory");
 }
 
+// Bulk prefetch of [src, src + bytes) into L2 (no shared memory, no
+// completion tracking): bytes a multiple of 16, src 16-byte aligned.
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
 }  // namespace bulk
 }  // namespace fm

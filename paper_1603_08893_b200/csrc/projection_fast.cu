@@ -697,6 +697,15 @@ __global__ void __launch_bounds__(LPC*(M / E), MINB)
   const int c = int(gl / nxy);
   const int L = int(gl - int64_t(c) * nxy);
   const double2* X = spec + gl * M;
+  const int64_t base = int64_t(c) * g.n + g.roff + int64_t(L) * N;
+  if (t == 0 && live) {  // epilogue operands stream into L2 while the line is transformed
+    if (epi.r) bulk::prefetch_l2(epi.r + base, N * 8);
+    if (epi.x) {
+      bulk::prefetch_l2(epi.x + base, N * 8);
+      bulk::prefetch_l2(epi.p + base, N * 8);
+    }
+    if (epi.pdot) bulk::prefetch_l2(epi.pdot + base, N * 8);
+  }
   double2 xk[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) xk[m] = X[t + T * m];
@@ -715,7 +724,6 @@ __global__ void __launch_bounds__(LPC*(M / E), MINB)
   }
   reg::fft_swz<M, E, +1>(v, sm + w * M, t, twM);
   // v[m] = z[n], n = t + T m: the real voxel pair (2n, 2n + 1)
-  const int64_t base = int64_t(c) * g.n + g.roff + int64_t(L) * N;
   double dot = 0.0;
   if (epi.r) {
     // fused CG update, solver.cpp:46-48 with the rounding of k_cg_update:
