@@ -730,24 +730,42 @@ __global__ void __launch_bounds__(LPC*(M / E), MINB)
     // Ap stays on chip; r -= alpha Ap, x += alpha p, partial <r, r>
     if (live && epi.scal[S_FLAG] == 0.0) {
       const double alpha = epi.scal[S_ALPHA];
+      double2* rp = reinterpret_cast<double2*>(epi.r + base) + t;
+      // r is read and written through one pointer: load a batch of KB lines'
+      // worth before any store so the loads are not serialised behind them
+      constexpr int KB = 8;
 #pragma unroll
-      for (int m = 0; m < E; ++m) {
-        const int64_t o = base + 2 * (t + T * m);
-        const double2 av = make_double2(v[m].x * scale, v[m].y * scale);
-        double2 rv = *reinterpret_cast<const double2*>(epi.r + o);
-        if (epi.x) {  // else the next pass 1 applies x += alpha p (ProArgs::x)
-          double2* xp = reinterpret_cast<double2*>(epi.x + o);
-          const double2 pv = __ldg(reinterpret_cast<const double2*>(epi.p + o));
-          double2 xv = *xp;
-          xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
-          xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
-          *xp = xv;
+      for (int m0 = 0; m0 < E; m0 += KB) {
+        double2 rv[KB];
+#pragma unroll
+        for (int q = 0; q < KB; ++q) rv[q] = __ldcg(rp + T * (m0 + q));
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          const int m = m0 + q;
+          const double2 av = make_double2(v[m].x * scale, v[m].y * scale);
+          rv[q].x = __dadd_rn(rv[q].x, __dmul_rn(-alpha, av.x));
+          rv[q].y = __dadd_rn(rv[q].y, __dmul_rn(-alpha, av.y));
+          rp[T * m] = rv[q];
+          dot += rv[q].x * rv[q].x;
+          dot += rv[q].y * rv[q].y;
         }
-        rv.x = __dadd_rn(rv.x, __dmul_rn(-alpha, av.x));
-        rv.y = __dadd_rn(rv.y, __dmul_rn(-alpha, av.y));
-        *reinterpret_cast<double2*>(epi.r + o) = rv;
-        dot += rv.x * rv.x;
-        dot += rv.y * rv.y;
+      }
+      if (epi.x) {  // K4 / compact J2: x += alpha p here (SVK: the next pass 1 applies it, ProArgs::x)
+        double2* xp = reinterpret_cast<double2*>(epi.x + base) + t;
+        const double2* pp = reinterpret_cast<const double2*>(epi.p + base) + t;
+#pragma unroll
+        for (int m0 = 0; m0 < E; m0 += KB) {
+          double2 xv[KB];
+#pragma unroll
+          for (int q = 0; q < KB; ++q) xv[q] = __ldcg(xp + T * (m0 + q));
+#pragma unroll
+          for (int q = 0; q < KB; ++q) {
+            const double2 pv = __ldg(pp + T * (m0 + q));
+            xv[q].x = __dadd_rn(xv[q].x, __dmul_rn(alpha, pv.x));
+            xv[q].y = __dadd_rn(xv[q].y, __dmul_rn(alpha, pv.y));
+            xp[T * (m0 + q)] = xv[q];
+          }
+        }
       }
     }
   } else if (live) {
