@@ -213,8 +213,12 @@ __global__ void __launch_bounds__(TW*(N / E)) k_x_fast3(Geo g, const double2* __
 // (component q+2 streams in while q is transformed) and each buffer doubles
 // as the transform's exchange scratch; the inverse transforms store straight
 // from registers.  64 KB per CTA at N = 256, TW = 8.
+template <int N, int TW, int E>
+constexpr int x4_minb() {  // CTAs/SM the register budget targets: capped by the two tile buffers
+  return std::max(1, std::min(E >= 16 ? 3 : 2, int((227 * 1024) / (2 * size_t(N) * TW * 16 + 1024))));
+}
 template <int N, int TW, int E, bool RT = false>
-__global__ void __launch_bounds__(TW*(N / E), E >= 16 ? 3 : 2) k_x_fast4(Geo g, const double2* __restrict__ tw,
+__global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo g, const double2* __restrict__ tw,
                                                        double2* __restrict__ spec) {
   constexpr int T = N / E;
   extern __shared__ double2 sm[];
@@ -898,14 +902,15 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   constexpr int TW = tw_x(N);
   constexpr int T = N / e_x(N);
   const size_t smem = size_t(N) * TW * 16;
-  // Measured (scripts/xvar.py): ZeroCompatible -> scalar-accumulating k_x_fast4
-  // (8-column tiles up to 256, 4-column tiles at 512: 3 CTAs/SM); other modes
+  // Measured (scripts/xvar.py, pass_times.py): ZeroCompatible -> scalar-accumulating
+  // k_x_fast4 (8-column tiles up to 256, 4-column tiles at 512 and 1024); other modes
   // -> whole-tile prefetch k_x_fast3; registers-only k_x_fast as the fallback.
+  // (512: 8-column tiles, 1 CTA/SM, measured no faster; 1024: 72.7 ms at 1024^3
+  // against 120 ms for the registers-only pass)
   const bool zc = ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE;
-  if (zc && N >= 64 && N <= 256 && ctx->nzh % 8 == 0) {
-    x4_go<N, 8, e_line(N)>(ctx, g, spec);
-  } else if (zc && N == 512 && ctx->nzh % 4 == 0) {
-    x4_go<N, 4, e_line(N)>(ctx, g, spec);
+  constexpr int X4TW = N >= 512 ? 4 : 8;
+  if (zc && N >= 64 && ctx->nzh % X4TW == 0) {
+    x4_go<N, X4TW, e_line(N)>(ctx, g, spec);
   } else if (N <= 512 && ctx->nzh % 8 == 0 && !(zc && N < 64)) {
     x3_go<N, 8, e_line(N)>(ctx, g, spec);
   } else {
