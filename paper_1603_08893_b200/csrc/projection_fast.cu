@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(TW*(N / E)) k_x_fast3(Geo g, const double2* __
 
 // x pass, scalar-accumulating variant (ZeroCompatible mode only).  The
 // projection of row i is Bhat_ij = s xi_j / |xi|^2 with s = sum_q Ahat_iq xi_q,
-// so the three forward transforms only have to accumulate s in registers:
-// per thread E values of s plus E working values, instead of all 3 x E.
+// so the forward transforms only have to accumulate s in registers: per
+// thread E values of s plus E working values, instead of all 3 x E.  Since
+// xi_y and xi_z are constant along an x-line, linearity folds the row into
+// two forward and two inverse transforms instead of three and three.
 // Component tiles (N x TW) are double-buffered in shared memory with cp.async
 // (component q+2 streams in while q is transformed) and each buffer doubles
 // as the transform's exchange scratch; the inverse transforms store straight
@@ -244,22 +246,37 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
   const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
   const double xiy = qy * g.invL[1], xiz = qz * g.invL[2];
   double2 s[E], v[E];
+  // s = FFT(A_i0) xi_x + FFT(A_i1) xi_y + FFT(A_i2) xi_z.  xi_y and xi_z are
+  // constant along the x-line, so by linearity the last two terms are ONE
+  // transform, FFT(xi_y A_i1 + xi_z A_i2): two forward FFTs instead of three.
+  // (Rolled loops keep one copy of each transform: the register budget.)
 #pragma unroll 1
-  for (int q = 0; q < 3; ++q) {
-    double2* B = (q == 1) ? buf1 : buf0;
-    if (q < 2) asm volatile("cp.async.wait_group 1;\n" ::);
-    else asm volatile("cp.async.wait_group 0;\n" ::);
+  for (int q = 0; q < 2; ++q) {
+    asm volatile("cp.async.wait_group 0;\n" ::);  // q = 0 waits for tile 1 as well (it lands with tile 0)
     __syncthreads();
+    if (q == 0) {
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = B[(t + T * m) * TW + l];
+      for (int m = 0; m < E; ++m) v[m] = buf0[(t + T * m) * TW + l];
+    } else {
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const double2 a1 = buf1[(t + T * m) * TW + l], a2 = buf0[(t + T * m) * TW + l];
+        v[m] = make_double2(fma(a1.x, xiy, a2.x * xiz), fma(a1.y, xiy, a2.y * xiz));
+      }
+    }
     __syncthreads();
-    reg::fft<N, E, -1>(v, B + l, TW, t, tw);  // ends past a barrier: B is free again
-    if (q == 0) fetch(2, buf0);
+    double2* X = q == 0 ? buf0 : buf1;
+    reg::fft<N, E, -1>(v, X + l, TW, t, tw);  // ends past a barrier: X is free again
+    if (q == 0) {
+      fetch(2, buf0);
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const double xq = q == 0 ? freq_of(t + T * m, N) * g.invL[0] : (q == 1 ? xiy : xiz);
-      if (q == 0) s[m] = make_double2(v[m].x * xq, v[m].y * xq);
-      else s[m] = make_double2(fma(v[m].x, xq, s[m].x), fma(v[m].y, xq, s[m].y));
+      for (int m = 0; m < E; ++m) {
+        const double xq = freq_of(t + T * m, N) * g.invL[0];
+        s[m] = make_double2(v[m].x * xq, v[m].y * xq);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < E; ++m) s[m] = make_double2(s[m].x + v[m].x, s[m].y + v[m].y);
     }
   }
   // s <- s / |xi|^2, zero at xi = 0 and on Nyquist planes (ZeroCompatible)
@@ -272,22 +289,29 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
     const double inv = zero ? 0.0 : 1.0 / norm2;
     s[m] = make_double2(s[m].x * inv, s[m].y * inv);
   }
+  // Bhat_i0 = IFFT(s xi_x); Bhat_i1 = xi_y IFFT(s), Bhat_i2 = xi_z IFFT(s): two
+  // inverse FFTs instead of three, by the same linearity
   double2* base = tile + l;
 #pragma unroll 1
-  for (int j = 0; j < 3; ++j) {
-    double2* B = (j == 1) ? buf0 : buf1;
+  for (int q = 0; q < 2; ++q) {
 #pragma unroll
     for (int m = 0; m < E; ++m) {
-      const double f = j == 0 ? freq_of(t + T * m, N) * g.invL[0] : (j == 1 ? xiy : xiz);
+      const double f = q == 0 ? freq_of(t + T * m, N) * g.invL[0] : 1.0;
       v[m] = make_double2(s[m].x * f, s[m].y * f);
     }
-    reg::fft<N, E, +1>(v, B + l, TW, t, tw);
-    if constexpr (!RT) {
+    reg::fft<N, E, +1>(v, (q == 0 ? buf0 : buf1) + l, TW, t, tw);
+#pragma unroll 1
+    for (int j = q; j < (q == 0 ? 1 : 3); ++j) {
+      const double f = j == 0 ? 1.0 : (j == 1 ? xiy : xiz);
+      if constexpr (!RT) {
 #pragma unroll
-      for (int m = 0; m < E; ++m) base[(int64_t(j) * N + t + T * m) * xstride] = v[m];
-    } else {
+        for (int m = 0; m < E; ++m)
+          base[(int64_t(j) * N + t + T * m) * xstride] = make_double2(v[m].x * f, v[m].y * f);
+      } else {
 #pragma unroll
-      for (int m = 0; m < E; ++m) store_xb(g, nullptr, i * 3 + j, t + T * m, y, kz, v[m]);
+        for (int m = 0; m < E; ++m)
+          store_xb(g, nullptr, i * 3 + j, t + T * m, y, kz, make_double2(v[m].x * f, v[m].y * f));
+      }
     }
   }
 }
