@@ -709,7 +709,9 @@ __global__ void __launch_bounds__(S::THREADS, 2048 / S::THREADS >= S::MINB ? S::
 // independent here, so this is the shape of the z-inverse (every operator)
 // and of the z-forward of G (no per-voxel prologue coupling the components).
 
-template <int M, int E, int LPC, int MINB>
+// PF: the epilogue reads operands (fused CG r / x / p, or the <p, Ap> pdot):
+// prefetch them into L2 at entry.  The plain store variant carries no such code.
+template <int M, int E, int LPC, int MINB, bool PF = false>
 __global__ void __launch_bounds__(LPC*(M / E), MINB)
     k_zi_reg(Geo g, const double2* __restrict__ twM, const double2* __restrict__ twN,
              const double2* __restrict__ spec, double* __restrict__ out, double scale, EpiArgs epi) {
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(LPC*(M / E), MINB)
   const int L = int(gl - int64_t(c) * nxy);
   const double2* X = spec + gl * M;
   const int64_t base = int64_t(c) * g.n + g.roff + int64_t(L) * N;
-  if (t == 0 && live) {  // epilogue operands stream into L2 while the line is transformed
+  if (PF && t == 0 && live) {  // epilogue operands stream into L2 while the line is transformed
     if (epi.r) bulk::prefetch_l2(epi.r + base, N * 8);
     if (epi.x) {
       bulk::prefetch_l2(epi.x + base, N * 8);
@@ -1071,12 +1073,19 @@ bool zi_reg_go(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, doub
   if constexpr (!S::OK) {
     return false;
   } else {
-    static bool a = (allow(k_zi_reg<M, S::E, S::LPC, S::MINB>, S::SMEM), true);
-    (void)a;
     const int64_t nl = int64_t(9) * g.Nx * g.Ny;
     const dim3 grid(unsigned((nl + S::LPC - 1) / S::LPC));
-    k_zi_reg<M, S::E, S::LPC, S::MINB>
-        <<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+    if (epi.r || epi.partial) {
+      static bool a = (allow(k_zi_reg<M, S::E, S::LPC, S::MINB, true>, S::SMEM), true);
+      (void)a;
+      k_zi_reg<M, S::E, S::LPC, S::MINB, true>
+          <<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+    } else {
+      static bool a = (allow(k_zi_reg<M, S::E, S::LPC, S::MINB>, S::SMEM), true);
+      (void)a;
+      k_zi_reg<M, S::E, S::LPC, S::MINB>
+          <<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
+    }
     ctx->zi_partials = int(grid.x);
     return true;
   }
