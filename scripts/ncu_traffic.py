@@ -10,8 +10,8 @@ import sys
 
 PASS_OF = [  # (regex on the kernel name, pass key of bench.py)
     (r"k_zf_pipe<\d+, 2, 0", "z_fwd_svk"), (r"k_zf_fast<\d+, 2, 0", "z_fwd_svk"),
-    (r"k_zf_fast<\d+, 1, 0", "z_fwd_k4"), (r"k_y_fast<\d+, \d+, \(int\)-1>", "y_fwd"),
-    (r"k_y_fast<\d+, \d+, 1>", "y_inv"), (r"k_x_fast", "x_ghat"), (r"k_zi_fast", "z_inv"),
+    (r"k_zf_fast<\d+, 1, 0", "z_fwd_k4"), (r"k_y_fast<\d+, \d+, \(int\)-1", "y_fwd"),
+    (r"k_y_fast<\d+, \d+, 1[,>]", "y_inv"), (r"k_x_fast", "x_ghat"), (r"k_zi_(fast|reg)", "z_inv"),
 ]
 
 
