@@ -935,7 +935,7 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   // against 120 ms for the registers-only pass)
   const bool zc = ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE;
   constexpr int X4TW = N >= 512 ? 4 : 8;
-  if (zc && N >= 64 && ctx->nzh % X4TW == 0) {
+  if (zc && N >= 64 && ctx->nzh % X4TW == 0) {  // (8 elements/thread at 512: 6.5 vs 5.9 ms)
     x4_go<N, X4TW, e_line(N)>(ctx, g, spec);
   } else if (N <= 512 && ctx->nzh % 8 == 0 && !(zc && N < 64)) {
     x3_go<N, 8, e_line(N)>(ctx, g, spec);
