@@ -348,7 +348,8 @@ struct ZS {
 };
 template <int M, bool HEAVY = false>
 struct ZShapeSel {
-  static constexpr int E = HEAVY ? e_line(M) : reg::e_z(M);
+  // (a line's T = M / E lanes must fit one warp: E = 16 from M = 512 up)
+  static constexpr int E = HEAVY ? e_line(M) : (M / reg::e_z(M) > 32 ? 16 : reg::e_z(M));
   static constexpr int T = M / E;
   static constexpr int TT = HEAVY ? 16 : 32;
   using type = ZS<M, E, (T >= TT ? 1 : TT / T)>;
@@ -361,7 +362,10 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
                                                                 const double2* __restrict__ twN,
                                                                 ProArgs pa, double2* __restrict__ spec) {
   using S = ZShape<M, PRO != PRO_COPY>;
-  constexpr int N = 2 * M, G = S::G, LSP = S::LSP, T = S::T, E = S::E;
+  constexpr int N = 2 * M, G = S::G, T = S::T, E = S::E;
+  // line l = c G + gi owns the swizzled region sm + l M (reg::fft_swz)
+  constexpr int SW = reg::ilog2(E);
+  static_assert(32 % T == 0, "a line must not straddle a warp");
   extern __shared__ double2 sm[];
   const int nxy = g.Nx * g.Ny;
   const int L0 = blockIdx.x * G;
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
       prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v0, &pap);
       prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node + 1, v1, &pap);
 #pragma unroll
-      for (int c = 0; c < 9; ++c) sm[m * LSP + c * G + gi] = make_double2(v0[c], v1[c]);
+      for (int c = 0; c < 9; ++c) sm[(c * G + gi) * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
     }
   } else {
     double* smd = reinterpret_cast<double*>(sm);
@@ -393,33 +397,33 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
       double v[9];
       prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v, &pap);
 #pragma unroll
-      for (int c = 0; c < 9; ++c) smd[((z >> 1) * LSP + c * G + gi) * 2 + (z & 1)] = v[c];
+      for (int c = 0; c < 9; ++c) smd[((c * G + gi) * M + reg::xaddr<SW>(z >> 1, 0)) * 2 + (z & 1)] = v[c];
     }
   }
   __syncthreads();
-  // phase 2: M-point complex FFT of every line, lines fastest across lanes
+  // phase 2: each line transformed by its T lanes (swizzled exchange, warp
+  // syncs), r2c untangling X[k] = E[k] + W_N^k O[k] with the partner M - k by
+  // shuffle, k < M stored from registers (kz = M dropped)
   {
-    const int l = threadIdx.x % S::LSL, t = threadIdx.x / S::LSL;
+    const int l = threadIdx.x / T, t = threadIdx.x % T;
+    const int c = l / G, gi = l - c * G;
+    double2* line = sm + l * M;
     double2 v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = sm[(t + T * m) * LSP + l];
-    __syncthreads();
-    reg::fft<M, E, -1>(v, sm + l, LSP, t, twM);
+    for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
+    __syncwarp();
+    reg::fft_swz<M, E, -1>(v, line, t, twM);
+    double2* dst = spec + (int64_t(c) * nxy + L0 + gi) * M;
 #pragma unroll
-    for (int m = 0; m < E; ++m) sm[(t + T * m) * LSP + l] = v[m];
-  }
-  __syncthreads();
-  // phase 3: untangle X[k] = E[k] + W_N^k O[k] and store k < M (kz = M dropped)
-  for (int w = threadIdx.x; w < 9 * Gb * M; w += blockDim.x) {
-    const int c = w / (Gb * M), rem = w - c * (Gb * M);
-    const int gi = rem / M, k = rem - gi * M;
-    const int l = c * G + gi;
-    const double2 a = sm[k * LSP + l];
-    const double2 b = cconj(sm[((M - k) & (M - 1)) * LSP + l]);
-    const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
-    const double2 D = csub(a, b);
-    const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
-    spec[(int64_t(c) * nxy + L0 + gi) * M + k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+    for (int m = 0; m < E; ++m) {
+      const int k = t + T * m;
+      const double2 a = v[m];
+      const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
+      const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+      const double2 D = csub(a, b);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      if (gi < Gb) dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+    }
   }
   if constexpr (PAP) {
     pap = block_sum_any(pap);
