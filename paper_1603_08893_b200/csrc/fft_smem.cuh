@@ -3,10 +3,11 @@
 // Generic path of the projection passes: a CTA holds `nl` lines of length
 // N in shared memory (element e of line l at a[l*ls + e*es]) and runs the
 // mixed-radix Stockham autosort recursion in place between two buffers.
-// Each work item produces ONE output of a radix-R stage:
+// A radix-R stage computes
 //   out[o] = sum_r in[j + r N/R] * W_N^{ r (j mod Ns + k Ns) N/(Ns R) }
 // with o = (j/Ns) Ns R + j mod Ns + k Ns, which covers any radix (including
-// a prime such as 31) with one table lookup per term.  Specialised
+// a prime such as 31) with one table lookup per term; each work item forms up
+// to four outputs k of one input set j.  Specialised
 // register-resident kernels for power-of-two N are layered on top of this
 // (fft_reg.cuh); this engine is the correctness baseline for every size.
 #pragma once
@@ -45,34 +46,53 @@ __device__ __forceinline__ double2* fft_smem(double2* a, double2* b, int nl, int
     const int R = P.radix[s];
     const int NR = N / R;
     const int tstep = N / (Ns * R);
-    const int total = nl * N;
+    // outputs (j, k) with the same j read the same R inputs: each work item
+    // computes up to KB of them (k = kg + KG q) from one pass over the inputs,
+    // cutting the shared-memory input traffic by KB (same accumulation order
+    // per output as one output per item, so results are bit-identical)
+    constexpr int KB = 4;
+    const int KG = (R + KB - 1) / KB;
+    const int total = nl * NR * KG;
     for (int w = threadIdx.x; w < total; w += blockDim.x) {
-      int l, o;
+      int l, rest;
       if (lfast) {
         l = w % nl;
-        o = w / nl;
+        rest = w / nl;
       } else {
-        l = w / N;
-        o = w - l * N;
+        l = w / (NR * KG);
+        rest = w - l * (NR * KG);
       }
-      const int k = (o / Ns) % R;
-      const int jm = o % Ns;
-      const int j = (o / (Ns * R)) * Ns + jm;
-      const int e0 = (jm + k * Ns) * tstep;  // < N
+      const int kg = rest % KG;
+      const int j = rest / KG;
+      const int jm = j % Ns;
       const double2* src = a + l * ls + j * es;
-      double2 acc = src[0];
-      int ex = 0;
-      // unrolled: the loads of 4 terms are issued together (small grids are
-      // load-latency bound here); the accumulation order is unchanged
-#pragma unroll 4
-      for (int r = 1; r < R; ++r) {
-        ex += e0;
-        if (ex >= N) ex -= N;
-        const double2 v = src[r * NR * es];
-        const double2 t = tws[ex];
-        acc = cadd(acc, sign < 0 ? cmul(v, t) : cmulc(v, t));
+      const double2 x0 = src[0];
+      double2 acc[KB];
+      int e0[KB], ex[KB];
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        const int k = kg + KG * q;
+        e0[q] = (jm + k * Ns) * tstep % N;  // < N (k < R); k >= R is computed and discarded
+        ex[q] = 0;
+        acc[q] = x0;
       }
-      b[l * ls + o * es] = acc;
+#pragma unroll 2
+      for (int r = 1; r < R; ++r) {
+        const double2 v = src[r * NR * es];
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+          ex[q] += e0[q];
+          if (ex[q] >= N) ex[q] -= N;
+          const double2 t = tws[ex[q]];
+          acc[q] = cadd(acc[q], sign < 0 ? cmul(v, t) : cmulc(v, t));
+        }
+      }
+      const int ob = (j / Ns) * Ns * R + jm;
+#pragma unroll
+      for (int q = 0; q < KB; ++q) {
+        const int k = kg + KG * q;
+        if (k < R) b[l * ls + (ob + k * Ns) * es] = acc[q];
+      }
     }
     __syncthreads();
     double2* t = a;
