@@ -18,7 +18,9 @@ flush is needed between steps).
 
 --impl reference times the CPU oracle (restatement of the reference
 apply_projected_tangent; the reference itself needs FFTW3/Eigen3, absent on
-the box) on a bounded 128^3 sample per step.
+the box) on one 256^3 matvec per step (one 128^3 matvec when --steps/--warmup
+would make that run longer than a few minutes); cpu_baseline is one 256^3
+matvec (~20 s of single-core work).
 """
 from __future__ import annotations
 
@@ -149,7 +151,11 @@ def cpu_reference_run(args, world, rank):
     if rank != 0:
         return
     from oracle import oracle as O
-    N = args.cpu_grid
+    # the config-2 grid itself when the whole --steps/--warmup run fits a few
+    # minutes of single-core work (~20 s per 256^3 matvec), else a 128^3 sample
+    N = args.grid
+    while N > 64 and (args.steps + args.warmup) * 20.0 * (N / 256.0) ** 3 > 150.0:
+        N //= 2
     n = N ** 3
     lam, mu = config2_inputs(N)
     F = np.zeros(9 * n)
@@ -168,7 +174,9 @@ def cpu_reference_run(args, world, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"config2 sample: {N}^3 SVK Bernoulli(0.3) contrast 10, one G:K4:dF matvec per step"},
+        "config": {"workload": f"config2: {args.grid}^3 SVK Bernoulli(0.3) seed 2, contrast 10, "
+                               "G:K4:dF matvec (K4 at F_bar)",
+                   "cpu_sample": f"one {N}^3 G:K4:dF matvec per step (same generator and seed)"},
         "cpu_baseline": {"value": v, "unit": "voxel/s", "cores": 1, "kind": "port",
                          "sample": f"{N}^3 apply_projected_tangent per step (reference is single-threaded; "
                                    f"FFTW3/Eigen3 absent so the oracle restatement is timed)"},
@@ -201,7 +209,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--grid", type=int, default=256)
-    ap.add_argument("--cpu-grid", type=int, default=128)
+    ap.add_argument("--cpu-grid", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent copies instead of slabs")
