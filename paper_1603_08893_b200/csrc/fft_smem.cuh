@@ -36,11 +36,18 @@ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -
 // interleaved element-wise, ls == 1) so smem accesses are consecutive.
 // tws: shared-memory space for the N-entry twiddle table (staged here once;
 // latency-bound small grids otherwise wait on one L2 round trip per term).
+// tw_pre: the table already staged in shared memory (persistent kernels stage
+// each axis's table once), else it is staged into tws here.
 __device__ __forceinline__ double2* fft_smem(double2* a, double2* b, int nl, int ls, int es,
-                                             const AxisPlan& P, int sign, bool lfast, double2* tws) {
+                                             const AxisPlan& P, int sign, bool lfast, double2* tws,
+                                             const double2* tw_pre = nullptr) {
   const int N = P.N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) tws[i] = __ldg(&P.tw[i]);
-  __syncthreads();
+  if (tw_pre) {
+    tws = const_cast<double2*>(tw_pre);
+  } else {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) tws[i] = __ldg(&P.tw[i]);
+    __syncthreads();
+  }
   int Ns = 1;
   for (int s = 0; s < P.nst; ++s) {
     const int R = P.radix[s];

@@ -35,7 +35,7 @@ namespace fm {
 template <int TD, int PRO, bool DIR, bool PAP = false>
 __device__ __forceinline__ void zfwd_body(const Geo& g, const AxisPlan& plan, const double2* __restrict__ twN,
                                           const ProArgs& pa, double2* __restrict__ spec, int G, int ls, int bx,
-                                          double2* sm) {
+                                          double2* sm, const double2* tw_pre = nullptr) {
   constexpr int NC = TD * TD;
   const int nxy = g.Nx * g.Ny;
   const int L0 = bx * G;
@@ -59,7 +59,7 @@ __device__ __forceinline__ void zfwd_body(const Geo& g, const AxisPlan& plan, co
     }
   }
   __syncthreads();
-  double2* R = fft_smem(A, B, NC * G, ls, 1, plan, -1, false, sm + 2 * NC * G * ls);
+  double2* R = fft_smem(A, B, NC * G, ls, 1, plan, -1, false, sm + 2 * NC * G * ls, tw_pre);
   const int M = g.Lz;
   for (int w = threadIdx.x; w < NC * Gb * g.nzh; w += blockDim.x) {
     const int line = w / g.nzh, k = w - line * g.nzh;
@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(256) k_zfwd(Geo g, AxisPlan plan, const double
 // In place on one device; P > 1 the forward pass (sign -1) stores into the
 // x-pass inputs of the y-slab owners (store_yf, the fused slab transpose).
 __device__ __forceinline__ void ypass_body(const Geo& g, const AxisPlan& plan, const double2* in, double2* out,
-                                           int TW, int sign, int bx, int by, int bz, double2* sm) {
+                                           int TW, int sign, int bx, int by, int bz, double2* sm,
+                                           const double2* tw_pre = nullptr) {
   const int kz0 = bx * TW;
   const int x = by, c = bz;
   const int Ny = g.Ny;
@@ -112,7 +113,7 @@ __device__ __forceinline__ void ypass_body(const Geo& g, const AxisPlan& plan, c
       A[w] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  double2* R = fft_smem(A, B, TW, 1, TW, plan, sign, true, sm + 2 * Ny * TW);
+  double2* R = fft_smem(A, B, TW, 1, TW, plan, sign, true, sm + 2 * Ny * TW, tw_pre);
   for (int w = threadIdx.x; w < Ny * TW; w += blockDim.x) {
     const int e = w / TW, t = w - e * TW;
     const int kz = kz0 + t;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(256) k_ypass(Geo g, AxisPlan plan, const doubl
 // ------------------------------------------------------------------ pass 3
 template <int TD>
 __device__ __forceinline__ void xpass_body(const Geo& g, const AxisPlan& plan, double2* spec, int TW,
-                                           int bx, int by, int bz, double2* sm) {
+                                           int bx, int by, int bz, double2* sm, const double2* tw_pre = nullptr) {
   const int kz0 = bx * TW;
   const int y = by, i = bz;
   const int Nx = g.Nx;
@@ -148,7 +149,7 @@ __device__ __forceinline__ void xpass_body(const Geo& g, const AxisPlan& plan, d
                : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  double2* R = fft_smem(A, B, nl, 1, nl, plan, -1, true, sm + 2 * Nx * nl);
+  double2* R = fft_smem(A, B, nl, 1, nl, plan, -1, true, sm + 2 * Nx * nl, tw_pre);
   double2* S = (R == A) ? B : A;
   // Bhat_ij = sum_l Ahat_il ghat_lj, ghat = xi (x) xi / |xi|^2 (projection.cpp:87-104,139-152)
   const int yg = g.y0 + y;
@@ -185,7 +186,7 @@ __device__ __forceinline__ void xpass_body(const Geo& g, const AxisPlan& plan, d
     }  // Nyquist in IdentityEquilibrium mode: ghat = I, keep v
   }
   __syncthreads();
-  R = fft_smem(R, S, nl, 1, nl, plan, +1, true, sm + 2 * Nx * nl);
+  R = fft_smem(R, S, nl, 1, nl, plan, +1, true, sm + 2 * Nx * nl, tw_pre);
   for (int w = threadIdx.x; w < Nx * nl; w += blockDim.x) {
     const int t = w % TW, j = (w / TW) % TD, e = w / nl;
     const int kz = kz0 + t;
@@ -210,7 +211,8 @@ __global__ void __launch_bounds__(256) k_xpass(Geo g, AxisPlan plan, double2* sp
 template <int TD>
 __device__ __forceinline__ void zinv_body(const Geo& g, const AxisPlan& plan, const double2* __restrict__ twN,
                                           const double2* __restrict__ spec, double* __restrict__ out, int G,
-                                          int ls, double scale, const EpiArgs& epi, int bx, double2* sm) {
+                                          int ls, double scale, const EpiArgs& epi, int bx, double2* sm,
+                                          const double2* tw_pre = nullptr) {
   constexpr int NC = TD * TD;
   const int nxy = g.Nx * g.Ny;
   const int L0 = bx * G;
@@ -247,7 +249,7 @@ __device__ __forceinline__ void zinv_body(const Geo& g, const AxisPlan& plan, co
     B[(c * G + gi) * ls + k] = Z;
   }
   __syncthreads();
-  double2* R = fft_smem(B, A, NC * G, ls, 1, plan, +1, false, sm + 2 * NC * G * ls);
+  double2* R = fft_smem(B, A, NC * G, ls, 1, plan, +1, false, sm + 2 * NC * G * ls, tw_pre);
   double dot = 0.0;
   for (int w = threadIdx.x; w < NC * Gb * g.Nz; w += blockDim.x) {
     const int line = w / g.Nz, z = w - line * g.Nz;
@@ -309,6 +311,7 @@ struct CgSmallArgs {
   double* rr_part;
   double* scal;
   int G, ls, tw_y, tw_x, nz_items, ny_items, nx_items, ny_gx, nx_gx;
+  int tw_off;  // dynamic-smem offset (double2) of the staged twiddle tables
   double rr0, thr, scale;
   int64_t cap;
   unsigned long long* tdbg;  // optional: block-0 phase timestamps of the first 8 iterations (FM_CG_SMALL_TIMING)
@@ -341,6 +344,14 @@ __global__ void __launch_bounds__(256) k_cg_small(CgSmallArgs a) {
   double rr = a.rr0, rr_new = 0.0, pap = 0.0, beta = 0.0;
   int64_t it = 0;
   int exit_kind = 3;  // 1: !(pAp > 0), 2: converged, 3: cap
+  // the three axes' twiddle tables, staged once for the whole CG loop
+  double2* twz = sm + a.tw_off;
+  double2* twy = twz + a.pz.N;
+  double2* twx = twy + a.py.N;
+  for (int i = threadIdx.x; i < a.pz.N; i += blockDim.x) twz[i] = __ldg(&a.pz.tw[i]);
+  for (int i = threadIdx.x; i < a.py.N; i += blockDim.x) twy[i] = __ldg(&a.py.tw[i]);
+  for (int i = threadIdx.x; i < a.px.N; i += blockDim.x) twx[i] = __ldg(&a.px.tw[i]);
+  __syncthreads();
   auto mark = [&](int k) {
     if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0 && it <= 8) a.tdbg[(it - 1) * 8 + k] = gtimer();
   };
@@ -356,7 +367,7 @@ __global__ void __launch_bounds__(256) k_cg_small(CgSmallArgs a) {
     pa.beta = &ssc[S_BETA];
     pa.pap_partial = a.pap_part;
     for (int w = blockIdx.x; w < a.nz_items; w += gridDim.x)
-      zfwd_body<3, PRO, true, true>(a.gz, a.pz, a.twN, pa, a.spec, a.G, a.ls, w, sm);
+      zfwd_body<3, PRO, true, true>(a.gz, a.pz, a.twN, pa, a.spec, a.G, a.ls, w, sm, twz);
     mark(1);
     grid.sync();
     mark(2);
@@ -372,19 +383,19 @@ __global__ void __launch_bounds__(256) k_cg_small(CgSmallArgs a) {
     __syncthreads();
     for (int w = blockIdx.x; w < a.ny_items; w += gridDim.x) {
       const int bx = w % a.ny_gx, rest = w / a.ny_gx;
-      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, -1, bx, rest % a.gz.Nx, rest / a.gz.Nx, sm);
+      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, -1, bx, rest % a.gz.Nx, rest / a.gz.Nx, sm, twy);
     }
     grid.sync();
     mark(3);
     for (int w = blockIdx.x; w < a.nx_items; w += gridDim.x) {
       const int bx = w % a.nx_gx, rest = w / a.nx_gx;
-      xpass_body<3>(a.gx, a.px, a.spec, a.tw_x, bx, rest % a.gx.Ny, rest / a.gx.Ny, sm);
+      xpass_body<3>(a.gx, a.px, a.spec, a.tw_x, bx, rest % a.gx.Ny, rest / a.gx.Ny, sm, twx);
     }
     grid.sync();
     mark(4);
     for (int w = blockIdx.x; w < a.ny_items; w += gridDim.x) {
       const int bx = w % a.ny_gx, rest = w / a.ny_gx;
-      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, +1, bx, rest % a.gz.Nx, rest / a.gz.Nx, sm);
+      ypass_body(a.gz, a.py, a.spec, a.spec, a.tw_y, +1, bx, rest % a.gz.Nx, rest / a.gz.Nx, sm, twy);
     }
     grid.sync();
     mark(5);
@@ -395,7 +406,7 @@ __global__ void __launch_bounds__(256) k_cg_small(CgSmallArgs a) {
     e.scal = ssc;
     e.partial = a.rr_part;
     for (int w = blockIdx.x; w < a.nz_items; w += gridDim.x)
-      zinv_body<3>(a.gz, a.pz, a.twN, a.spec, nullptr, a.G, a.ls, a.scale, e, w, sm);
+      zinv_body<3>(a.gz, a.pz, a.twN, a.spec, nullptr, a.G, a.ls, a.scale, e, w, sm, twz);
     mark(6);
     grid.sync();
     rr_new = items_sum(a.rr_part, a.nz_items, &ssc[8]);
@@ -726,7 +737,9 @@ int cg_small_run(fm_ctx* ctx, const ProArgs& op, double* x, double* r, double* p
     cudaMemsetAsync(tdbg, 0, 64 * sizeof(unsigned long long), ctx->stream);
     a.tdbg = tdbg;
   }
-  const size_t smem = std::max({L.smem, size_t(2 * twy + 1) * gz.Ny * 16, size_t(2 * 3 * twx + 1) * gx.Nx * 16});
+  const size_t body = std::max({L.smem, size_t(2 * twy + 1) * gz.Ny * 16, size_t(2 * 3 * twx + 1) * gx.Nx * 16});
+  a.tw_off = int((body + 15) / 16);
+  const size_t smem = size_t(a.tw_off + a.pz.N + a.py.N + a.px.N) * 16;
   const int items = std::max({a.nz_items, a.ny_items, a.nx_items});
   if (smem > size_t(64 * 1024) || a.nz_items > ctx->epi_cap) return FM_E_UNSUPPORTED;
   int st = FM_E_UNSUPPORTED;
