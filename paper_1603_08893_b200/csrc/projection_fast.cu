@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
   // (Rolled loops keep one copy of each transform: the register budget.)
 #pragma unroll 1
   for (int q = 0; q < 2; ++q) {
-    asm volatile("cp.async.wait_group 0;\n" ::);  // q = 0 waits for tile 1 as well (it lands with tile 0)
+    if (q == 0) asm volatile("cp.async.wait_group 1;\n" ::);  // tile 0 (tile 1 may still be in flight)
+    else asm volatile("cp.async.wait_group 0;\n" ::);          // tiles 1 and 2
     __syncthreads();
     if (q == 0) {
 #pragma unroll
