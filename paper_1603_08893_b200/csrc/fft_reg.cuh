@@ -101,8 +101,9 @@ __device__ __forceinline__ int xaddr(int p, int LS) {
 }
 
 // One Stockham stage of radix R (Ns = product of earlier radices).
-// tw: table W_N^e, e < N (global or shared).  sml = sm + line offset.
-template <int N, int E, int R, int Ns, int SIGN, int SW = 0>
+// tw: table W_N^e, e < N (global or shared), or, with TS > 1, a table of
+// W_{N TS} read at stride TS.  sml = sm + line offset.
+template <int N, int E, int R, int Ns, int SIGN, int SW = 0, int TS = 1>
 __device__ __forceinline__ void stage(double2 (&v)[E], double2* sml, int LS, int t,
                                       const double2* __restrict__ tw) {
   constexpr int T = N / E;
@@ -119,7 +120,7 @@ __device__ __forceinline__ void stage(double2 (&v)[E], double2* sml, int LS, int
     for (int r = 0; r < R; ++r) a[r] = v[b + r * B];
     if constexpr (Ns > 1) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) a[r] = tw_mul(a[r], __ldg(&tw[jm * r * (N / (Ns * R))]), SIGN);
+      for (int r = 1; r < R; ++r) a[r] = tw_mul(a[r], __ldg(&tw[jm * r * (N / (Ns * R)) * TS]), SIGN);
     }
     Dft<R, SIGN>::run(a);
     if constexpr (last) {
@@ -140,26 +141,27 @@ __device__ __forceinline__ void stage(double2 (&v)[E], double2* sml, int LS, int
   }
 }
 
-template <int N, int E, int Ns, int SIGN, int SW>
+template <int N, int E, int Ns, int SIGN, int SW, int TS = 1>
 struct Stages {
   static constexpr int R = (N / Ns >= E) ? E : N / Ns;
   __device__ __forceinline__ static void run(double2 (&v)[E], double2* sml, int LS, int t,
                                              const double2* __restrict__ tw) {
-    stage<N, E, R, Ns, SIGN, SW>(v, sml, LS, t, tw);
-    Stages<N, E, Ns * R, SIGN, SW>::run(v, sml, LS, t, tw);
+    stage<N, E, R, Ns, SIGN, SW, TS>(v, sml, LS, t, tw);
+    Stages<N, E, Ns * R, SIGN, SW, TS>::run(v, sml, LS, t, tw);
   }
 };
-template <int N, int E, int SIGN, int SW>
-struct Stages<N, E, N, SIGN, SW> {
+template <int N, int E, int SIGN, int SW, int TS>
+struct Stages<N, E, N, SIGN, SW, TS> {
   __device__ __forceinline__ static void run(double2 (&)[E], double2*, int, int, const double2*) {}
 };
 
 // Full N-point transform of the register-resident line (unnormalised).
-template <int N, int E, int SIGN>
+// TS > 1: tw is the W_{N TS} table (a longer line's), read at stride TS.
+template <int N, int E, int SIGN, int TS = 1>
 __device__ __forceinline__ void fft(double2 (&v)[E], double2* sml, int LS, int t,
                                     const double2* __restrict__ tw) {
   static_assert(N % E == 0, "E must divide N");
-  Stages<N, E, 1, SIGN, 0>::run(v, sml, LS, t, tw);
+  Stages<N, E, 1, SIGN, 0, TS>::run(v, sml, LS, t, tw);
 }
 
 constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }

@@ -317,6 +317,142 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
   }
 }
 
+// x pass for N = 2H (512 = 2 x 256), scalar-accumulating like k_x_fast4, with
+// the outermost radix-2 step done across a lane pair instead of through
+// shared memory.  Decimation in time: X[k] = E[k] + W_N^k O[k] and
+// X[k + H] = E[k] - W_N^k O[k], E and O the H-point transforms of the even and
+// odd rows.  The T = N/E threads of a line are two groups of TH = H/E: group
+// h = 0 transforms the even rows, h = 1 the odd ones (each an H-point
+// register FFT with ONE shared-memory exchange at H = 256, where the N-point
+// transform needs two), then the lane pair (lanes TW apart) swaps half its
+// values with one shuffle per element and each lane forms both outputs of its
+// half of the butterflies.  Spectrum slot s of lane (t, h) then holds
+// frequency kslot(t, h, s) below; every frequency-domain step of this pass is
+// pointwise, so the permuted order is used as is, and the inverse transforms
+// run the mirror image (decimation in frequency: the radix-2 split by
+// shuffle, then two H-point inverse FFTs whose outputs are rows 2n and
+// 2n + 1).
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int mask) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
+}
+template <int TH, int H>
+__device__ __forceinline__ int kslot(int t, int h, int s) {  // frequency held in slot s (E = 16)
+  return t + TH * ((s & 7) + 8 * h) + H * ((s >> 3) ^ h);
+}
+// Forward radix-2 DIT combine of the lane pair (E = 16): lane h = 0 holds
+// E[t + TH m], h = 1 holds O[t + TH m]; h = 0 keeps slots m < 8 (gives
+// E[m + 8]), h = 1 keeps m >= 8 (gives O[m]); the kept slot ends as X[k],
+// the other as X[k + H] (kslot).  tw: the W_N table, N = 2H.
+template <int TH, int TW>
+__device__ __forceinline__ void pair_dit(double2 (&v)[16], int t, int h, const double2* __restrict__ tw) {
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const double2 got = shfl_xor2(h == 0 ? v[m + 8] : v[m], TW);
+    const double2 e = h == 0 ? v[m] : got, o = h == 0 ? got : v[m + 8];
+    const int k = t + TH * (m + 8 * h);
+    const double2 wo = reg::tw_mul(o, __ldg(&tw[k]), -1);
+    const double2 lo = make_double2(e.x + wo.x, e.y + wo.y), hi = make_double2(e.x - wo.x, e.y - wo.y);
+    v[m] = h == 0 ? lo : hi;
+    v[m + 8] = h == 0 ? hi : lo;
+  }
+}
+// Inverse radix-2 DIF split (the mirror image): from the kslot order, the
+// sums X[k] + X[k + H] go to lane h = 0 (even output rows), the differences
+// (X[k] - X[k + H]) W_N^-k to h = 1, each as slot m of k = t + TH m.
+template <int TH, int TW>
+__device__ __forceinline__ void pair_dif(double2 (&v)[16], int t, int h, const double2* __restrict__ tw) {
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const double2 xa = h == 0 ? v[m] : v[m + 8], xb = h == 0 ? v[m + 8] : v[m];  // X[k], X[k + H]
+    const int k = t + TH * (m + 8 * h);
+    const double2 sum = make_double2(xa.x + xb.x, xa.y + xb.y);
+    const double2 dif = reg::tw_mul(make_double2(xa.x - xb.x, xa.y - xb.y), __ldg(&tw[k]), +1);
+    const double2 got = shfl_xor2(h == 0 ? dif : sum, TW);
+    v[m] = h == 0 ? sum : got;
+    v[m + 8] = h == 0 ? got : dif;
+  }
+}
+// The same 512-point x pass without tile staging, shaped like the y pass:
+// 8-column tiles (one 128-byte segment per row and component, where the
+// staged pass's 64 KB double buffer only allows 4 columns = 64-byte
+// segments), every lane loading its rows straight from HBM into registers and
+// storing its results straight from registers; shared memory is only the
+// one H-point exchange buffer (64 KB), 2 CTAs x 256 threads per SM.  The
+// forward transform of B = xi_y A_1 + xi_z A_2 runs first, so the
+// accumulator is not live while A_1 and A_2 are loaded.
+template <int N, int TW, bool RT = false>
+__global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* __restrict__ tw,
+                                                         double2* __restrict__ spec) {
+  constexpr int E = 16, H = N / 2, TH = H / E;
+  static_assert(TH == 16 && TW * 2 <= 32, "lane pairs inside a warp");
+  extern __shared__ double2 sm[];
+  const int l = threadIdx.x % TW, u = threadIdx.x / TW;
+  const int h = u & 1, t = u >> 1;
+  const int kz = blockIdx.x * TW + l;
+  const int y = blockIdx.y, i = blockIdx.z;
+  const int64_t xstride = int64_t(g.Ny) * g.nzh;
+  // rows 2 (t + TH m) + h of this lane: one base pointer, 32-bit element offsets
+  // (the launcher checks 3 N xstride < 2^31)
+  const int rs = 2 * TH * int(xstride);
+  double2* const row0 = spec + int64_t(i * 3) * N * xstride + (2 * t + h) * xstride + int64_t(y) * g.nzh + kz;
+  const int cs = N * int(xstride);  // component stride
+  const int yg = g.y0 + y;
+  const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
+  const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+  const double xiy = qy * g.invL[1], xiz = qz * g.invL[2];
+  double2* const X = sm + l + TW * h;  // sub-line of the H-point exchange (2 TW per CTA, interleaved)
+  double2 s[E], v[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = row0[cs + m * rs];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const double2 a2 = row0[2 * cs + m * rs];
+    v[m] = make_double2(fma(v[m].x, xiy, a2.x * xiz), fma(v[m].y, xiy, a2.y * xiz));
+  }
+  reg::fft<H, E, -1, 2>(v, X, 2 * TW, t, tw);
+  pair_dit<TH, TW>(v, t, h, tw);
+#pragma unroll
+  for (int m = 0; m < E; ++m) s[m] = v[m];
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = row0[m * rs];
+  reg::fft<H, E, -1, 2>(v, X, 2 * TW, t, tw);
+  pair_dit<TH, TW>(v, t, h, tw);
+  // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int kx = kslot<TH, H>(t, h, m);
+    const double xix = freq_of(kx, N) * g.invL[0];
+    const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
+    const bool zero = norm2 == 0.0 || nyq_yz || kx == N / 2;
+    const double inv = zero ? 0.0 : 1.0 / norm2;
+    s[m] = make_double2((v[m].x * xix + s[m].x) * inv, (v[m].y * xix + s[m].y) * inv);
+  }
+  // Bhat_i0 = IFFT(s xi_x); Bhat_i1 = xi_y IFFT(s), Bhat_i2 = xi_z IFFT(s)
+#pragma unroll 1
+  for (int q = 0; q < 2; ++q) {
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const double f = q == 0 ? freq_of(kslot<TH, H>(t, h, m), N) * g.invL[0] : 1.0;
+      v[m] = make_double2(s[m].x * f, s[m].y * f);
+    }
+    pair_dif<TH, TW>(v, t, h, tw);
+    reg::fft<H, E, +1, 2>(v, X, 2 * TW, t, tw);
+#pragma unroll 1
+    for (int j = q; j < (q == 0 ? 1 : 3); ++j) {
+      const double f = j == 0 ? 1.0 : (j == 1 ? xiy : xiz);
+      if constexpr (!RT) {
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+          row0[j * cs + m * rs] = make_double2(v[m].x * f, v[m].y * f);
+      } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m)
+          store_xb(g, nullptr, i * 3 + j, 2 * (t + TH * m) + h, y, kz, make_double2(v[m].x * f, v[m].y * f));
+      }
+    }
+  }
+}
+
 // r2c / c2r untangling pairs element k of a z-line with M - k.  With the
 // line's elements spread as k = t + T m over its T lanes (T | 32), the partner
 // of (t, m) sits in lane (T - t) mod T of the same warp:
@@ -928,6 +1064,24 @@ void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
   g.P > 1 ? x4_rt<N, TW, E, true>(ctx, g, spec) : x4_rt<N, TW, E, false>(ctx, g, spec);
 }
 
+template <int N, int TW, bool RT>
+void xd_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
+  const size_t smem = size_t(N) * TW * 16;
+  static bool a = (allow(k_x_direct<N, TW, RT>, smem), true);
+  (void)a;
+  const dim3 grid(ctx->nzh / TW, g.Ny, 3);
+  k_x_direct<N, TW, RT><<<grid, TW * 32, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+}
+
+// FM_XDIRECT=0: the 512-point x pass falls back to the staged k_x_fast4
+int xdirect_mode() {
+  static int v = [] {
+    const char* e = getenv("FM_XDIRECT");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int N>
 bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   constexpr int TW = tw_x(N);
@@ -940,7 +1094,15 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   // against 120 ms for the registers-only pass)
   const bool zc = ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE;
   constexpr int X4TW = N >= 512 ? 4 : 8;
-  if (zc && N >= 64 && ctx->nzh % X4TW == 0) {  // (8 elements/thread at 512: 6.5 vs 5.9 ms)
+  bool done = false;
+  if constexpr (N == 512) {  // 5.3 vs 6.0 ms at 512^3 (k_x_fast4, 4-column tiles)
+    if (zc && ctx->nzh % 8 == 0 && xdirect_mode() && 3 * int64_t(N) * g.Ny * ctx->nzh < (int64_t(1) << 31)) {
+      g.P > 1 ? xd_rt<N, 8, true>(ctx, g, spec) : xd_rt<N, 8, false>(ctx, g, spec);
+      done = true;
+    }
+  }
+  if (done) {
+  } else if (zc && N >= 64 && ctx->nzh % X4TW == 0) {  // (8 elements/thread at 512: 6.5 vs 5.9 ms)
     x4_go<N, X4TW, e_line(N)>(ctx, g, spec);
   } else if (N <= 512 && ctx->nzh % 8 == 0 && !(zc && N < 64)) {
     x3_go<N, 8, e_line(N)>(ctx, g, spec);

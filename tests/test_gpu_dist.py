@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("pts,P", [((64, 64, 64), 2), ((64, 64, 64), 8), ((32, 32, 32), 4),
                                    ((128, 64, 32), 8), ((12, 10, 14), 2), ((16, 24, 9), 4),
                                    ((256, 256, 32), 8),
-                                   # long routed x lines (4-column x tiles) and y lines at 512 / 1024
+                                   # long routed x lines (512: direct lane-pair pass, 1024: 4-column tiles) and y lines
                                    ((512, 32, 16), 4), ((1024, 16, 32), 2), ((32, 512, 16), 2),
                                    ((16, 1024, 32), 4)])
 def test_virtual_ranks_bitwise_equal(pts, P):

@@ -28,6 +28,7 @@ CASES = [
     ((128, 64, 32), None, 3, 0),
     ((32, 256, 64), (2.0, 1.0, 0.5), 3, 0),
     ((512, 32, 32), None, 3, 0),
+    ((512, 8, 16), (1.0, 0.5, 2.0), 3, 0),
     ((1024, 16, 32), None, 3, 0),
     ((32, 1024, 16), None, 3, 0),
     ((16, 16, 1024), None, 3, 0),
