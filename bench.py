@@ -42,8 +42,9 @@ sys.path.insert(0, ROOT)
 PASS_BYTES = [648 + 72 + 72, 144, 144, 144, 144]  # z-fwd(+K4), y-fwd, x+ghat, y-inv, z-inv
 MATVEC_BYTES = sum(PASS_BYTES)  # 1368 = B_mv
 PASS_NAMES = ["z_fwd_k4", "y_fwd", "x_ghat", "y_inv", "z_inv"]
-# matrix-free SVK action: pass 1 reads F, dF, lambda, mu instead of K4 and dF
-PASS_BYTES_MF = [72 + 72 + 16 + 72, 144, 144, 144, 144]  # 808 B/voxel
+# matrix-free SVK action: pass 1 reads F, dF and a 1-byte phase label (the
+# two-phase (lambda, mu) table, ProArgs::lab) instead of K4 and dF
+PASS_BYTES_MF = [72 + 72 + 1 + 72, 144, 144, 144, 144]  # 793 B/voxel
 PASS_NAMES_MF = ["z_fwd_svk", "y_fwd", "x_ghat", "y_inv", "z_inv"]
 
 
@@ -303,7 +304,7 @@ def main():
     ms_k4, roof_k4, _, _ = time_variant(False)
     ms_step, roofline, launches, clocks = time_variant(True)
     value = jobs_n / (ms_step * 1e-3)
-    roofline["model"] = ("matrix-free SVK tangent action in pass 1 (808 B/voxel: F 72 + dF 72 + lambda,mu 16 "
+    roofline["model"] = ("matrix-free SVK tangent action in pass 1 (793 B/voxel: F 72 + dF 72 + phase label 1 "
                          "+ 4 x 144 + 72); frac_of_canonical_1368 compares with the K4 form")
     k4 = {"value": jobs_n / (ms_k4 * 1e-3), "ms_per_step": ms_k4, "roofline": roof_k4,
           "what": "same operator with K4 materialised (reference form, 1368 B/voxel)"}

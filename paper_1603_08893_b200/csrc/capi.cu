@@ -2,7 +2,9 @@
 // Every entry point validates its arguments the way the reference does
 // (std::invalid_argument -> FM_E_INVALID) and returns an fm_status; there
 // is no CPU fallback anywhere behind it.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -472,6 +474,51 @@ int fm_cg_solve(fm_ctx* ctx, const fm_field* K, const fm_field* rhs, double eta_
   return cg_run_k4(ctx, K->d, rhs->d, eta_cg, max_cg, x->d, iterations, rel_residual);
 }
 
+// Matrix-free SVK: when the per-voxel (lambda, mu) pairs take at most 256
+// distinct values (a phase microstructure, bind_parameters,
+// microstructure.cpp:176-203), keep a 1-byte label per voxel and the pair
+// table for the pipelined pass 1 (ProArgs::lab).  Pairs are compared bit for
+// bit, so the table holds exactly the doubles the fields hold.
+// FM_PHASE_LABELS=0 keeps the two per-voxel fields in pass 1.
+static int build_phase_labels(fm_ctx* ctx, fm_model* m, const double* lambda, const double* mu) {
+  static const int env = [] {
+    const char* e = getenv("FM_PHASE_LABELS");
+    return e ? atoi(e) : 1;
+  }();
+  if (!env) return FM_OK;
+  std::vector<uint8_t> lab(size_t(ctx->n));
+  std::vector<uint64_t> tl, tm;
+  int last = -1;
+  for (int64_t i = 0; i < ctx->n; ++i) {
+    uint64_t a, b;
+    std::memcpy(&a, lambda + i, 8);
+    std::memcpy(&b, mu + i, 8);
+    if (last < 0 || tl[last] != a || tm[last] != b) {
+      last = -1;
+      for (size_t k = 0; k < tl.size(); ++k)
+        if (tl[k] == a && tm[k] == b) {
+          last = int(k);
+          break;
+        }
+      if (last < 0) {
+        if (tl.size() == 256) return FM_OK;  // too many phases: per-voxel fields
+        tl.push_back(a);
+        tm.push_back(b);
+        last = int(tl.size()) - 1;
+      }
+    }
+    lab[size_t(i)] = uint8_t(last);
+  }
+  std::vector<uint64_t> tab(512, 0);
+  std::copy(tl.begin(), tl.end(), tab.begin());
+  std::copy(tm.begin(), tm.end(), tab.begin() + 256);
+  FM_CUDA(ctx, cudaMalloc(&m->lab, size_t(ctx->n) + 16));
+  FM_CUDA(ctx, cudaMalloc(&m->ptab, 512 * sizeof(double)));
+  FM_CUDA(ctx, cudaMemcpy(m->lab, lab.data(), size_t(ctx->n), cudaMemcpyHostToDevice));
+  FM_CUDA(ctx, cudaMemcpy(m->ptab, tab.data(), 512 * sizeof(double), cudaMemcpyHostToDevice));
+  return FM_OK;
+}
+
 int fm_model_create_hyper(fm_ctx* ctx, const double* lambda, const double* mu, int matrix_free,
                           fm_model** out) {
   if (!ctx || !lambda || !mu || !out) return FM_E_INVALID;
@@ -485,6 +532,7 @@ int fm_model_create_hyper(fm_ctx* ctx, const double* lambda, const double* mu, i
                                : ensure_field(ctx, m->K, ctx->ncomp * ctx->ncomp);
   if (!st) st = fm_field_upload(ctx, &m->lambda, lambda, ctx->n);
   if (!st) st = fm_field_upload(ctx, &m->mu, mu, ctx->n);
+  if (!st && m->matrix_free) st = build_phase_labels(ctx, m, lambda, mu);
   if (st) {
     fm_model_destroy(ctx, m);
     return st;
@@ -536,6 +584,8 @@ int fm_model_destroy(fm_ctx* ctx, fm_model* m) {
   for (fm_field* f : {&m->lambda, &m->mu, &m->tau_y0, &m->hard, &m->K, &m->Kc, &m->F_eval, &m->be_c,
                       &m->epsp_c, &m->be_t, &m->epsp_t, &m->f_old})
     release_field(*f);
+  if (m->lab) cudaFree(m->lab);
+  if (m->ptab) cudaFree(m->ptab);
   delete m;
   return FM_OK;
 }

@@ -68,6 +68,8 @@ struct fm_model {
   int compact = 0;              // Simo: keep the 45-slab compact tangent instead of K4
   fm_field Kc;                  // compact J2 tangent (45n)
   fm_field F_eval;              // F at the last evaluate (matrix-free SVK action)
+  uint8_t* lab = nullptr;       // matrix-free SVK: phase labels + (lambda, mu) table (ProArgs::lab)
+  double* ptab = nullptr;
   fm_field be_c, epsp_c, be_t, epsp_t, f_old;  // Simo history
 };
 
@@ -161,6 +163,11 @@ struct ProArgs {
   const double* F = nullptr;   // PRO_SVK
   const double* lam = nullptr; // PRO_SVK
   const double* mu = nullptr;  // PRO_SVK
+  // PRO_SVK with at most 256 distinct (lambda, mu) pairs: a 1-byte phase label
+  // per voxel and the pair table (lambda at [k], mu at [256 + k]) replace the
+  // two per-voxel fields in the pipelined pass 1 (16 -> 1 B/voxel)
+  const uint8_t* lab = nullptr;
+  const double* ptab = nullptr;
   // CG direction update fused into the prologue (solver.cpp:51-55):
   // p = beta p + r is formed per voxel, written back to p and used as dF.
   const double* r = nullptr;

@@ -578,6 +578,12 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
 #define FM_PIPE_COPY_MINB 5
 #endif
 constexpr int kPipeCopyMinB = FM_PIPE_COPY_MINB;
+#ifndef FM_PIPE_LAB_MINB
+#define FM_PIPE_LAB_MINB 3
+#endif
+// SVK with phase labels: 4 CTAs/SM would fit the shared memory, but the
+// 96-register budget spills (256^3 pass 1: 0.83 ms at 4, 0.69 ms at 3 CTAs/SM)
+constexpr int kPipeLabMinB = FM_PIPE_LAB_MINB;
 
 template <int M>
 struct ZPipe {
@@ -586,21 +592,24 @@ struct ZPipe {
   static constexpr int THREADS = 9 * T;
   static constexpr size_t FFT_SM = size_t(M) * LSP * 16;
 };
-template <int PRO, bool DIR, bool XUPD = false>
+// fp64 input chunks per line; LAB: the lambda and mu chunks replaced by one
+// N-byte phase-label chunk (ProArgs::lab)
+template <int PRO, bool DIR, bool XUPD = false, bool LAB = false>
 constexpr int pipe_chunks() {
-  return PRO == PRO_COPY ? 9 : (DIR ? (XUPD ? 38 : 29) : 20);
+  return (PRO == PRO_COPY ? 9 : (DIR ? (XUPD ? 38 : 29) : 20)) - (LAB ? 2 : 0);
 }
-template <int M, int PRO, bool DIR, bool XUPD = false>
+template <int M, int PRO, bool DIR, bool XUPD = false, bool LAB = false>
 constexpr size_t pipe_smem() {
-  return ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR, XUPD>()) * 2 * M * 8;
+  return ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR, XUPD, LAB>()) * 2 * M * 8 + (LAB ? size_t(2 * M) : 0);
 }
 
-template <int M, int PRO, bool DIR, int MINB, bool PAP = false, bool XUPD = false>
+template <int M, int PRO, bool DIR, int MINB, bool PAP = false, bool XUPD = false, bool LAB = false>
 __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, const double2* __restrict__ twM,
                                                                const double2* __restrict__ twN, ProArgs pa,
                                                                double2* __restrict__ spec) {
   using S = ZPipe<M>;
-  constexpr int N = 2 * M, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR, XUPD>();
+  constexpr int N = 2 * M, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR, XUPD, LAB>();
+  static_assert(!LAB || PRO == PRO_SVK, "phase labels replace the SVK lambda / mu chunks");
   constexpr int SW = reg::ilog2(E);  // line-major swizzled line buffer (reg::fft_swz)
   static_assert(32 % T == 0, "a component line must not straddle a warp");
   static_assert(!XUPD || (DIR && PRO == PRO_SVK), "x update rides on the SVK direction prologue");
@@ -611,7 +620,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   const int64_t n = g.n;
   auto issue = [&](int L) {
     const int64_t node0 = g.roff + int64_t(L) * N;
-    bulk::mbar_expect_tx(&bar, NCH * N * 8);
+    bulk::mbar_expect_tx(&bar, NCH * N * 8 + (LAB ? N : 0));
     int q = 0;
     auto cp = [&](const double* base) { bulk::g2s(stage + (q++) * N, base + node0, N * 8, &bar); };
     if constexpr (PRO == PRO_COPY) {
@@ -626,8 +635,12 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
         for (int c = 0; c < 9; ++c) cp(pa.A + c * n);
       }
       for (int c = 0; c < 9; ++c) cp(pa.F + c * n);
-      cp(pa.lam);
-      cp(pa.mu);
+      if constexpr (LAB) {
+        bulk::g2s(stage + NCH * N, pa.lab + node0, N, &bar);
+      } else {
+        cp(pa.lam);
+        cp(pa.mu);
+      }
     }
   };
   if (threadIdx.x == 0) bulk::mbar_init(&bar, 1);
@@ -683,8 +696,15 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
           f0[c] = a.x;
           f1[c] = a.y;
         }
-        const double2 lm = *reinterpret_cast<const double2*>(stage + (FB + 9) * N + 2 * m);
-        const double2 mu = *reinterpret_cast<const double2*>(stage + (FB + 10) * N + 2 * m);
+        double2 lm, mu;
+        if constexpr (LAB) {
+          const uchar2 ph = *reinterpret_cast<const uchar2*>(reinterpret_cast<const uint8_t*>(stage + NCH * N) + 2 * m);
+          lm = make_double2(__ldg(pa.ptab + ph.x), __ldg(pa.ptab + ph.y));
+          mu = make_double2(__ldg(pa.ptab + 256 + ph.x), __ldg(pa.ptab + 256 + ph.y));
+        } else {
+          lm = *reinterpret_cast<const double2*>(stage + (FB + 9) * N + 2 * m);
+          mu = *reinterpret_cast<const double2*>(stage + (FB + 10) * N + 2 * m);
+        }
         svk_action<3>(f0, d0, lm.x, mu.x, v0);
         svk_action<3>(f1, d1, lm.y, mu.y, v1);
         if constexpr (PAP) {
@@ -1142,22 +1162,22 @@ int zpipe_mode() {  // FM_ZPIPE=0 disables the pipelined z-forward pass
 }
 
 // 3 CTAs/SM register budget (measured best of 1..4 and single-voxel variants)
-template <int PRO, int M>
+template <int PRO, int M, bool LAB = false, bool DIR = false>
 constexpr int pipe_minb() {  // copy: fewer registers suffice up to M = 128 (512^3: 5 CTAs/SM is slower)
-  return (PRO == PRO_COPY && M <= 128) ? kPipeCopyMinB : 3;
+  return (PRO == PRO_COPY && M <= 128) ? kPipeCopyMinB : (LAB && !DIR && M <= 128 ? kPipeLabMinB : 3);
 }
 
-template <int M, int PRO, bool DIR, bool PAP, bool XUPD = false>
+template <int M, int PRO, bool DIR, bool PAP, bool XUPD = false, bool LAB = false>
 bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
-  constexpr int MB = pipe_minb<PRO, M>();
-  constexpr size_t smem = pipe_smem<M, PRO, DIR, XUPD>();
+  constexpr int MB = pipe_minb<PRO, M, LAB, DIR>();
+  constexpr size_t smem = pipe_smem<M, PRO, DIR, XUPD, LAB>();
   if constexpr (smem > 100 * 1024 || M < 16) {  // one CTA per SM does not pay (512^3: 2x slower)
     return false;
   } else {
     static const int per_sm = [] {
-      allow(k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD>, smem);
+      allow(k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB>, smem);
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB>,
                                                     ZPipe<M>::THREADS, smem);
       cudaGetLastError();
       return b > 0 ? b : 1;
@@ -1167,7 +1187,7 @@ bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int nxy = g.Nx * g.Ny;
     const int grid = std::min(nxy, std::max(sms, 1) * per_sm);
-    k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD>
+    k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB>
         <<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
     ctx->zf_partials = grid;
     return true;
@@ -1177,16 +1197,23 @@ bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
 template <int M, int PRO, bool PAP>
 void zf_kind(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, bool dir, int* st) {
   if constexpr (PRO == PRO_SVK) {
+    const bool lab = pa.lab != nullptr;
     if (pa.x) {  // fused CG x update: only the pipelined kernel carries it (cg_xupd_supported)
-      if (dir && PAP && zpipe_go<M, PRO, true, PAP, true>(ctx, g, pa, spec)) {
+      if (dir && PAP && (lab ? zpipe_go<M, PRO, true, PAP, true, true>(ctx, g, pa, spec)
+                             : zpipe_go<M, PRO, true, PAP, true>(ctx, g, pa, spec))) {
         *st = launched(ctx, "k_zf_pipe");
       } else {
         *st = set_error(ctx, FM_E_UNSUPPORTED, "fused x update without the pipelined z-forward pass");
       }
       return;
     }
-    if (zpipe_mode() && (dir ? zpipe_go<M, PRO, true, PAP>(ctx, g, pa, spec)
-                             : zpipe_go<M, PRO, false, PAP>(ctx, g, pa, spec))) {
+    bool ok = false;
+    if (zpipe_mode()) {
+      if (lab && dir) ok = zpipe_go<M, PRO, true, PAP, false, true>(ctx, g, pa, spec);
+      else if (lab) ok = zpipe_go<M, PRO, false, PAP, false, true>(ctx, g, pa, spec);
+      else ok = dir ? zpipe_go<M, PRO, true, PAP>(ctx, g, pa, spec) : zpipe_go<M, PRO, false, PAP>(ctx, g, pa, spec);
+    }
+    if (ok) {
       *st = launched(ctx, "k_zf_pipe");
       return;
     }

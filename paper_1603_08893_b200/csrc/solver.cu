@@ -50,6 +50,8 @@ struct Op {
   const double* F = nullptr;
   const double* lam = nullptr;
   const double* mu = nullptr;
+  const uint8_t* lab = nullptr;
+  const double* ptab = nullptr;
 };
 
 int op_apply(fm_ctx* ctx, const Op& op, const double* x, double* out, double scale) {
@@ -60,6 +62,8 @@ int op_apply(fm_ctx* ctx, const Op& op, const double* x, double* out, double sca
   pa.F = op.F;
   pa.lam = op.lam;
   pa.mu = op.mu;
+  pa.lab = op.lab;
+  pa.ptab = op.ptab;
   return projection_run(ctx, pa, out, scale);
 }
 
@@ -74,6 +78,8 @@ int op_apply_cg(fm_ctx* ctx, const Op& op, double* p, const double* r, bool firs
   pa.F = op.F;
   pa.lam = op.lam;
   pa.mu = op.mu;
+  pa.lab = op.lab;
+  pa.ptab = op.ptab;
   if (!first) {
     pa.r = r;
     pa.p = p;
@@ -109,6 +115,8 @@ int op_apply_cg_fused(fm_ctx* ctx, const Op& op, double* p, double* r, bool firs
   pa.F = op.F;
   pa.lam = op.lam;
   pa.mu = op.mu;
+  pa.lab = op.lab;
+  pa.ptab = op.ptab;
   pa.pap_partial = ctx->d_epi2;
   if (!first) {
     pa.r = r;
@@ -153,6 +161,8 @@ Op model_op(fm_model* m) {
     op.F = m->F_eval.d;
     op.lam = m->lambda.d;
     op.mu = m->mu.d;
+    op.lab = m->lab;
+    op.ptab = m->ptab;
   } else if (m->kind == 1 && m->compact) {
     op.kind = PRO_J2C;
     op.K = m->Kc.d;
@@ -185,7 +195,7 @@ int op_apply_cg(fm_ctx* ctx, const Op& op, double* p, const double* r, bool firs
 int cg_loop_graph(fm_ctx* ctx, const Op& op, double* x, int64_t count, int64_t cap, double thr, double bnorm,
                   int32_t* iters, double* rel) {
   const std::vector<const void*> key = {reinterpret_cast<const void*>(intptr_t(op.kind)), op.K, op.F, op.lam, op.mu,
-                                        x, ctx->r.d, ctx->p.d, ctx->Ap.d, reinterpret_cast<const void*>(cap),
+                                        op.lab, x, ctx->r.d, ctx->p.d, ctx->Ap.d, reinterpret_cast<const void*>(cap),
                                         reinterpret_cast<const void*>(intptr_t(ctx->P * 2 + (ctx->virt ? 1 : 0)))};
   k_cg_init<<<1, 1, 0, ctx->stream>>>(ctx->d_scal, thr);
   FM_LAUNCHED(ctx);
@@ -282,6 +292,8 @@ int cg_run(fm_ctx* ctx, const Op& op, const double* b, double eta_cg, int64_t ma
     pa.F = op.F;
     pa.lam = op.lam;
     pa.mu = op.mu;
+    pa.lab = op.lab;
+    pa.ptab = op.ptab;
     const int st = cg_small_run(ctx, pa, x, ctx->r.d, ctx->p.d, cap, eta_cg * bnorm, rr);
     if (st != FM_E_UNSUPPORTED) {
       if (st) return st;

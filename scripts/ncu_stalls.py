@@ -5,7 +5,10 @@ import sys
 from collections import Counter
 
 rows = list(csv.reader(open(sys.argv[1])))
-h, data = rows[1], rows[2:]
+# one section per kernel ("Kernel Name" row, header row, data rows): the first
+end = next((k for k in range(2, len(rows)) if rows[k] and rows[k][0] == "Kernel Name"), len(rows))
+print(rows[0][1][:100])
+h, data = rows[1], rows[2:end]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
 idx = {c: h.index(c) for c in cols}

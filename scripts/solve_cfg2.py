@@ -15,3 +15,4 @@ fbar = np.eye(3); fbar[0, 1] = 0.1
 t = time.perf_counter()
 rep = model.solve_increment(F, fbar)
 print("solve", time.perf_counter() - t, rep["cg_it"], rep["matvecs"], "launches", ctx.launches)
+print("rel_update", rep.get("rel_update"), "F checksum", repr(float(np.sum(F.download()))))

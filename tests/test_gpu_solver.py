@@ -287,3 +287,34 @@ def test_fused_cg_matches_unfused(N, kind, graph):
     assert all(abs(x - y) <= 1 for x, y in zip(a["cg"], b["cg"])), (a["cg"], b["cg"])
     fa, fb = np.array(a["F"]), np.array(b["F"])
     assert np.linalg.norm(fa - fb) <= 1e-9 * np.linalg.norm(fa)
+
+
+@pytest.mark.parametrize("phases", ["two", "per_voxel"])
+def test_svk_phase_labels_match_k4(phases):
+    """Matrix-free SVK action through the pipelined pass 1: with <= 256 distinct
+    (lambda, mu) pairs it reads 1-byte phase labels and the pair table, with
+    per-voxel parameters the two fields; both equal the K4 form (hyperelastic.cpp:55-63)."""
+    pts = (64, 64, 64)
+    n = int(np.prod(pts))
+    if phases == "two":
+        lam, mu, _, _ = M.bind_parameters(M.bernoulli(pts, 0.3, 5), [M.ElasticParams(1.0, 0.3),
+                                                                     M.ElasticParams(10.0, 0.3)])
+    else:
+        rng = np.random.default_rng(6)
+        lam, mu = rng.uniform(0.5, 6.0, n), rng.uniform(0.3, 4.0, n)
+    rng = np.random.default_rng(7)
+    F0 = abi.identity_field(pts, 3) + 0.05 * rng.uniform(-1, 1, 9 * n)
+    dF0 = rng.uniform(-1, 1, 9 * n)
+    with abi.Context(pts, 3) as ctx:
+        F, dF = ctx.field(9, F0), ctx.field(9, dF0)
+        P1, P2, o1, o2 = ctx.field(9), ctx.field(9), ctx.field(9), ctx.field(9)
+        mf = abi.Model(ctx, "hyper", lam, mu, matrix_free=True)
+        k4 = abi.Model(ctx, "hyper", lam, mu, matrix_free=False)
+        mf.evaluate(F, P1)
+        k4.evaluate(F, P2)
+        mf.apply(dF, o1)
+        k4.apply(dF, o2)
+        a, b = o1.download(), o2.download()
+        mf.close()
+        k4.close()
+    assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)
