@@ -1087,7 +1087,14 @@ void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
 template <int N, int TW, bool RT>
 void xd_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   const size_t smem = size_t(N) * TW * 16;
-  static bool a = (allow(k_x_direct<N, TW, RT>, smem), true);
+  static bool a = [] {
+    allow(k_x_direct<N, TW, RT>, smem);
+    // shared-memory carveout: FM_XCARVE percent of the maximum (A/B)
+    if (const char* e = getenv("FM_XCARVE"))
+      cudaFuncSetAttribute(k_x_direct<N, TW, RT>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
+    cudaGetLastError();
+    return true;
+  }();
   (void)a;
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
   k_x_direct<N, TW, RT><<<grid, TW * 32, smem, ctx->stream>>>(g, ctx->px.tw, spec);
@@ -1116,7 +1123,10 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   constexpr int X4TW = N >= 512 ? 4 : 8;
   bool done = false;
   if constexpr (N == 512) {  // 5.3 vs 6.0 ms at 512^3 (k_x_fast4, 4-column tiles)
-    if (zc && ctx->nzh % 8 == 0 && xdirect_mode() && 3 * int64_t(N) * g.Ny * ctx->nzh < (int64_t(1) << 31)) {
+    const bool fits = 3 * int64_t(N) * g.Ny * ctx->nzh < (int64_t(1) << 31);
+    // (two thread groups transforming A_0 and B side by side without spills,
+    // k_x_split, measured 6.0 ms at 4 columns / 2 CTAs per SM, 6.8 ms at 8 / 1)
+    if (zc && ctx->nzh % 8 == 0 && xdirect_mode() && fits) {
       g.P > 1 ? xd_rt<N, 8, true>(ctx, g, spec) : xd_rt<N, 8, false>(ctx, g, spec);
       done = true;
     }
