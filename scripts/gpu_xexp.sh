@@ -1,3 +1,3 @@
-# 512-point x pass variants: FM_XSPLIT 0 (k_x_direct), 1..3 (k_x_split shapes)
-mkdir -p gpurun_out
-for m in 0 1 2 3; do FM_XSPLIT=$m timeout 300 python scripts/xdirect_check.py > gpurun_out/xs$m.json 2>&1; echo "xsplit=$m rc=$?"; python -c "import json;d=json.load(open('gpurun_out/xs$m.json'));print(d['G_passes_ms'],d['virtual_P4_bitwise'],d['(512, 8, 16)'], d['idempotence_512'])"; done
+# SVK pass 1 A/B (double-buffered staging measured 0.72 vs 0.69 ms at 256^3 and removed)
+for v in "FM_PIPE_DB=0" "FM_PIPE_DB=1" "FM_PHASE_LABELS=0"; do env $v python scripts/svk_check.py 256; done
+for v in "FM_PIPE_DB=0" "FM_PIPE_DB=1"; do env $v python scripts/svk_check.py 256; done
