@@ -14,3 +14,5 @@ with abi.Context(pts, 3) as ctx:
     reps = abi.run_program(m, F, M.simple_shear_program(0.1, 20, 3)[:incs])
     ctx.sync()
     print("time", time.perf_counter() - t, [sum(r["cg_it"]) for r in reps])
+    import hashlib
+    print("F sha1", hashlib.sha1(F.download().tobytes()).hexdigest()[:16])

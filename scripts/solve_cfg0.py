@@ -10,3 +10,8 @@ model = abi.Model(ctx, "hyper", lam, mu)
 F = ctx.field(9, abi.identity_field(pts, 3))
 rep = model.solve_increment(F, M.simple_shear_program(0.1, 1, 3)[0])
 print(rep["cg_it"])
+import hashlib, time
+t = time.perf_counter()
+F2 = ctx.field(9, abi.identity_field(pts, 3))
+rep = model.solve_increment(F2, M.simple_shear_program(0.1, 1, 3)[0])
+print("second solve", time.perf_counter() - t, "F sha1", hashlib.sha1(F2.download().tobytes()).hexdigest()[:16])
