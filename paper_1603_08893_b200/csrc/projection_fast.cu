@@ -505,62 +505,88 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
   static_assert(32 % T == 0, "a line must not straddle a warp");
   extern __shared__ double2 sm[];
   const int nxy = g.Nx * g.Ny;
-  const int L0 = blockIdx.x * G;
-  const int Gb = min(G, nxy - L0);
-  // phase 1: prologue, one thread per voxel; z -> packed complex m = z/2
-  // voxel pairs (z, z+1) per thread: both voxels' loads in flight together,
-  // one 16-byte shared store per component (the packed complex z_m)
-  // light prologues (copy, SVK action): voxel pairs (z, z+1) per thread, both
-  // voxels' loads in flight together and one 16-byte shared store per
-  // component; heavy ones (K4, compact J2) one voxel per thread (registers)
-  constexpr bool PAIRS = (PRO == PRO_COPY || PRO == PRO_SVK);
+  const int ngroups = (nxy + G - 1) / G;
   double pap = 0.0;  // fused CG: <p, dP> over this CTA's voxels
-  if constexpr (PAIRS) {
-    constexpr int N2 = N / 2;
-    for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
-      const int gi = w / N2, m = w - gi * N2;
-      const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
-      double v0[9], v1[9];
-      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v0, &pap);
-      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node + 1, v1, &pap);
-#pragma unroll
-      for (int c = 0; c < 9; ++c) sm[(c * G + gi) * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
+  // persistent CTAs over line groups; while a group is transformed, warp 0
+  // prefetches the inputs of this CTA's next group into L2 (bulk prefetch:
+  // no registers, no shared memory), so the next prologue's loads hit L2
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int L0 = grp * G;
+    const int Gb = min(G, nxy - L0);
+    // phase 1: prologue, one thread per voxel; z -> packed complex m = z/2
+    // voxel pairs (z, z+1) per thread: both voxels' loads in flight together,
+    // one 16-byte shared store per component (the packed complex z_m)
+    // light prologues (copy, SVK action): voxel pairs (z, z+1) per thread, both
+    // voxels' loads in flight together and one 16-byte shared store per
+    // component; heavy ones (K4, compact J2) one voxel per thread (registers)
+    constexpr bool PAIRS = (PRO == PRO_COPY || PRO == PRO_SVK);
+    if constexpr (PAIRS) {
+      constexpr int N2 = N / 2;
+      for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
+        const int gi = w / N2, m = w - gi * N2;
+        const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
+        double v0[9], v1[9];
+        prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v0, &pap);
+        prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node + 1, v1, &pap);
+  #pragma unroll
+        for (int c = 0; c < 9; ++c) sm[(c * G + gi) * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
+      }
+    } else {
+      double* smd = reinterpret_cast<double*>(sm);
+      for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
+        const int gi = w / N, z = w - gi * N;
+        const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
+        double v[9];
+        prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v, &pap);
+  #pragma unroll
+        for (int c = 0; c < 9; ++c) smd[((c * G + gi) * M + reg::xaddr<SW>(z >> 1, 0)) * 2 + (z & 1)] = v[c];
+      }
     }
-  } else {
-    double* smd = reinterpret_cast<double*>(sm);
-    for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
-      const int gi = w / N, z = w - gi * N;
-      const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
-      double v[9];
-      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v, &pap);
-#pragma unroll
-      for (int c = 0; c < 9; ++c) smd[((c * G + gi) * M + reg::xaddr<SW>(z >> 1, 0)) * 2 + (z & 1)] = v[c];
+    __syncthreads();
+    if (threadIdx.x < 32 && grp + int(gridDim.x) < ngroups) {
+      const int L1 = (grp + gridDim.x) * G;
+      const int64_t node1 = g.roff + int64_t(L1) * N;
+      const unsigned bytes = unsigned(min(G, nxy - L1)) * N * 8;
+      constexpr int NKS = PRO == PRO_K4 ? 81 : (PRO == PRO_J2C ? 45 : (PRO == PRO_SVK ? 11 : 0));
+      constexpr int NIN = DIR ? 18 : 9;  // dF slabs (r and p for the fused direction update)
+      for (int q = threadIdx.x; q < NKS + NIN; q += 32) {
+        const double* base;
+        if (q < NKS) {
+          if constexpr (PRO == PRO_SVK) base = q < 9 ? pa.F + int64_t(q) * g.n : (q == 9 ? pa.lam : pa.mu);
+          else base = pa.K + int64_t(q) * g.n;
+        } else {
+          const int c = q - NKS;
+          if constexpr (DIR) base = c < 9 ? pa.r + int64_t(c) * g.n : pa.p + int64_t(c - 9) * g.n;
+          else base = pa.A + int64_t(c) * g.n;
+        }
+        bulk::prefetch_l2(base + node1, bytes);
+      }
     }
-  }
-  __syncthreads();
-  // phase 2: each line transformed by its T lanes (swizzled exchange, warp
-  // syncs), r2c untangling X[k] = E[k] + W_N^k O[k] with the partner M - k by
-  // shuffle, k < M stored from registers (kz = M dropped)
-  {
-    const int l = threadIdx.x / T, t = threadIdx.x % T;
-    const int c = l / G, gi = l - c * G;
-    double2* line = sm + l * M;
-    double2 v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
-    __syncwarp();
-    reg::fft_swz<M, E, -1>(v, line, t, twM);
-    double2* dst = spec + (int64_t(c) * nxy + L0 + gi) * M;
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-      const int k = t + T * m;
-      const double2 a = v[m];
-      const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
-      const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
-      const double2 D = csub(a, b);
-      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
-      if (gi < Gb) dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+    // phase 2: each line transformed by its T lanes (swizzled exchange, warp
+    // syncs), r2c untangling X[k] = E[k] + W_N^k O[k] with the partner M - k by
+    // shuffle, k < M stored from registers (kz = M dropped)
+    {
+      const int l = threadIdx.x / T, t = threadIdx.x % T;
+      const int c = l / G, gi = l - c * G;
+      double2* line = sm + l * M;
+      double2 v[E];
+  #pragma unroll
+      for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
+      __syncwarp();
+      reg::fft_swz<M, E, -1>(v, line, t, twM);
+      double2* dst = spec + (int64_t(c) * nxy + L0 + gi) * M;
+  #pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const int k = t + T * m;
+        const double2 a = v[m];
+        const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
+        const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+        const double2 D = csub(a, b);
+        const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+        if (gi < Gb) dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+      }
     }
+    __syncthreads();  // sm free for the next group's prologue
   }
   if constexpr (PAP) {
     pap = block_sum_any(pap);
@@ -1155,10 +1181,22 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
 template <int M, int PRO, bool DIR, bool PAP>
 void zf_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   using S = ZShape<M, PRO != PRO_COPY>;
-  static bool a = (allow(k_zf_fast<M, PRO, DIR, PAP>, S::SMEM), true);
-  (void)a;
+  static const int co = [] {  // co-resident CTAs (persistent grid)
+    allow(k_zf_fast<M, PRO, DIR, PAP>, S::SMEM);
+    int b = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_fast<M, PRO, DIR, PAP>, S::THREADS, S::SMEM);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    return std::max(b, 1) * std::max(sms, 1);
+  }();
+  static const int persist = [] {  // FM_ZF_PERSIST=0: one CTA per line group (no prefetch)
+    const char* e = getenv("FM_ZF_PERSIST");
+    return e ? atoi(e) : 1;
+  }();
   const int nxy = g.Nx * g.Ny;
-  const dim3 grid((nxy + S::G - 1) / S::G);
+  const int groups = (nxy + S::G - 1) / S::G;
+  const dim3 grid(persist ? std::min(groups, co) : groups);
   k_zf_fast<M, PRO, DIR, PAP><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
   ctx->zf_partials = int(grid.x);
 }

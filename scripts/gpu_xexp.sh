@@ -1,3 +1,3 @@
-# SVK pass 1 A/B (double-buffered staging measured 0.72 vs 0.69 ms at 256^3 and removed)
-for v in "FM_PIPE_DB=0" "FM_PIPE_DB=1" "FM_PHASE_LABELS=0"; do env $v python scripts/svk_check.py 256; done
-for v in "FM_PIPE_DB=0" "FM_PIPE_DB=1"; do env $v python scripts/svk_check.py 256; done
+# persistent k_zf_fast with L2 prefetch of the next line group (K4 / compact J2 pass 1) against one CTA per group
+for v in 0 1; do FM_ZF_PERSIST=$v python scripts/svk_check.py 256 k4; FM_ZF_PERSIST=$v python scripts/svk_check.py 512; done
+for v in 0 1; do FM_ZF_PERSIST=$v CFG1_COMPACT=1 python scripts/cfg1_short.py 3 | tail -2; done

@@ -1,4 +1,4 @@
-"""Matrix-free SVK matvec at N^3 (config-2 phases): output checksum and per-pass times
+"""Matrix-free SVK (or, with "k4", materialised-K4) matvec at N^3 (config-2 phases): output checksum and per-pass times
 (run under different FM_* switches to A/B pass-1 variants; checksums must agree bitwise)."""
 import hashlib
 import json
@@ -13,6 +13,7 @@ from paper_1603_08893_b200 import abi  # noqa: E402
 from paper_1603_08893_b200 import microstructure as M  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+mf = not (len(sys.argv) > 2 and sys.argv[2] == "k4")  # "k4": the materialised tangent
 n = N ** 3
 pg = M.bernoulli((N, N, N), 0.3, 2)
 lam, mu, _, _ = M.bind_parameters(pg, [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)])
@@ -22,7 +23,7 @@ with abi.Context((N, N, N), 3) as ctx:
     F, P, dF, out = ctx.field(9, F0), ctx.field(9), ctx.field(9), ctx.field(9)
     torch.manual_seed(0)
     torch.as_tensor(dF, device="cuda").uniform_(-1, 1)
-    model = abi.Model(ctx, "hyper", lam, mu, matrix_free=True)
+    model = abi.Model(ctx, "hyper", lam, mu, matrix_free=mf)
     model.evaluate(F, P)
     model.apply(dF, out)
     ctx.sync()
@@ -34,5 +35,5 @@ with abi.Context((N, N, N), 3) as ctx:
     ctx.profile(False)
     per = [round(m / calls, 4) for m in ms]
     model.close()
-print(json.dumps({"N": N, "env": {k: v for k, v in os.environ.items() if k.startswith("FM_")}, "sha1": h,
+print(json.dumps({"N": N, "operator": "svk" if mf else "k4", "env": {k: v for k, v in os.environ.items() if k.startswith("FM_")}, "sha1": h,
                   "passes_ms": per, "ms": round(sum(per), 4)}))
