@@ -380,7 +380,7 @@ __device__ __forceinline__ void pair_dif(double2 (&v)[16], int t, int h, const d
 // one H-point exchange buffer (64 KB), 2 CTAs x 256 threads per SM.  The
 // forward transform of B = xi_y A_1 + xi_z A_2 runs first, so the
 // accumulator is not live while A_1 and A_2 are loaded.
-template <int N, int TW, bool RT = false>
+template <int N, int TW, bool RT = false, bool CS = false>
 __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* __restrict__ tw,
                                                          double2* __restrict__ spec) {
   constexpr int E = 16, H = N / 2, TH = H / E;
@@ -401,12 +401,15 @@ __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* _
   const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
   const double xiy = qy * g.invL[1], xiz = qz * g.invL[2];
   double2* const X = sm + l + TW * h;  // sub-line of the H-point exchange (2 TW per CTA, interleaved)
+  // CS: streaming (evict-first) loads and stores, so the register spills of
+  // this pass stay in L2 instead of being written back to HBM
+  auto ld = [&](int off) { return CS ? __ldcs(row0 + off) : row0[off]; };
   double2 s[E], v[E];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = row0[cs + m * rs];
+  for (int m = 0; m < E; ++m) v[m] = ld(cs + m * rs);
 #pragma unroll
   for (int m = 0; m < E; ++m) {
-    const double2 a2 = row0[2 * cs + m * rs];
+    const double2 a2 = ld(2 * cs + m * rs);
     v[m] = make_double2(fma(v[m].x, xiy, a2.x * xiz), fma(v[m].y, xiy, a2.y * xiz));
   }
   reg::fft<H, E, -1, 2>(v, X, 2 * TW, t, tw);
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* _
 #pragma unroll
   for (int m = 0; m < E; ++m) s[m] = v[m];
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = row0[m * rs];
+  for (int m = 0; m < E; ++m) v[m] = ld(m * rs);
   reg::fft<H, E, -1, 2>(v, X, 2 * TW, t, tw);
   pair_dit<TH, TW>(v, t, h, tw);
   // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
@@ -443,7 +446,8 @@ __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* _
       if constexpr (!RT) {
 #pragma unroll
         for (int m = 0; m < E; ++m)
-          row0[j * cs + m * rs] = make_double2(v[m].x * f, v[m].y * f);
+          if constexpr (CS) __stcs(row0 + j * cs + m * rs, make_double2(v[m].x * f, v[m].y * f));
+          else row0[j * cs + m * rs] = make_double2(v[m].x * f, v[m].y * f);
       } else {
 #pragma unroll
         for (int m = 0; m < E; ++m)
@@ -494,8 +498,19 @@ struct ZShapeSel {
 template <int M, bool HEAVY = false>
 using ZShape = typename ZShapeSel<M, HEAVY>::type;
 
+// Register budget (CTAs/SM) of pass 1 with a staged prologue: 4 for the
+// materialised K4 (96 registers, more loads in flight: 256^3 pass 1 2.36 ->
+// 1.96 ms), 3 for the compact J2 and SVK prologues.  (Persistent CTAs that
+// prefetch the next line group into L2 measured slower at every budget.)
+// (Capped so that no budget falls below 96 registers: the 288-thread shape of
+// 1024-point lines keeps 2.)
+template <int PRO, int M>
+constexpr int zf_minb() {
+  return std::min(PRO == PRO_K4 ? 4 : (PRO == PRO_COPY ? 1 : 3),
+                  std::max(1, 65536 / (ZShape<M, PRO != PRO_COPY>::THREADS * 96)));
+}
 template <int M, int PRO, bool DIR, bool PAP = false>
-__global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast(Geo g, const double2* __restrict__ twM,
+__global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS, zf_minb<PRO, M>()) k_zf_fast(Geo g, const double2* __restrict__ twM,
                                                                 const double2* __restrict__ twN,
                                                                 ProArgs pa, double2* __restrict__ spec) {
   using S = ZShape<M, PRO != PRO_COPY>;
@@ -505,88 +520,62 @@ __global__ void __launch_bounds__(ZShape<M, PRO != PRO_COPY>::THREADS) k_zf_fast
   static_assert(32 % T == 0, "a line must not straddle a warp");
   extern __shared__ double2 sm[];
   const int nxy = g.Nx * g.Ny;
-  const int ngroups = (nxy + G - 1) / G;
+  const int L0 = blockIdx.x * G;
+  const int Gb = min(G, nxy - L0);
+  // phase 1: prologue, one thread per voxel; z -> packed complex m = z/2
+  // voxel pairs (z, z+1) per thread: both voxels' loads in flight together,
+  // one 16-byte shared store per component (the packed complex z_m)
+  // light prologues (copy, SVK action): voxel pairs (z, z+1) per thread, both
+  // voxels' loads in flight together and one 16-byte shared store per
+  // component; heavy ones (K4, compact J2) one voxel per thread (registers)
+  constexpr bool PAIRS = (PRO == PRO_COPY || PRO == PRO_SVK);
   double pap = 0.0;  // fused CG: <p, dP> over this CTA's voxels
-  // persistent CTAs over line groups; while a group is transformed, warp 0
-  // prefetches the inputs of this CTA's next group into L2 (bulk prefetch:
-  // no registers, no shared memory), so the next prologue's loads hit L2
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int L0 = grp * G;
-    const int Gb = min(G, nxy - L0);
-    // phase 1: prologue, one thread per voxel; z -> packed complex m = z/2
-    // voxel pairs (z, z+1) per thread: both voxels' loads in flight together,
-    // one 16-byte shared store per component (the packed complex z_m)
-    // light prologues (copy, SVK action): voxel pairs (z, z+1) per thread, both
-    // voxels' loads in flight together and one 16-byte shared store per
-    // component; heavy ones (K4, compact J2) one voxel per thread (registers)
-    constexpr bool PAIRS = (PRO == PRO_COPY || PRO == PRO_SVK);
-    if constexpr (PAIRS) {
-      constexpr int N2 = N / 2;
-      for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
-        const int gi = w / N2, m = w - gi * N2;
-        const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
-        double v0[9], v1[9];
-        prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v0, &pap);
-        prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node + 1, v1, &pap);
-  #pragma unroll
-        for (int c = 0; c < 9; ++c) sm[(c * G + gi) * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
-      }
-    } else {
-      double* smd = reinterpret_cast<double*>(sm);
-      for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
-        const int gi = w / N, z = w - gi * N;
-        const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
-        double v[9];
-        prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v, &pap);
-  #pragma unroll
-        for (int c = 0; c < 9; ++c) smd[((c * G + gi) * M + reg::xaddr<SW>(z >> 1, 0)) * 2 + (z & 1)] = v[c];
-      }
+  if constexpr (PAIRS) {
+    constexpr int N2 = N / 2;
+    for (int w = threadIdx.x; w < Gb * N2; w += blockDim.x) {
+      const int gi = w / N2, m = w - gi * N2;
+      const int64_t node = g.roff + int64_t(L0 + gi) * N + 2 * m;
+      double v0[9], v1[9];
+      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v0, &pap);
+      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node + 1, v1, &pap);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) sm[(c * G + gi) * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
     }
-    __syncthreads();
-    if (threadIdx.x < 32 && grp + int(gridDim.x) < ngroups) {
-      const int L1 = (grp + gridDim.x) * G;
-      const int64_t node1 = g.roff + int64_t(L1) * N;
-      const unsigned bytes = unsigned(min(G, nxy - L1)) * N * 8;
-      constexpr int NKS = PRO == PRO_K4 ? 81 : (PRO == PRO_J2C ? 45 : (PRO == PRO_SVK ? 11 : 0));
-      constexpr int NIN = DIR ? 18 : 9;  // dF slabs (r and p for the fused direction update)
-      for (int q = threadIdx.x; q < NKS + NIN; q += 32) {
-        const double* base;
-        if (q < NKS) {
-          if constexpr (PRO == PRO_SVK) base = q < 9 ? pa.F + int64_t(q) * g.n : (q == 9 ? pa.lam : pa.mu);
-          else base = pa.K + int64_t(q) * g.n;
-        } else {
-          const int c = q - NKS;
-          if constexpr (DIR) base = c < 9 ? pa.r + int64_t(c) * g.n : pa.p + int64_t(c - 9) * g.n;
-          else base = pa.A + int64_t(c) * g.n;
-        }
-        bulk::prefetch_l2(base + node1, bytes);
-      }
+  } else {
+    double* smd = reinterpret_cast<double*>(sm);
+    for (int w = threadIdx.x; w < Gb * N; w += blockDim.x) {
+      const int gi = w / N, z = w - gi * N;
+      const int64_t node = g.roff + int64_t(L0 + gi) * N + z;
+      double v[9];
+      prologue_voxel<3, PRO, DIR, PAP>(pa, g.n, node, v, &pap);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) smd[((c * G + gi) * M + reg::xaddr<SW>(z >> 1, 0)) * 2 + (z & 1)] = v[c];
     }
-    // phase 2: each line transformed by its T lanes (swizzled exchange, warp
-    // syncs), r2c untangling X[k] = E[k] + W_N^k O[k] with the partner M - k by
-    // shuffle, k < M stored from registers (kz = M dropped)
-    {
-      const int l = threadIdx.x / T, t = threadIdx.x % T;
-      const int c = l / G, gi = l - c * G;
-      double2* line = sm + l * M;
-      double2 v[E];
-  #pragma unroll
-      for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
-      __syncwarp();
-      reg::fft_swz<M, E, -1>(v, line, t, twM);
-      double2* dst = spec + (int64_t(c) * nxy + L0 + gi) * M;
-  #pragma unroll
-      for (int m = 0; m < E; ++m) {
-        const int k = t + T * m;
-        const double2 a = v[m];
-        const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
-        const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
-        const double2 D = csub(a, b);
-        const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
-        if (gi < Gb) dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
-      }
+  }
+  __syncthreads();
+  // phase 2: each line transformed by its T lanes (swizzled exchange, warp
+  // syncs), r2c untangling X[k] = E[k] + W_N^k O[k] with the partner M - k by
+  // shuffle, k < M stored from registers (kz = M dropped)
+  {
+    const int l = threadIdx.x / T, t = threadIdx.x % T;
+    const int c = l / G, gi = l - c * G;
+    double2* line = sm + l * M;
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
+    __syncwarp();
+    reg::fft_swz<M, E, -1>(v, line, t, twM);
+    double2* dst = spec + (int64_t(c) * nxy + L0 + gi) * M;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int k = t + T * m;
+      const double2 a = v[m];
+      const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
+      const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+      const double2 D = csub(a, b);
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      if (gi < Gb) dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
     }
-    __syncthreads();  // sm free for the next group's prologue
   }
   if constexpr (PAP) {
     pap = block_sum_any(pap);
@@ -1110,20 +1099,20 @@ void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
   g.P > 1 ? x4_rt<N, TW, E, true>(ctx, g, spec) : x4_rt<N, TW, E, false>(ctx, g, spec);
 }
 
-template <int N, int TW, bool RT>
+template <int N, int TW, bool RT, bool CS>
 void xd_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   const size_t smem = size_t(N) * TW * 16;
-  static bool a = [] {
-    allow(k_x_direct<N, TW, RT>, smem);
-    // shared-memory carveout: FM_XCARVE percent of the maximum (A/B)
-    if (const char* e = getenv("FM_XCARVE"))
-      cudaFuncSetAttribute(k_x_direct<N, TW, RT>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
-    cudaGetLastError();
-    return true;
-  }();
+  static bool a = (allow(k_x_direct<N, TW, RT, CS>, smem), true);
   (void)a;
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
-  k_x_direct<N, TW, RT><<<grid, TW * 32, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+  k_x_direct<N, TW, RT, CS><<<grid, TW * 32, smem, ctx->stream>>>(g, ctx->px.tw, spec);
+}
+int xcs_mode() {  // FM_XCS=1: streaming loads / stores in the 512-point x pass (A/B)
+  static int v = [] {
+    const char* e = getenv("FM_XCS");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 // FM_XDIRECT=0: the 512-point x pass falls back to the staged k_x_fast4
@@ -1153,7 +1142,9 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
     // (two thread groups transforming A_0 and B side by side without spills,
     // k_x_split, measured 6.0 ms at 4 columns / 2 CTAs per SM, 6.8 ms at 8 / 1)
     if (zc && ctx->nzh % 8 == 0 && xdirect_mode() && fits) {
-      g.P > 1 ? xd_rt<N, 8, true>(ctx, g, spec) : xd_rt<N, 8, false>(ctx, g, spec);
+      if (g.P > 1) xd_rt<N, 8, true, false>(ctx, g, spec);
+      else if (xcs_mode()) xd_rt<N, 8, false, true>(ctx, g, spec);
+      else xd_rt<N, 8, false, false>(ctx, g, spec);
       done = true;
     }
   }
@@ -1181,22 +1172,10 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
 template <int M, int PRO, bool DIR, bool PAP>
 void zf_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   using S = ZShape<M, PRO != PRO_COPY>;
-  static const int co = [] {  // co-resident CTAs (persistent grid)
-    allow(k_zf_fast<M, PRO, DIR, PAP>, S::SMEM);
-    int b = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_fast<M, PRO, DIR, PAP>, S::THREADS, S::SMEM);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
-    return std::max(b, 1) * std::max(sms, 1);
-  }();
-  static const int persist = [] {  // FM_ZF_PERSIST=0: one CTA per line group (no prefetch)
-    const char* e = getenv("FM_ZF_PERSIST");
-    return e ? atoi(e) : 1;
-  }();
+  static bool a = (allow(k_zf_fast<M, PRO, DIR, PAP>, S::SMEM), true);
+  (void)a;
   const int nxy = g.Nx * g.Ny;
-  const int groups = (nxy + S::G - 1) / S::G;
-  const dim3 grid(persist ? std::min(groups, co) : groups);
+  const dim3 grid((nxy + S::G - 1) / S::G);
   k_zf_fast<M, PRO, DIR, PAP><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
   ctx->zf_partials = int(grid.x);
 }
