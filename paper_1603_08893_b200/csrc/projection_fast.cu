@@ -380,7 +380,7 @@ __device__ __forceinline__ void pair_dif(double2 (&v)[16], int t, int h, const d
 // one H-point exchange buffer (64 KB), 2 CTAs x 256 threads per SM.  The
 // forward transform of B = xi_y A_1 + xi_z A_2 runs first, so the
 // accumulator is not live while A_1 and A_2 are loaded.
-template <int N, int TW, bool RT = false, bool CS = false>
+template <int N, int TW, bool RT = false>
 __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* __restrict__ tw,
                                                          double2* __restrict__ spec) {
   constexpr int E = 16, H = N / 2, TH = H / E;
@@ -401,9 +401,7 @@ __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* _
   const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
   const double xiy = qy * g.invL[1], xiz = qz * g.invL[2];
   double2* const X = sm + l + TW * h;  // sub-line of the H-point exchange (2 TW per CTA, interleaved)
-  // CS: streaming (evict-first) loads and stores, so the register spills of
-  // this pass stay in L2 instead of being written back to HBM
-  auto ld = [&](int off) { return CS ? __ldcs(row0 + off) : row0[off]; };
+  auto ld = [&](int off) { return row0[off]; };
   double2 s[E], v[E];
 #pragma unroll
   for (int m = 0; m < E; ++m) v[m] = ld(cs + m * rs);
@@ -446,8 +444,7 @@ __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* _
       if constexpr (!RT) {
 #pragma unroll
         for (int m = 0; m < E; ++m)
-          if constexpr (CS) __stcs(row0 + j * cs + m * rs, make_double2(v[m].x * f, v[m].y * f));
-          else row0[j * cs + m * rs] = make_double2(v[m].x * f, v[m].y * f);
+          row0[j * cs + m * rs] = make_double2(v[m].x * f, v[m].y * f);
       } else {
 #pragma unroll
         for (int m = 0; m < E; ++m)
@@ -504,9 +501,12 @@ using ZShape = typename ZShapeSel<M, HEAVY>::type;
 // prefetch the next line group into L2 measured slower at every budget.)
 // (Capped so that no budget falls below 96 registers: the 288-thread shape of
 // 1024-point lines keeps 2.)
+#ifndef FM_ZF_J2C_MINB
+#define FM_ZF_J2C_MINB 3
+#endif
 template <int PRO, int M>
 constexpr int zf_minb() {
-  return std::min(PRO == PRO_K4 ? 4 : (PRO == PRO_COPY ? 1 : 3),
+  return std::min(PRO == PRO_K4 ? 4 : (PRO == PRO_COPY ? 1 : (PRO == PRO_J2C ? FM_ZF_J2C_MINB : 3)),
                   std::max(1, 65536 / (ZShape<M, PRO != PRO_COPY>::THREADS * 96)));
 }
 template <int M, int PRO, bool DIR, bool PAP = false>
@@ -1099,20 +1099,13 @@ void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
   g.P > 1 ? x4_rt<N, TW, E, true>(ctx, g, spec) : x4_rt<N, TW, E, false>(ctx, g, spec);
 }
 
-template <int N, int TW, bool RT, bool CS>
+template <int N, int TW, bool RT>
 void xd_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   const size_t smem = size_t(N) * TW * 16;
-  static bool a = (allow(k_x_direct<N, TW, RT, CS>, smem), true);
+  static bool a = (allow(k_x_direct<N, TW, RT>, smem), true);
   (void)a;
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
-  k_x_direct<N, TW, RT, CS><<<grid, TW * 32, smem, ctx->stream>>>(g, ctx->px.tw, spec);
-}
-int xcs_mode() {  // FM_XCS=1: streaming loads / stores in the 512-point x pass (A/B)
-  static int v = [] {
-    const char* e = getenv("FM_XCS");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
+  k_x_direct<N, TW, RT><<<grid, TW * 32, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
 
 // FM_XDIRECT=0: the 512-point x pass falls back to the staged k_x_fast4
@@ -1142,9 +1135,8 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
     // (two thread groups transforming A_0 and B side by side without spills,
     // k_x_split, measured 6.0 ms at 4 columns / 2 CTAs per SM, 6.8 ms at 8 / 1)
     if (zc && ctx->nzh % 8 == 0 && xdirect_mode() && fits) {
-      if (g.P > 1) xd_rt<N, 8, true, false>(ctx, g, spec);
-      else if (xcs_mode()) xd_rt<N, 8, false, true>(ctx, g, spec);
-      else xd_rt<N, 8, false, false>(ctx, g, spec);
+      // (streaming evict-first loads / stores, to keep the spills in L2: 5.8 vs 5.2 ms)
+      g.P > 1 ? xd_rt<N, 8, true>(ctx, g, spec) : xd_rt<N, 8, false>(ctx, g, spec);
       done = true;
     }
   }

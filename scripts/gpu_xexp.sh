@@ -1,2 +1,3 @@
-# 512-point x pass: streaming (evict-first) loads/stores so spills stay in L2 (FM_XCS A/B)
-for v in 0 1 0 1; do FM_XCS=$v python scripts/pass_times.py 512 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('xcs=$v', d['G_passes_ms'])"; done
+# compact-J2 pass 1 register budget: 2 / 3 / 4 CTAs per SM (lib_exp builds; measured 1.31 / 1.31 / 1.66 ms at 256^3, 3 kept)
+for mb in 3 4 2; do cp paper_1603_08893_b200/lib_exp/j2c$mb.so paper_1603_08893_b200/lib/libfftmech_b200.so
+  echo "j2c minb=$mb"; python scripts/svk_check.py 256 j2c; python scripts/svk_check.py 512 j2c; done
