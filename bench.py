@@ -216,10 +216,11 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N>1: independent copies instead of slabs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
-    world, rank, local = dist_setup()
     if args.impl == "reference":
-        cpu_reference_run(args, world, rank)
+        # host-core work on rank 0 only: this arm has no collective, so no process group
+        cpu_reference_run(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
         return
+    world, rank, local = dist_setup()
 
     import torch
     from paper_1603_08893_b200 import abi
