@@ -613,12 +613,16 @@ template <int PRO, bool DIR, bool XUPD = false, bool LAB = false>
 constexpr int pipe_chunks() {
   return (PRO == PRO_COPY ? 9 : (DIR ? (XUPD ? 38 : 29) : 20)) - (LAB ? 2 : 0);
 }
-template <int M, int PRO, bool DIR, bool XUPD = false, bool LAB = false>
+// LB2: two line buffers, so the next line's prologue may start while slow
+// warps still transform the current one (one block barrier per line)
+template <int M, int PRO, bool DIR, bool XUPD = false, bool LAB = false, bool LB2 = false>
 constexpr size_t pipe_smem() {
-  return ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR, XUPD, LAB>()) * 2 * M * 8 + (LAB ? size_t(2 * M) : 0);
+  return (LB2 ? 2 : 1) * ZPipe<M>::FFT_SM + size_t(pipe_chunks<PRO, DIR, XUPD, LAB>()) * 2 * M * 8 +
+         (LAB ? size_t(2 * M) : 0);
 }
 
-template <int M, int PRO, bool DIR, int MINB, bool PAP = false, bool XUPD = false, bool LAB = false>
+template <int M, int PRO, bool DIR, int MINB, bool PAP = false, bool XUPD = false, bool LAB = false,
+          bool LB2 = false>
 __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, const double2* __restrict__ twM,
                                                                const double2* __restrict__ twN, ProArgs pa,
                                                                double2* __restrict__ spec) {
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   static_assert(32 % T == 0, "a component line must not straddle a warp");
   static_assert(!XUPD || (DIR && PRO == PRO_SVK), "x update rides on the SVK direction prologue");
   extern __shared__ __align__(16) double2 sm[];
-  double* stage = reinterpret_cast<double*>(sm + M * S::LSP);  // NCH chunks of N doubles
+  double* stage = reinterpret_cast<double*>(sm + (LB2 ? 2 : 1) * M * S::LSP);  // NCH chunks of N doubles
   __shared__ uint64_t bar;
   const int nxy = g.Nx * g.Ny;
   const int64_t n = g.n;
@@ -666,6 +670,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   unsigned phase = 0;
   for (; L < nxy; L += gridDim.x) {
     bulk::mbar_wait(&bar, phase);
+    double2* const lsm = sm + (LB2 && phase ? M * S::LSP : 0);  // this line's buffer
     phase ^= 1;
     // prologue on voxel pairs (z, z+1) out of the staging area
     for (int m = threadIdx.x; m < N / 2; m += blockDim.x) {
@@ -736,15 +741,15 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
         }
       }
 #pragma unroll
-      for (int c = 0; c < 9; ++c) sm[c * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
+      for (int c = 0; c < 9; ++c) lsm[c * M + reg::xaddr<SW>(m, 0)] = make_double2(v0[c], v1[c]);
     }
-    __syncthreads();  // staging consumed, packed line in sm
+    __syncthreads();  // staging consumed, packed line in lsm
     if (threadIdx.x == 0 && L + int(gridDim.x) < nxy) issue(L + gridDim.x);
     {
       // component c's line in the T lanes of one warp: swizzled exchange with
       // warp syncs, untangling by shuffle, spectrum stored from registers
       const int c = threadIdx.x / T, t = threadIdx.x % T;
-      double2* line = sm + c * M;
+      double2* line = lsm + c * M;
       double2 v[E];
 #pragma unroll
       for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
@@ -762,7 +767,10 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
         dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
       }
     }
-    __syncthreads();  // sm free for the next line's prologue
+    // one buffer: wait until every warp is done with it; two: the next
+    // prologue writes the other one, and the barrier after it orders this
+    // buffer's reads before its reuse two lines on
+    if constexpr (!LB2) __syncthreads();
   }
   if constexpr (PAP) {
     pap = block_sum_any(pap);
@@ -1186,17 +1194,49 @@ constexpr int pipe_minb() {  // copy: fewer registers suffice up to M = 128 (512
   return (PRO == PRO_COPY && M <= 128) ? kPipeCopyMinB : (LAB && !DIR && M <= 128 ? kPipeLabMinB : 3);
 }
 
+// FM_ZPIPE_LB2=0: one line buffer (two block barriers per line; A/B)
+int zpipe_lb2_mode() {
+  static int v = [] {
+    const char* e = getenv("FM_ZPIPE_LB2");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+template <int M, int PRO, bool DIR, bool PAP, bool XUPD, bool LAB, bool LB2>
+bool zpipe_go2(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec);
+
+// CTAs per SM a pipelined pass gets: shared memory (227 KB / SM, 1 KB reserved per CTA) or the register budget
+template <int M, int PRO, bool DIR, bool XUPD, bool LAB, bool LB2>
+constexpr int pipe_per_sm() {
+  return std::min(int((227 * 1024) / (pipe_smem<M, PRO, DIR, XUPD, LAB, LB2>() + 1024)), pipe_minb<PRO, M, LAB, DIR>());
+}
+// the second line buffer is used where it costs no CTA per SM
+template <int M, int PRO, bool DIR, bool XUPD, bool LAB>
+constexpr bool lb2_free() {
+  return pipe_per_sm<M, PRO, DIR, XUPD, LAB, true>() == pipe_per_sm<M, PRO, DIR, XUPD, LAB, false>();
+}
+
 template <int M, int PRO, bool DIR, bool PAP, bool XUPD = false, bool LAB = false>
 bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
+  if constexpr (lb2_free<M, PRO, DIR, XUPD, LAB>()) {
+    if (zpipe_lb2_mode()) return zpipe_go2<M, PRO, DIR, PAP, XUPD, LAB, true>(ctx, g, pa, spec);
+  }
+  return zpipe_go2<M, PRO, DIR, PAP, XUPD, LAB, false>(ctx, g, pa, spec);
+}
+
+template <int M, int PRO, bool DIR, bool PAP, bool XUPD, bool LAB, bool LB2>
+bool zpipe_go2(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   constexpr int MB = pipe_minb<PRO, M, LAB, DIR>();
-  constexpr size_t smem = pipe_smem<M, PRO, DIR, XUPD, LAB>();
-  if constexpr (smem > 100 * 1024 || M < 16) {  // one CTA per SM does not pay (512^3: 2x slower)
+  constexpr size_t smem = pipe_smem<M, PRO, DIR, XUPD, LAB, LB2>();
+  // one CTA per SM does not pay (512^3: 2x slower); single-buffered passes above 100 KB lose to k_zf_fast
+  if constexpr ((!LB2 && smem > 100 * 1024) || pipe_per_sm<M, PRO, DIR, XUPD, LAB, LB2>() < 2 || M < 16) {
     return false;
   } else {
     static const int per_sm = [] {
-      allow(k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB>, smem);
+      allow(k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB, LB2>, smem);
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB>,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB, LB2>,
                                                     ZPipe<M>::THREADS, smem);
       cudaGetLastError();
       return b > 0 ? b : 1;
@@ -1206,7 +1246,7 @@ bool zpipe_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int nxy = g.Nx * g.Ny;
     const int grid = std::min(nxy, std::max(sms, 1) * per_sm);
-    k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB>
+    k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB, LB2>
         <<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
     ctx->zf_partials = grid;
     return true;
