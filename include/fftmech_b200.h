@@ -101,6 +101,10 @@ int fm_ctx_profile(fm_ctx* ctx, int enable);
 int fm_ctx_profile_read(fm_ctx* ctx, double* ms /* 5 */, int64_t* calls);
 /* Number of this library's kernels launched on the context so far. */
 int64_t fm_ctx_launch_count(const fm_ctx* ctx);
+/* Distinct names of the kernels launched on the context so far, comma
+ * separated into buf (NUL-terminated, truncated to cap); returns the full
+ * length.  Evidence of which kernel variants a call actually ran. */
+int fm_ctx_kernel_names(const fm_ctx* ctx, char* buf, int cap);
 
 /* ---- slab decomposition ---------------------------------
  * Rank r of P owns x-planes [r Nx/P, (r+1) Nx/P) of every field; the

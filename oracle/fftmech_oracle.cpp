@@ -1,7 +1,7 @@
 // ============================================================================
 // fftmech CPU ORACLE — TEST INFRASTRUCTURE ONLY.
 //
-// A single-threaded C++ restatement of the reference `fftmech` hot path
+// A C++ restatement of the reference `fftmech` hot path
 // (arXiv 1603.08893, Galerkin-FFT finite-strain homogenisation), used as the
 // parity checker for the sm_100a product in paper_1603_08893_b200/.
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
@@ -31,14 +31,41 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <mutex>
+#include <thread>
 
 namespace oracle {
+
+// ------------------------------------------------------------ threading
+// par_for(count, body): body(begin, end) over contiguous chunks of [0, count)
+// on g_threads std::threads (default 1, or $OR_THREADS).  Only independent
+// work (FFT lines, nodes, vector entries) is split; every reduction stays the
+// reference's sequential sum, so results never depend on the thread count.
+static int g_threads = [] {
+  const char* e = std::getenv("OR_THREADS");
+  return e ? std::max(1, std::atoi(e)) : 1;
+}();
+
+template <class Body>
+void par_for(int64_t count, Body body) {
+  const int T = int(std::min<int64_t>(g_threads, std::max<int64_t>(1, count / 2048)));
+  if (T <= 1) {
+    body(int64_t(0), count);
+    return;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(size_t(T));
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] { body(count * t / T, count * (t + 1) / T); });
+  for (auto& th : pool) th.join();
+}
 
 using cplx = std::complex<double>;
 
@@ -207,27 +234,44 @@ struct PlanND {
   explicit PlanND(const Grid& gr) : g(gr) {
     for (int a = 0; a < g.dim; ++a) ax.emplace_back(new Plan1D(g.pts[a]));
   }
+  // Lines are independent, so they are transformed in parallel (OpenMP) and,
+  // on strided axes, gathered kLB adjacent lines at a time (one contiguous
+  // kLB*16-byte row per element) -- both change only the memory order of the
+  // work, never the arithmetic of a line, so the output is bit-identical to
+  // one line at a time on one thread.
+  static constexpr size_t kLB = 16;
   void run(cplx* data, int howmany, int sign) const {
     const size_t n = g.n();
     int maxN = 1;
     for (int a = 0; a < g.dim; ++a) maxN = std::max(maxN, g.pts[a]);
-    std::vector<cplx> line(static_cast<size_t>(maxN)), scratch(static_cast<size_t>(maxN));
-    for (int h = 0; h < howmany; ++h) {
-      cplx* slab = data + size_t(h) * n;
-      for (int a = 0; a < g.dim; ++a) {
-        const int N = g.pts[a];
-        if (N == 1) continue;
-        size_t inner = 1;
-        for (int b = a + 1; b < g.dim; ++b) inner *= size_t(g.pts[b]);
-        const size_t outer = n / (inner * size_t(N));
-        for (size_t o = 0; o < outer; ++o)
-          for (size_t i = 0; i < inner; ++i) {
-            cplx* base = slab + o * inner * size_t(N) + i;
-            for (int e = 0; e < N; ++e) line[size_t(e)] = base[size_t(e) * inner];
-            ax[size_t(a)]->run(line.data(), scratch.data(), sign);
-            for (int e = 0; e < N; ++e) base[size_t(e) * inner] = line[size_t(e)];
+    for (int a = 0; a < g.dim; ++a) {
+      const int N = g.pts[a];
+      if (N == 1) continue;
+      size_t inner = 1;
+      for (int b = a + 1; b < g.dim; ++b) inner *= size_t(g.pts[b]);
+      const size_t outer = n / (inner * size_t(N));
+      const size_t nblk = (inner + kLB - 1) / kLB;
+      const int64_t jobs = int64_t(howmany) * int64_t(outer) * int64_t(nblk);
+      par_for(jobs * int64_t(N) * int64_t(std::min(inner, kLB)), [&](int64_t w0, int64_t w1) {
+        const int64_t per = int64_t(N) * int64_t(std::min(inner, kLB));
+        std::vector<cplx> buf(size_t(maxN) * kLB), scratch(static_cast<size_t>(maxN));
+        for (int64_t job = w0 / per; job < w1 / per; ++job) {
+          const size_t ib = size_t(job) % nblk;
+          const size_t o = (size_t(job) / nblk) % outer;
+          const size_t h = size_t(job) / (nblk * outer);
+          cplx* base = data + h * n + o * inner * size_t(N);
+          if (inner == 1) {  // contiguous line: in place
+            ax[size_t(a)]->run(base, scratch.data(), sign);
+            continue;
           }
-      }
+          const size_t i0 = ib * kLB, nb = std::min(kLB, inner - i0);
+          for (int e = 0; e < N; ++e)
+            for (size_t b = 0; b < nb; ++b) buf[b * size_t(N) + size_t(e)] = base[size_t(e) * inner + i0 + b];
+          for (size_t b = 0; b < nb; ++b) ax[size_t(a)]->run(buf.data() + b * size_t(N), scratch.data(), sign);
+          for (int e = 0; e < N; ++e)
+            for (size_t b = 0; b < nb; ++b) base[size_t(e) * inner + i0 + b] = buf[b * size_t(N) + size_t(e)];
+        }
+      });
     }
   }
 };
@@ -300,7 +344,9 @@ int apply_projection(const Projection& G, const double* A, double* out, double* 
   const size_t n = G.g.n();
   const size_t total = n * size_t(d * d);
   std::vector<cplx> buf(total);
-  for (size_t i = 0; i < total; ++i) buf[i] = A[i];
+  par_for(int64_t(total), [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) buf[size_t(i)] = A[i];
+  });
   G.plan->run(buf.data(), d * d, -1);
   std::vector<cplx> o(total, cplx(0, 0));
   for (int i = 0; i < d; ++i)  // :139-152, Bhat_ij = Ahat_il ghat_lj
@@ -309,14 +355,18 @@ int apply_projection(const Projection& G, const double* A, double* out, double* 
       for (int l = 0; l < d; ++l) {
         const cplx* src = buf.data() + size_t(i * d + l) * n;
         const double* gg = G.ghat.data() + size_t(l * d + j) * n;
-        for (size_t k = 0; k < n; ++k) dst[k] += src[k] * gg[k];
+        par_for(int64_t(n), [&](int64_t a, int64_t b) {
+          for (int64_t k = a; k < b; ++k) dst[k] += src[k] * gg[k];
+        });
       }
     }
   G.plan->run(o.data(), d * d, +1);
   const double scale = 1.0 / double(n);  // :157-165
   double imag2 = 0.0;
-  for (size_t i = 0; i < total; ++i) {
-    out[i] = o[i].real() * scale;
+  par_for(int64_t(total), [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) out[i] = o[size_t(i)].real() * scale;
+  });
+  for (size_t i = 0; i < total; ++i) {  // sequential sum, as the reference's
     const double im = o[i].imag() * scale;
     imag2 += im * im;
   }
@@ -338,7 +388,9 @@ int apply_projected_tangent(const Projection& G, const double* K, const double* 
         for (int l = 0; l < d; ++l) {
           const double* a = K + size_t(((j * d + i) * d + k) * d + l) * n;
           const double* b = dF + size_t(k * d + l) * n;
-          for (size_t m = 0; m < n; ++m) o[m] += a[m] * b[m];
+          par_for(int64_t(n), [&](int64_t m0, int64_t m1) {
+            for (int64_t m = m0; m < m1; ++m) o[m] += a[m] * b[m];
+          });
         }
     }
   return apply_projection(G, dP.data(), out, nullptr);
@@ -368,16 +420,50 @@ bool inv3(const double* a, double* inv) {
 
 // --------------------------------------------------------- hyperelastic
 // hyperelastic_evaluate, hyperelastic.cpp:10-65.
+// Nodes are independent: evaluated in parallel; the error reported is the
+// one of the LOWEST failing node, i.e. the reference's first throw in node
+// order (see for_each_node below).
+struct NodeErr {
+  int status;
+  double value;
+};
+
+template <class Body>
+int for_each_node(size_t n, Body body, int64_t* bad, double* bad_value) {
+  // each chunk stops at its own first failure; the lowest one over all chunks
+  // is the lowest failing node
+  std::mutex mx;
+  int64_t fq = INT64_MAX;
+  NodeErr fe{OK, 0.0};
+  par_for(int64_t(n), [&](int64_t q0, int64_t q1) {
+    for (int64_t q = q0; q < q1; ++q) {
+      const NodeErr e = body(size_t(q));
+      if (e.status != OK) {
+        std::lock_guard<std::mutex> lk(mx);
+        if (q < fq) {
+          fq = q;
+          fe = e;
+        }
+        break;
+      }
+    }
+  });
+  const int fst = fe.status;
+  const double fval = fe.value;
+  if (fst != OK) {
+    if (bad) *bad = fq;
+    if (bad_value) *bad_value = fval;
+  }
+  return fst;
+}
+
 int hyper_evaluate(size_t n, int d, const double* F, const double* lambda, const double* mu,
                    double* P, double* K, int64_t* bad) {
-  double f[9], b[9], e[9], s[9];
-  for (size_t q = 0; q < n; ++q) {
+  return for_each_node(n, [&](size_t q) -> NodeErr {
+    double f[9], b[9], e[9], s[9];
     const double lam = lambda[q], g = mu[q];
     for (int c = 0; c < d * d; ++c) f[c] = F[size_t(c) * n + q];
-    if (det_t(f, d) <= 0.0) {  // :29
-      if (bad) *bad = int64_t(q);
-      return E_INVERTED;
-    }
+    if (det_t(f, d) <= 0.0) return {E_INVERTED, 0.0};  // :29
     double trE = 0.0;
     for (int i = 0; i < d; ++i)
       for (int j = 0; j < d; ++j) {
@@ -408,8 +494,8 @@ int hyper_evaluate(size_t n, int d, const double* F, const double* lambda, const
               if (j == k) v += s[i * d + l];
               K[size_t(((i * d + j) * d + k) * d + l) * n + q] = v;
             }
-  }
-  return OK;
+    return {OK, 0.0};
+  }, bad, nullptr);
 }
 
 // ------------------------------------------------------------- eigen 3x3
@@ -470,8 +556,8 @@ int simo_evaluate(size_t n, const double* F, const double* Fold, const double* b
                   const double* epsp_c, const double* lambda, const double* mu,
                   const double* tau_y0, const double* hard, double* P, double* K, double* be_t,
                   double* epsp_t, int64_t* bad, double* bad_value) {
-  double D[3][3][3][3], L[3][3][3][3], DL[3][3][3][3], A4[3][3][3][3];
-  for (size_t q = 0; q < n; ++q) {
+  return for_each_node(n, [&](size_t q) -> NodeErr {
+    double D[3][3][3][3], L[3][3][3][3], DL[3][3][3][3], A4[3][3][3][3];
     const double lam = lambda[q], g = mu[q], ty0 = tau_y0[q], h = hard[q];
     double Fm[9], Fo[9], Finv[9], Foinv[9], f[9], be[9];
     for (int c = 0; c < 9; ++c) {
@@ -479,14 +565,8 @@ int simo_evaluate(size_t n, const double* F, const double* Fold, const double* b
       Fo[c] = Fold[size_t(c) * n + q];
       be[c] = be_c[size_t(c) * n + q];
     }
-    if (det_t(Fm, 3) <= 0.0) {  // :49
-      if (bad) *bad = int64_t(q);
-      return E_INVERTED;
-    }
-    if (!inv3(Fm, Finv) || !inv3(Fo, Foinv)) {
-      if (bad) *bad = int64_t(q);
-      return E_SINGULAR;
-    }
+    if (det_t(Fm, 3) <= 0.0) return {E_INVERTED, 0.0};  // :49
+    if (!inv3(Fm, Finv) || !inv3(Fo, Foinv)) return {E_SINGULAR, 0.0};
     for (int i = 0; i < 3; ++i)  // f = F F_old^-1, :60-66
       for (int j = 0; j < 3; ++j) {
         double s = 0.0;
@@ -511,11 +591,7 @@ int simo_evaluate(size_t n, const double* F, const double* Fold, const double* b
     double lb[3], V[9];
     sym_eig3(bsym, lb, V);  // :74-78
     for (int m = 0; m < 3; ++m)
-      if (lb[m] < 1e-30) {  // kMinLogEigenvalue, tensor_ops.hpp:56
-        if (bad) *bad = int64_t(q);
-        if (bad_value) *bad_value = lb[m];
-        return E_NOT_SPD;
-      }
+      if (lb[m] < 1e-30) return {E_NOT_SPD, lb[m]};  // kMinLogEigenvalue, tensor_ops.hpp:56
     double eps[3], tau_d[3], dev[3];
     for (int m = 0; m < 3; ++m) eps[m] = 0.5 * std::log(lb[m]);  // :81
     const double tr_eps = eps[0] + eps[1] + eps[2];
@@ -554,7 +630,7 @@ int simo_evaluate(size_t n, const double* F, const double* Fold, const double* b
         for (int k = 0; k < 3; ++k) s += tau[i * 3 + k] * Finv[j * 3 + k];
         P[size_t(i * 3 + j) * n + q] = s;
       }
-    if (!K) continue;
+    if (!K) return {OK, 0.0};
     for (int i = 0; i < 3; ++i)  // D, :131-147
       for (int j = 0; j < 3; ++j)
         for (int k = 0; k < 3; ++k)
@@ -610,8 +686,8 @@ int simo_evaluate(size_t n, const double* F, const double* Fold, const double* b
             }
             K[size_t(((i * 3 + j) * 3 + k) * 3 + l) * n + q] = s;
           }
-  }
-  return OK;
+    return {OK, 0.0};
+  }, bad, bad_value);
 }
 
 // ---------------------------------------------------------------- models
@@ -689,8 +765,12 @@ int cg_solve(const Projection& G, const double* K, const double* b, const Solver
       return OK;
     }
     const double alpha = rr / pAp;
-    for (size_t i = 0; i < cnt; ++i) x[i] += alpha * p[i];
-    for (size_t i = 0; i < cnt; ++i) r[i] += -alpha * Ap[i];
+    par_for(int64_t(cnt), [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i) {
+        x[i] += alpha * p[size_t(i)];
+        r[size_t(i)] += -alpha * Ap[size_t(i)];
+      }
+    });
     const double rr_new = field_dot(r.data(), r.data(), cnt);
     if (std::sqrt(rr_new) <= prm.eta_cg * bnorm) {
       *res = {it, std::sqrt(rr_new) / bnorm};
@@ -698,8 +778,12 @@ int cg_solve(const Projection& G, const double* K, const double* b, const Solver
     }
     const double beta = rr_new / rr;
     rr = rr_new;
-    for (size_t i = 0; i < cnt; ++i) p[i] *= beta;
-    for (size_t i = 0; i < cnt; ++i) p[i] += r[i];
+    par_for(int64_t(cnt), [&](int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i) {
+        p[size_t(i)] *= beta;
+        p[size_t(i)] += r[size_t(i)];
+      }
+    });
   }
   *res = {cap, std::sqrt(rr) / bnorm};
   return E_CG_STALLED;
@@ -812,6 +896,15 @@ Grid make_grid(int dim, const int* pts, const double* len) {
 }  // namespace
 
 extern "C" {
+
+// Worker threads of the parallel loops (default 1, or $OR_THREADS: the
+// reference itself is single-threaded).  Results do not depend on it: only
+// independent lines / nodes / vector entries are split across threads, every
+// reduction is the reference's sequential sum (see PlanND::run).
+int or_set_threads(int nthreads) {
+  g_threads = nthreads < 1 ? 1 : nthreads;
+  return g_threads;
+}
 
 struct or_report {
   int32_t n_passes;

@@ -67,8 +67,17 @@ def lib():
                                      _dp, _dp, C.c_void_p, C.POINTER(OrReport)]
         L.or_time_projected_tangent.argtypes = [C.c_int, _ip, _dp, C.c_int, _dp, _dp, _dp, C.c_int]
         L.or_time_projected_tangent.restype = C.c_double
+        L.or_set_threads.argtypes = [C.c_int]
+        L.or_set_threads.restype = C.c_int
         _lib = L
     return _lib
+
+
+def set_threads(n=None):
+    """Worker threads of the oracle's parallel loops (None = all host cores).
+    Output is bit-identical for every thread count: only independent lines,
+    nodes and vector entries are split, all reductions stay sequential."""
+    return lib().or_set_threads(int(n) if n else (os.cpu_count() or 1))
 
 
 def _grid(points, lengths=None):

@@ -78,6 +78,7 @@ _SIGS = {
     "fm_ctx_stream": (_P, [_P]),
     "fm_ctx_launch_count": (C.c_int64, [_P]),
     "fm_ctx_profile": (C.c_int, [_P, C.c_int]),
+    "fm_ctx_kernel_names": (C.c_int, [_P, C.c_char_p, C.c_int]),
     "fm_ctx_profile_read": (C.c_int, [_P, _dp, C.POINTER(C.c_int64)]),
     "fm_field_alloc": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "fm_field_free": (C.c_int, [_P, _P]),
@@ -252,6 +253,13 @@ class Context:
     def launches(self):
         return lib().fm_ctx_launch_count(self.h)
 
+    @property
+    def kernel_names(self):
+        """Distinct names of this library's kernels launched on the context."""
+        buf = C.create_string_buffer(4096)
+        lib().fm_ctx_kernel_names(self.h, buf, 4096)
+        return [k for k in buf.value.decode().split(",") if k]
+
     # -- fields
     def field(self, ncomp=None, data=None):
         ncomp = self.ncomp if ncomp is None else ncomp
@@ -401,6 +409,15 @@ class Model:
     def apply(self, dF, out):
         self.ctx.check(lib().fm_model_apply(self.ctx.h, self.h, dF.h, out.h))
         return out
+
+    def tangent(self):
+        """The model-owned K4 field (not owned by the caller), or None when the
+        model is matrix-free / compact."""
+        h = lib().fm_model_tangent(self.h)
+        if not h:
+            return None
+        nc = self.ctx.ncomp
+        return Field(self.ctx, h, nc * nc)
 
     def history(self, which=0):
         n = self.ctx.n

@@ -203,54 +203,54 @@ static int finalize(fm_ctx* ctx, const double* partial, int nb, double* scal, in
   if (nb > 2 * kFold) {  // one block over 65536 partials costs ~60 us: fold first
     const int nf = (nb + kFold - 1) / kFold;
     k_fold<<<nf, kRedThreads, 0, ctx->stream>>>(partial, nb, ctx->d_fold);
-    FM_LAUNCHED(ctx);
+    FM_LAUNCHED_K(ctx, "k_fold");
     partial = ctx->d_fold;
     nb = nf;
   }
   if (!distributed(ctx) || op == 0) {
     k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(partial, nb, scal, op, slot);
-    FM_LAUNCHED(ctx);
+    FM_LAUNCHED_K(ctx, "k_finalize");
     return op == 0 ? combine_ranks(ctx, scal + slot, 1) : FM_OK;
   }
   constexpr int kLocal = 40;  // scratch slot for the local value
   k_finalize<<<1, kRedThreads, 0, ctx->stream>>>(partial, nb, scal, 0, kLocal);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_finalize");
   if (int st = combine_ranks(ctx, scal + kLocal, 1)) return st;
   k_scalar_op<<<1, 1, 0, ctx->stream>>>(scal, op, kLocal);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_scalar_op");
   return FM_OK;
 }
 
 int dot_async(fm_ctx* ctx, const double* a, const double* b, int64_t count, double* d_out) {
   k_dot_partial<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(a, b, count, ctx->d_partial);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_dot_partial");
   return finalize(ctx, ctx->d_partial, ctx->red_blocks, d_out, 0, 0);
 }
 
 int sum_comp_async(fm_ctx* ctx, const double* a, int ncomp, int64_t n, double* d_out) {
   const int nb = ctx->red_blocks / 16 > 0 ? ctx->red_blocks / 16 : 1;
   k_sum_comp_partial<<<dim3(nb, ncomp), kRedThreads, 0, ctx->stream>>>(a, n, ctx->d_partial);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_sum_comp_partial");
   k_finalize<<<ncomp, kRedThreads, 0, ctx->stream>>>(ctx->d_partial, nb, d_out, 0, 0);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_finalize");
   return combine_ranks(ctx, d_out, ncomp);
 }
 
 int axpy_async(fm_ctx* ctx, double a, const double* x, double* y, int64_t count) {
   k_axpy<<<ew_blocks(count), 256, 0, ctx->stream>>>(a, x, y, count);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_axpy");
   return FM_OK;
 }
 
 int scale_async(fm_ctx* ctx, double* x, double s, int64_t count) {
   k_scale<<<ew_blocks(count), 256, 0, ctx->stream>>>(x, s, count);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_scale");
   return FM_OK;
 }
 
 int add_async(fm_ctx* ctx, double* y, const double* x, double sign, int64_t count) {
   k_add<<<ew_blocks(count), 256, 0, ctx->stream>>>(y, x, sign, count);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_add");
   return FM_OK;
 }
 
@@ -258,7 +258,7 @@ static int uniform_async(fm_ctx* ctx, double* f, const double* t, int ncomp, int
   Uni u{};
   for (int c = 0; c < ncomp && c < 9; ++c) u.t[c] = t[c];
   k_uniform<<<ew_blocks(n * ncomp), 256, 0, ctx->stream>>>(f, u, ncomp, n, add);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_uniform");
   return FM_OK;
 }
 int add_uniform_async(fm_ctx* ctx, double* f, const double* t, int ncomp, int64_t n) {
@@ -279,19 +279,19 @@ int cg_update_async(fm_ctx* ctx, double* x, double* r, const double* p, const do
                     int64_t count) {
   k_cg_update<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(x, r, p, Ap, count, ctx->d_scal,
                                                                 ctx->d_partial);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_cg_update");
   return finalize(ctx, ctx->d_partial, ctx->red_blocks, ctx->d_scal, 2, 0);
 }
 
 int cg_final_x_async(fm_ctx* ctx, double* x, const double* p, int64_t count) {
   k_cg_xfinal<<<ew_blocks(count), 256, 0, ctx->stream>>>(x, p, count, ctx->d_scal);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_cg_xfinal");
   return FM_OK;
 }
 
 int cg_direction_async(fm_ctx* ctx, double* p, const double* r, int64_t count) {
   k_cg_direction<<<ew_blocks(count), 256, 0, ctx->stream>>>(p, r, count, ctx->d_scal);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_cg_direction");
   return FM_OK;
 }
 
@@ -312,7 +312,7 @@ int cg_pap_finalize_async(fm_ctx* ctx, int n_partials) {
 // pAp finalisation used by the CG driver
 int cg_pap_async(fm_ctx* ctx, const double* p, const double* Ap, int64_t count) {
   k_dot_partial<<<ctx->red_blocks, kRedThreads, 0, ctx->stream>>>(p, Ap, count, ctx->d_partial);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_dot_partial");
   return finalize(ctx, ctx->d_partial, ctx->red_blocks, ctx->d_scal, 1, 0);
 }
 

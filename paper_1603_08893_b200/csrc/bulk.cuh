@@ -45,6 +45,16 @@ __device__ __forceinline__ void g2s(void* dst, const void* src, unsigned bytes, 
                : "memory");
 }
 
+// 3-D tensor-map tile load (TMA) into shared memory, completing on `bar`;
+// map: address of a __grid_constant__ CUtensorMap parameter; c0 innermost.
+__device__ __forceinline__ void tma3d(void* dst, const void* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+      : "memory");
+}
+
 // Bulk prefetch of [src, src + bytes) into L2 (no shared memory, no
 // completion tracking): bytes a multiple of 16, src 16-byte aligned.
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {

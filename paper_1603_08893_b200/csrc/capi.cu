@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -34,6 +35,25 @@ int ensure_field(fm_ctx* ctx, fm_field& f, int ncomp) {
   f.n = ctx->n;
   FM_CUDA(ctx, cudaMalloc(&f.d, sizeof(double) * size_t(ncomp) * size_t(ctx->n)));
   return FM_OK;
+}
+
+void set_smem_limit(const void* kernel, int bytes) {
+  static std::mutex mx;
+  static std::vector<std::pair<std::pair<int, const void*>, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mx);
+  for (auto& d : done)
+    if (d.first.first == dev && d.first.second == kernel) {
+      if (d.second >= bytes) return;
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaGetLastError();
+      d.second = bytes;
+      return;
+    }
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaGetLastError();  // attribute calls must not leave a sticky launch error behind
+  done.push_back({{dev, kernel}, bytes});
 }
 
 void release_field(fm_field& f) {
@@ -95,8 +115,19 @@ using namespace fm;
 
 extern "C" {
 
+namespace {
+struct RestoreDevice {  // fm_ctx_create selects `device`; the caller's current device is restored
+  int prev = -1;
+  RestoreDevice() { cudaGetDevice(&prev); }
+  ~RestoreDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
 int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdim,
                   int nyquist_mode, int device, fm_ctx** out) {
+  RestoreDevice restore_;
   if (!out || !points || !lengths) return FM_E_INVALID;
   *out = nullptr;
   if (dim != 2 && dim != 3) return FM_E_INVALID;
@@ -173,6 +204,7 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
 }
 
 int fm_ctx_destroy(fm_ctx* ctx) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx) return FM_OK;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->cg_exec) cudaGraphExecDestroy(ctx->cg_exec);
@@ -219,6 +251,7 @@ static int setup_slabs(fm_ctx* ctx, int P) {
 }
 
 int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || P < 1) return FM_E_INVALID;
   if (ctx->nccl) return set_error(ctx, FM_E_INVALID, "context is distributed over devices");
   ctx->virt = P > 1;
@@ -239,6 +272,7 @@ int fm_ctx_create_dist(int dim, const int32_t* points, const double* lengths, in
   int st = fm_ctx_create(dim, points, lengths, tdim, nyquist_mode, device, out);
   if (st) return st;
   fm_ctx* ctx = *out;
+  FM_DEVICE_SCOPE(ctx);
   ctx->rank = rank;
   ctx->n_global = ctx->n;
   ctx->n = ctx->n_global / nranks;  // local x-slab: fields hold n_local nodes
@@ -279,7 +313,23 @@ int fm_ctx_tdim(const fm_ctx* ctx) { return ctx ? ctx->tdim : 0; }
 void* fm_ctx_stream(fm_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 int64_t fm_ctx_launch_count(const fm_ctx* ctx) { return ctx ? ctx->cnt.launches : 0; }
 
+int fm_ctx_kernel_names(const fm_ctx* ctx, char* buf, int cap) {
+  if (!ctx) return -1;
+  std::string s;
+  for (const char* k : ctx->cnt.kernels) {
+    if (!s.empty()) s += ',';
+    s += k;
+  }
+  if (buf && cap > 0) {
+    const size_t m = std::min(s.size(), size_t(cap - 1));
+    std::memcpy(buf, s.data(), m);
+    buf[m] = '\0';
+  }
+  return int(s.size());
+}
+
 int fm_ctx_profile(fm_ctx* ctx, int enable) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx) return FM_E_INVALID;
   if (int st = profile_collect(ctx)) return st;
   ctx->prof.on = enable != 0;
@@ -289,6 +339,7 @@ int fm_ctx_profile(fm_ctx* ctx, int enable) {
 }
 
 int fm_ctx_profile_read(fm_ctx* ctx, double* ms, int64_t* calls) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !ms || !calls) return FM_E_INVALID;
   if (int st = profile_collect(ctx)) return st;
   for (int s = 0; s < kPasses; ++s) ms[s] = ctx->prof.ms[s];
@@ -297,6 +348,7 @@ int fm_ctx_profile_read(fm_ctx* ctx, double* ms, int64_t* calls) {
 }
 
 int fm_ctx_synchronize(fm_ctx* ctx) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx) return FM_E_INVALID;
   FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FM_OK;
@@ -304,6 +356,7 @@ int fm_ctx_synchronize(fm_ctx* ctx) {
 
 // ------------------------------------------------------------------ fields
 int fm_field_alloc(fm_ctx* ctx, int ncomp, fm_field** out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !out || ncomp < 1 || ncomp > 81) return FM_E_INVALID;
   fm_field* f = new (std::nothrow) fm_field;
   if (!f) return FM_E_OOM;
@@ -317,6 +370,7 @@ int fm_field_alloc(fm_ctx* ctx, int ncomp, fm_field** out) {
 }
 
 int fm_field_free(fm_ctx* ctx, fm_field* f) {
+  FM_DEVICE_SCOPE(ctx);
   if (!f) return FM_OK;
   if (ctx) cudaStreamSynchronize(ctx->stream);
   release_field(*f);
@@ -327,6 +381,7 @@ int fm_field_free(fm_ctx* ctx, fm_field* f) {
 double* fm_field_device_ptr(fm_field* f) { return f ? f->d : nullptr; }
 
 int fm_field_upload(fm_ctx* ctx, fm_field* f, const double* host, int64_t count) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !f || !host || count != f->n * f->ncomp)
     return set_error(ctx, FM_E_INVALID, "fm_field_upload: size mismatch");
   FM_CUDA(ctx, cudaMemcpyAsync(f->d, host, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
@@ -335,6 +390,7 @@ int fm_field_upload(fm_ctx* ctx, fm_field* f, const double* host, int64_t count)
 }
 
 int fm_field_download(fm_ctx* ctx, const fm_field* f, double* host, int64_t count) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !f || !host || count != f->n * f->ncomp)
     return set_error(ctx, FM_E_INVALID, "fm_field_download: size mismatch");
   FM_CUDA(ctx, cudaMemcpyAsync(host, f->d, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
@@ -343,6 +399,7 @@ int fm_field_download(fm_ctx* ctx, const fm_field* f, double* host, int64_t coun
 }
 
 int fm_field_fill(fm_ctx* ctx, fm_field* f, double value) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !f) return FM_E_INVALID;
   if (value == 0.0) {
     FM_CUDA(ctx, cudaMemsetAsync(f->d, 0, sizeof(double) * f->ncomp * size_t(f->n), ctx->stream));
@@ -354,6 +411,7 @@ int fm_field_fill(fm_ctx* ctx, fm_field* f, double value) {
 }
 
 int fm_field_copy(fm_ctx* ctx, const fm_field* src, fm_field* dst) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !src || !dst || src->ncomp != dst->ncomp) return set_error(ctx, FM_E_INVALID, "copy: shape mismatch");
   FM_CUDA(ctx, cudaMemcpyAsync(dst->d, src->d, sizeof(double) * src->ncomp * size_t(src->n),
                                cudaMemcpyDeviceToDevice, ctx->stream));
@@ -362,6 +420,7 @@ int fm_field_copy(fm_ctx* ctx, const fm_field* src, fm_field* dst) {
 
 // -------------------------------------------------------------- projection
 int fm_projection_apply(fm_ctx* ctx, const fm_field* A, fm_field* out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !A || !out || A->ncomp != ctx->ncomp || out->ncomp != ctx->ncomp)
     return set_error(ctx, FM_E_INVALID, "apply_projection: field does not match operator");
   ProArgs pa;
@@ -371,6 +430,7 @@ int fm_projection_apply(fm_ctx* ctx, const fm_field* A, fm_field* out) {
 }
 
 int fm_projected_tangent_apply(fm_ctx* ctx, const fm_field* K, const fm_field* dF, fm_field* out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !K || !dF || !out || K->ncomp != ctx->ncomp * ctx->ncomp || dF->ncomp != ctx->ncomp ||
       out->ncomp != ctx->ncomp)
     return set_error(ctx, FM_E_INVALID, "apply_projected_tangent: shape mismatch");
@@ -384,6 +444,7 @@ int fm_projected_tangent_apply(fm_ctx* ctx, const fm_field* K, const fm_field* d
 // ------------------------------------------------------------ constitutive
 int fm_hyper_evaluate(fm_ctx* ctx, const fm_field* F, const fm_field* lambda, const fm_field* mu,
                       fm_field* P, fm_field* K) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !F || !lambda || !mu || !P || F->ncomp != ctx->ncomp || P->ncomp != ctx->ncomp ||
       lambda->ncomp != 1 || mu->ncomp != 1 || (K && K->ncomp != ctx->ncomp * ctx->ncomp))
     return set_error(ctx, FM_E_INVALID, "hyperelastic_evaluate: parameter field size mismatch");
@@ -396,6 +457,7 @@ int fm_simo_evaluate(fm_ctx* ctx, const fm_field* F, const fm_field* F_old,
                      const fm_field* lambda, const fm_field* mu, const fm_field* tau_y0,
                      const fm_field* hardening, fm_field* P, fm_field* K, fm_field* be_trial,
                      fm_field* epsp_trial) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "simo_evaluate: tensors must be 3x3");
   if (!F || !F_old || !be_committed || !epsp_committed || !lambda || !mu || !tau_y0 || !hardening ||
       !P || !be_trial || !epsp_trial || F->ncomp != 9 || F_old->ncomp != 9 || be_committed->ncomp != 9 ||
@@ -410,6 +472,7 @@ int fm_simo_evaluate(fm_ctx* ctx, const fm_field* F, const fm_field* F_old,
 }
 
 int fm_equivalent_stress(fm_ctx* ctx, const fm_field* F, const fm_field* P, int kind, fm_field* out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !P || !out || P->ncomp != ctx->ncomp || out->ncomp != 1 ||
       (kind != FM_EQ_TENSOR && (!F || F->ncomp != ctx->ncomp)) || kind < FM_EQ_TENSOR || kind > FM_EQ_KIRCHHOFF)
     return set_error(ctx, FM_E_INVALID, "equivalent_stress: field size mismatch");
@@ -421,6 +484,7 @@ int fm_equivalent_stress(fm_ctx* ctx, const fm_field* F, const fm_field* P, int 
 static bool same(const fm_field* a, const fm_field* b) { return a && b && a->ncomp == b->ncomp && a->n == b->n; }
 
 int fm_dot(fm_ctx* ctx, const fm_field* a, const fm_field* b, double* out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !same(a, b) || !out) return set_error(ctx, FM_E_INVALID, "tensor field shape/dimension mismatch");
   if (int st = dot_async(ctx, a->d, b->d, a->n * a->ncomp, ctx->d_scal + 8)) return st;
   if (int st = fetch_scalars(ctx, 9)) return st;
@@ -429,6 +493,7 @@ int fm_dot(fm_ctx* ctx, const fm_field* a, const fm_field* b, double* out) {
 }
 
 int fm_norm(fm_ctx* ctx, const fm_field* a, double* out) {
+  FM_DEVICE_SCOPE(ctx);
   double s;
   if (int st = fm_dot(ctx, a, a, &s)) return st;
   *out = std::sqrt(s);
@@ -436,6 +501,7 @@ int fm_norm(fm_ctx* ctx, const fm_field* a, double* out) {
 }
 
 int fm_mean(fm_ctx* ctx, const fm_field* a, double* out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !a || !out || a->ncomp > 9) return set_error(ctx, FM_E_INVALID, "mean: bad field");
   if (int st = sum_comp_async(ctx, a->d, a->ncomp, a->n, ctx->d_scal + 16)) return st;
   if (int st = fetch_scalars(ctx, 16 + a->ncomp)) return st;
@@ -444,21 +510,25 @@ int fm_mean(fm_ctx* ctx, const fm_field* a, double* out) {
 }
 
 int fm_axpy(fm_ctx* ctx, double a, const fm_field* x, fm_field* y) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !same(x, y)) return set_error(ctx, FM_E_INVALID, "tensor field shape/dimension mismatch");
   return axpy_async(ctx, a, x->d, y->d, x->n * x->ncomp);
 }
 
 int fm_scale(fm_ctx* ctx, fm_field* x, double s) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !x) return FM_E_INVALID;
   return scale_async(ctx, x->d, s, x->n * x->ncomp);
 }
 
 int fm_add(fm_ctx* ctx, fm_field* y, const fm_field* x, double sign) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !same(x, y)) return set_error(ctx, FM_E_INVALID, "tensor field shape/dimension mismatch");
   return add_async(ctx, y->d, x->d, sign, x->n * x->ncomp);
 }
 
 int fm_add_uniform(fm_ctx* ctx, fm_field* f, const double* t) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !f || !t || f->ncomp > 9) return set_error(ctx, FM_E_INVALID, "add_uniform: tensor dimension mismatch");
   return add_uniform_async(ctx, f->d, t, f->ncomp, f->n);
 }
@@ -466,6 +536,7 @@ int fm_add_uniform(fm_ctx* ctx, fm_field* f, const double* t) {
 // ------------------------------------------------------------------ solver
 int fm_cg_solve(fm_ctx* ctx, const fm_field* K, const fm_field* rhs, double eta_cg, int64_t max_cg,
                 fm_field* x, int32_t* iterations, double* rel_residual) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !K || !rhs || !x || !iterations || !rel_residual || K->ncomp != ctx->ncomp * ctx->ncomp ||
       rhs->ncomp != ctx->ncomp || x->ncomp != ctx->ncomp)
     return set_error(ctx, FM_E_INVALID, "cg_solve: shape mismatch");
@@ -521,6 +592,7 @@ static int build_phase_labels(fm_ctx* ctx, fm_model* m, const double* lambda, co
 
 int fm_model_create_hyper(fm_ctx* ctx, const double* lambda, const double* mu, int matrix_free,
                           fm_model** out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !lambda || !mu || !out) return FM_E_INVALID;
   fm_model* m = new (std::nothrow) fm_model;
   if (!m) return FM_E_OOM;
@@ -543,6 +615,7 @@ int fm_model_create_hyper(fm_ctx* ctx, const double* lambda, const double* mu, i
 
 int fm_model_create_simo(fm_ctx* ctx, const double* lambda, const double* mu, const double* tau_y0,
                          const double* hardening, fm_model** out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !lambda || !mu || !tau_y0 || !hardening || !out) return FM_E_INVALID;
   if (ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "Simo model needs tdim 3");
   fm_model* m = new (std::nothrow) fm_model;
@@ -579,6 +652,7 @@ int fm_model_create_simo(fm_ctx* ctx, const double* lambda, const double* mu, co
 }
 
 int fm_model_destroy(fm_ctx* ctx, fm_model* m) {
+  FM_DEVICE_SCOPE(ctx);
   if (!m) return FM_OK;
   if (ctx) cudaStreamSynchronize(ctx->stream);
   for (fm_field* f : {&m->lambda, &m->mu, &m->tau_y0, &m->hard, &m->K, &m->Kc, &m->F_eval, &m->be_c,
@@ -591,12 +665,14 @@ int fm_model_destroy(fm_ctx* ctx, fm_model* m) {
 }
 
 int fm_model_evaluate(fm_ctx* ctx, fm_model* m, const fm_field* F, fm_field* P) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !m || !F || !P || F->ncomp != ctx->ncomp || P->ncomp != ctx->ncomp)
     return set_error(ctx, FM_E_INVALID, "evaluate: shape mismatch");
   return model_evaluate(ctx, m, F->d, P->d);
 }
 
 int fm_model_commit(fm_ctx* ctx, fm_model* m, const fm_field* F) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !m || !F || F->ncomp != ctx->ncomp) return set_error(ctx, FM_E_INVALID, "commit: shape mismatch");
   return model_commit(ctx, m, F->d);
 }
@@ -604,6 +680,7 @@ int fm_model_commit(fm_ctx* ctx, fm_model* m, const fm_field* F) {
 fm_field* fm_model_tangent(fm_model* m) { return (m && m->K.d) ? &m->K : nullptr; }
 
 int fm_model_set_tangent_form(fm_ctx* ctx, fm_model* m, int form) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !m || form < 0 || form > 1) return FM_E_INVALID;
   if (m->kind != 1) return form == 0 ? FM_OK : set_error(ctx, FM_E_INVALID, "compact tangent: Simo model only");
   if (form == m->compact) return FM_OK;
@@ -620,6 +697,7 @@ int fm_model_set_tangent_form(fm_ctx* ctx, fm_model* m, int form) {
 }
 
 int fm_model_get_history(fm_ctx* ctx, fm_model* m, int which, double* be, double* epsp) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !m || m->kind != 1) return set_error(ctx, FM_E_INVALID, "history: not a Simo model");
   const fm_field& b = which ? m->be_t : m->be_c;
   const fm_field& e = which ? m->epsp_t : m->epsp_c;
@@ -632,6 +710,7 @@ int fm_model_get_history(fm_ctx* ctx, fm_model* m, int which, double* be, double
 
 int fm_model_set_history(fm_ctx* ctx, fm_model* m, const double* be, const double* epsp,
                          const double* f_old) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !m || m->kind != 1) return set_error(ctx, FM_E_INVALID, "history: not a Simo model");
   if (be)
     if (int st = fm_field_upload(ctx, &m->be_c, be, 9 * ctx->n)) return st;
@@ -643,6 +722,7 @@ int fm_model_set_history(fm_ctx* ctx, fm_model* m, const double* be, const doubl
 }
 
 int fm_model_apply(fm_ctx* ctx, fm_model* m, const fm_field* dF, fm_field* out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !m || !dF || !out || dF->ncomp != ctx->ncomp || out->ncomp != ctx->ncomp)
     return set_error(ctx, FM_E_INVALID, "apply: shape mismatch");
   return model_apply(ctx, m, dF->d, out->d);
@@ -650,6 +730,7 @@ int fm_model_apply(fm_ctx* ctx, fm_model* m, const fm_field* dF, fm_field* out) 
 
 int fm_solve_increment(fm_ctx* ctx, fm_model* m, fm_field* F, const double* fbar,
                        const fm_solver_params* params, fm_report* report, fm_field* P_out) {
+  FM_DEVICE_SCOPE(ctx);
   if (!ctx || !m || !F || !fbar || !params || !report) return FM_E_INVALID;
   if (P_out && P_out->ncomp != ctx->ncomp) return set_error(ctx, FM_E_INVALID, "P_out shape mismatch");
   return solve_increment(ctx, m, F, fbar, *params, report, P_out);

@@ -3,6 +3,8 @@
 // coalesced loads/stores.  Errors report the LOWEST offending node via a
 // 64-bit atomicMin on (node << 4 | status), reproducing the reference's
 // first-throw-in-node-order semantics (hyperelastic.cpp:29, simo.cpp:49,77).
+#include <cstdlib>
+
 #include "fm_internal.cuh"
 
 namespace fm {
@@ -39,8 +41,9 @@ __device__ __forceinline__ bool inv3(const double* a, double* inv) {
 
 // --------------------------------------------------------------------- SVK
 // hyperelastic_evaluate, hyperelastic.cpp:10-65.
-template <int TD>
-__global__ void __launch_bounds__(128) k_hyper(int64_t n, const double* __restrict__ F,
+// MINB: CTAs per SM the register budget targets (A/B via FM_HYPER_MINB).
+template <int TD, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_hyper(int64_t n, const double* __restrict__ F,
                                                const double* __restrict__ lam_f,
                                                const double* __restrict__ mu_f,
                                                double* __restrict__ P, double* __restrict__ K,
@@ -182,7 +185,8 @@ __device__ __forceinline__ double log_dd(double a, double b) {
 // with a_pq = (lam - c1/3 + c2 N_p N_q) w_qq l_q,  b_pq = (mu + c1/2) w_pq l_q - tau_q,
 //      c_pq = (mu + c1/2) w_qp l_p,  c1 = -6 mu^2 dg/taueq,
 //      c2 = -4 mu^2 (1/(3mu+H) - dg/taueq)   (c1 = c2 = 0 on the elastic branch).
-__global__ void __launch_bounds__(128) k_simo(int64_t n, const double* __restrict__ F,
+template <int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_simo(int64_t n, const double* __restrict__ F,
                                               const double* __restrict__ Fold,
                                               const double* __restrict__ be_c,
                                               const double* __restrict__ epsp_c,
@@ -483,11 +487,23 @@ int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const doub
                      double* K) {
   if (int st = reset_bad(ctx)) return st;
   const int blocks = grid_for(ctx->n, 128);
-  if (ctx->tdim == 3)
-    k_hyper<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
-  else
+  static const int minb = [] {
+    const char* e = getenv("FM_HYPER_MINB");
+    return e ? atoi(e) : 1;
+  }();
+  if (ctx->tdim == 3) {
+    if (minb >= 8)
+      k_hyper<3, 8><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
+    else if (minb >= 6)
+      k_hyper<3, 6><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
+    else if (minb >= 4)
+      k_hyper<3, 4><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
+    else
+      k_hyper<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
+  } else {
     k_hyper<2><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
-  FM_LAUNCHED(ctx);
+  }
+  FM_LAUNCHED_K(ctx, "k_hyper");
   return FM_OK;
 }
 
@@ -507,7 +523,7 @@ int eq_stress_async(fm_ctx* ctx, int kind, const double* F, const double* P, dou
   const int blocks = grid_for(ctx->n, 256);
   if (ctx->tdim == 3) eq_launch<3>(ctx, kind, F, P, out, blocks);
   else eq_launch<2>(ctx, kind, F, P, out, blocks);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_eq_stress");
   return FM_OK;
 }
 
@@ -517,9 +533,20 @@ int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const doub
   if (ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "simo_evaluate: tensors must be 3x3");
   if (int st = reset_bad(ctx)) return st;
   const int blocks = grid_for(ctx->n, 128);
-  k_simo<<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K,
-                                          be_t, epsp_t, ctx->d_bad, ctx->d_badval, ctx->node_offset, Kc);
-  FM_LAUNCHED(ctx);
+  static const int minb = [] {  // A/B of the register budget (FM_SIMO_MINB)
+    const char* e = getenv("FM_SIMO_MINB");
+    return e ? atoi(e) : 1;
+  }();
+  if (minb >= 3)
+    k_simo<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K, be_t, epsp_t,
+                                               ctx->d_bad, ctx->d_badval, ctx->node_offset, Kc);
+  else if (minb == 2)
+    k_simo<2><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K, be_t, epsp_t,
+                                               ctx->d_bad, ctx->d_badval, ctx->node_offset, Kc);
+  else
+    k_simo<1><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K, be_t, epsp_t,
+                                               ctx->d_bad, ctx->d_badval, ctx->node_offset, Kc);
+  FM_LAUNCHED_K(ctx, "k_simo");
   return FM_OK;
 }
 

@@ -125,7 +125,7 @@ int combine_ranks(fm_ctx* ctx, double* d_vals, int count) {
                           "ncclAllGather"))
     return st;
   k_sum_ranks<<<1, 32, 0, ctx->stream>>>(ctx->d_gather, ctx->P, count, d_vals);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_sum_ranks");
   return FM_OK;
 }
 

@@ -40,6 +40,12 @@ enum Prologue : int {
 
 struct Counters {
   int64_t launches = 0;
+  std::vector<const char*> kernels;  // distinct kernel names launched (string literals)
+  void note(const char* k) {
+    for (const char* s : kernels)
+      if (s == k || std::string(s) == k) return;
+    kernels.push_back(k);
+  }
 };
 
 // Optional per-pass CUDA-event timing of the projection (bench roofline).
@@ -145,14 +151,37 @@ int check_cuda(fm_ctx* ctx, cudaError_t e, const char* what);
     cudaError_t e_ = (call);                                    \
     if (e_ != cudaSuccess) return ::fm::check_cuda(ctx, e_, #call); \
   } while (0)
-#define FM_LAUNCHED(ctx)                                                         \
+#define FM_LAUNCHED_K(ctx, name)                                                 \
   do {                                                                           \
     (ctx)->cnt.launches++;                                                       \
+    (ctx)->cnt.note(name);                                                       \
     cudaError_t e_ = cudaGetLastError();                                         \
-    if (e_ != cudaSuccess) return ::fm::check_cuda(ctx, e_, "kernel launch");    \
+    if (e_ != cudaSuccess) return ::fm::check_cuda(ctx, e_, name);               \
   } while (0)
 
 int ensure_field(fm_ctx* ctx, fm_field& f, int ncomp);
+
+// Function attributes are per device: raise a kernel's dynamic shared-memory
+// limit on the CURRENT device once (memoised per (device, kernel)).
+void set_smem_limit(const void* kernel, int bytes);
+
+// Every entry point runs on its context's device and restores the caller's
+// current device on return (a context may be driven from any thread, and two
+// contexts of one process may live on different devices).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const fm_ctx* c) {
+    if (!c) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess) prev = cur;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+#define FM_DEVICE_SCOPE(ctx) ::fm::DeviceScope fm_device_scope_(ctx)
 void release_field(fm_field& f);
 
 // projection.cu -------------------------------------------------------------

@@ -437,9 +437,8 @@ void allow_smem(K kernel) {
   // dynamic limit = 227 KB minus the kernel's static shared memory
   cudaFuncAttributes attr{};
   cudaFuncGetAttributes(&attr, kernel);
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kMaxSmem - int(attr.sharedSizeBytes));
-  cudaGetLastError();  // attribute calls must not leave a sticky launch error behind
+  cudaGetLastError();
+  set_smem_limit(reinterpret_cast<const void*>(kernel), kMaxSmem - int(attr.sharedSizeBytes));
 }
 
 int tile_width(int nzh, int N, int lines_per_col, int& TW, int64_t other_blocks) {
@@ -489,9 +488,11 @@ void prof_mark(fm_ctx* ctx) {
 }
 
 template <int TD>
-void init_generic() {
-  static bool init = false;
-  if (init) return;
+void init_generic() {  // once per device (function attributes are per device)
+  static bool init[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || init[dev]) return;
   allow_smem(k_zfwd<TD, PRO_COPY, false>);
   allow_smem(k_zfwd<TD, PRO_K4, false>);
   allow_smem(k_zfwd<TD, PRO_SVK, false>);
@@ -502,7 +503,7 @@ void init_generic() {
   allow_smem(k_ypass);
   allow_smem(k_xpass<TD>);
   allow_smem(k_zinv<TD>);
-  init = true;
+  init[dev] = true;
 }
 
 template <int TD>
@@ -529,7 +530,7 @@ int pass_zf(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* A) {
     k_zfwd<TD, PRO_SVK, false><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
   else
     k_zfwd<TD, PRO_SVK, true><<<L.grid, L.threads, L.smem, s>>>(g, pzp, ctx->pz.tw, pa, A, L.G, L.ls);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_zfwd");
   return FM_OK;
 }
 
@@ -543,7 +544,7 @@ int pass_y(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out)
     return set_error(ctx, FM_E_UNSUPPORTED, "y line too long for the shared-memory FFT");
   const dim3 grid((ctx->nzh + TW - 1) / TW, g.Nx, ctx->ncomp);
   k_ypass<<<grid, 256, size_t(2 * TW + 1) * g.Ny * 16, ctx->stream>>>(g, ctx->py, in, out, TW, sign);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_ypass");
   return FM_OK;
 }
 
@@ -556,7 +557,7 @@ int pass_x(fm_ctx* ctx, const Geo& g, double2* T) {
     return set_error(ctx, FM_E_UNSUPPORTED, "x line too long for the shared-memory FFT");
   const dim3 grid((ctx->nzh + TW - 1) / TW, g.Ny, TD);
   k_xpass<TD><<<grid, 256, size_t(2 * TD * TW + 1) * g.Nx * 16, ctx->stream>>>(g, ctx->px, T, TW);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_xpass");
   return FM_OK;
 }
 
@@ -571,7 +572,7 @@ int pass_zi(fm_ctx* ctx, const Geo& g, const double2* A, double* out, double sca
   const ZLaunch L = z_launch(ctx, g);
   const AxisPlan& pzp = (ctx->Nz % 2 == 0) ? ctx->pzh : ctx->pz;
   k_zinv<TD><<<L.grid, L.threads, L.smem, ctx->stream>>>(g, pzp, ctx->pz.tw, A, out, L.G, L.ls, scale, epi);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_zinv");
   if (nparts) *nparts = int(L.grid.x);
   return FM_OK;
 }
@@ -666,14 +667,13 @@ static int cg_small_go(fm_ctx* ctx, CgSmallArgs& a, size_t smem, int items_max) 
   const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_cg_small<PRO>), dim3(grid), dim3(256),
                                                     args, smem, ctx->stream);
   ctx->cnt.launches++;
+  ctx->cnt.note("k_cg_small");
   return e == cudaSuccess ? FM_OK : check_cuda(ctx, e, "k_cg_small");
 }
 
 template <int PRO>
 static int cg_small_blocks(size_t smem) {
-  static bool attr = (cudaFuncSetAttribute(k_cg_small<PRO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                      cudaGetLastError(), true);
-  (void)attr;
+  set_smem_limit(reinterpret_cast<const void*>(k_cg_small<PRO>), 200 * 1024);
   int per_sm = 0, dev = 0, sms = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_small<PRO>, 256, smem);
   cudaGetLastError();

@@ -13,9 +13,13 @@
 //   x pass   : one thread holds all 3 components of its row, so the
 //              projection Bhat_i. = (Ahat_i . xi) xi / |xi|^2 is applied in
 //              registers between the forward and inverse x transforms.
+#include <cuda.h>  // CUtensorMap (the encoder is fetched with cudaGetDriverEntryPoint)
+
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "bulk.cuh"
 #include "proj_common.cuh"
@@ -451,6 +455,170 @@ __global__ void __launch_bounds__(TW * 32, 2) k_x_direct(Geo g, const double2* _
           store_xb(g, nullptr, i * 3 + j, 2 * (t + TH * m) + h, y, kz, make_double2(v[m].x * f, v[m].y * f));
       }
     }
+  }
+}
+
+// The x pass for long lines (N = 512, 1024), streamed: the component tiles
+// of a row (N x TW each) arrive in shared memory by bulk async copies
+// (cp.async.bulk, one 16*TW-byte row segment per copy, mbarrier completion)
+// instead of register loads, so no HBM latency is exposed to the transforms
+// and nothing caps the registers: persistent CTAs (one per SM, TW * N/16
+// threads) walk the (kz block, y, row) tiles.  Buffers C1 / C2 (components
+// 1, 2) are refilled with the NEXT tile's as soon as the forward transform of
+// B = xi_y A_1 + xi_z A_2 has consumed them, C0 once the inverse transforms
+// (which exchange through it) are done; every buffer doubles as the exchange
+// scratch of the transform that consumed it.  The transforms are the plain
+// N-point register FFT of k_x_fast4 (E = 16 elements per thread: 16 x 16 x 2
+// at 512), whose 168-register footprint fits where k_x_direct's lane-pair
+// variant spilled at 128.
+// Thread shape of k_x_stream: E elements per thread; PAIR: the lane-pair
+// split of k_x_direct (two H = N/2-point half-line transforms joined by a
+// shuffle radix-2 step: one shared-memory exchange per transform at 512
+// instead of two).
+template <int N, int E, bool PAIR>
+struct XsShape {
+  static constexpr int T = N / E;  // threads per line
+  static constexpr int H = N / 2, TH = H / E;
+};
+template <int N, int TW, int E, bool PAIR, bool RT = false>
+__global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const double2* __restrict__ tw,
+                                                             double2* spec, int tiles,
+                                                             const __grid_constant__ CUtensorMap tmap) {
+  using S = XsShape<N, E, PAIR>;
+  constexpr int T = S::T, TH = S::TH, H = S::H;
+  static_assert(!PAIR || (E == 16 && TH == 16 && TW * 2 <= 32), "lane pairs inside a warp");
+  constexpr int TILE = N * TW;  // complex elements of one component tile
+  extern __shared__ __align__(128) double2 sm[];
+  __shared__ uint64_t bar[3];
+  const int l = threadIdx.x % TW, u = threadIdx.x / TW;
+  const int h = PAIR ? (u & 1) : 0, t = PAIR ? (u >> 1) : u;
+  const int64_t xstride = int64_t(g.Ny) * g.nzh;
+  const int kzb = g.nzh / TW;
+  auto buf = [&](int q) { return sm + q * TILE; };
+  // The twiddles only depend on t, so the compiler would hoist all of them out
+  // of the persistent loop and keep them live (~90 registers, spills): each
+  // transform gets the table through an opaque copy of the pointer instead.
+  auto twp = [&]() {
+    const double2* p;
+    asm volatile("mov.b64 %0, %1;\n" : "=l"(p) : "l"(tw));
+    return p;
+  };
+  // row of slot m; frequency held in slot m after the forward transform
+  auto row_of = [&](int m) { return PAIR ? 2 * (t + TH * m) + h : t + T * m; };
+  auto kx_of = [&](int m) { return PAIR ? kslot<TH, H>(t, h, m) : t + T * m; };
+  auto fwd = [&](double2(&v)[E], double2* X) {
+    if constexpr (PAIR) {
+      reg::fft<H, E, -1, 2>(v, X + l + TW * h, 2 * TW, t, twp());
+      pair_dit<TH, TW>(*reinterpret_cast<double2(*)[16]>(&v), t, h, twp());
+    } else {
+      reg::fft<N, E, -1>(v, X + l, TW, t, twp());
+    }
+  };
+  auto inv = [&](double2(&v)[E], double2* X) {
+    if constexpr (PAIR) {
+      pair_dif<TH, TW>(*reinterpret_cast<double2(*)[16]>(&v), t, h, twp());
+      reg::fft<H, E, +1, 2>(v, X + l + TW * h, 2 * TW, t, twp());
+    } else {
+      reg::fft<N, E, +1>(v, X + l, TW, t, twp());
+    }
+  };
+  // tile -> (kz block fastest, y, row i): neighbouring CTAs read neighbouring
+  // 16 TW-byte segments of the same rows
+  auto tile_base = [&](int T_, int& kz0, int& y, int& i) {
+    kz0 = (T_ % kzb) * TW;
+    const int r = T_ / kzb;
+    y = r % g.Ny;
+    i = r / g.Ny;
+    return spec + int64_t(i * 3) * N * xstride + int64_t(y) * g.nzh + kz0;
+  };
+  // thread 0 fills buffer q with component q of tile T_: N / 256 tensor-map
+  // boxes of 256 rows x TW columns (the map views the spectrum as
+  // [comp * N + x][y][2 kz] doubles)
+  auto issue = [&](int T_, int q) {
+    if (threadIdx.x != 0) return;
+    int kz0, y, i;
+    tile_base(T_, kz0, y, i);
+    bulk::mbar_expect_tx(&bar[q], TILE * 16);
+#pragma unroll
+    for (int r0 = 0; r0 < N; r0 += 256)
+      bulk::tma3d(buf(q) + r0 * TW, &tmap, 2 * kz0, y, (i * 3 + q) * N + r0, &bar[q]);
+  };
+  if (threadIdx.x < 3) bulk::mbar_init(&bar[threadIdx.x], 1);
+  __syncthreads();
+  int T_ = blockIdx.x;
+  if (T_ < tiles)
+    for (int q = 0; q < 3; ++q) issue(T_, q);
+  unsigned par = 0;
+  for (; T_ < tiles; T_ += gridDim.x, par ^= 1) {
+    int kz0, y, i;
+    double2* const base = tile_base(T_, kz0, y, i);
+    const int kz = kz0 + l;
+    const int yg = g.y0 + y;
+    const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
+    const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+    const double xiy = qy * g.invL[1], xiz = qz * g.invL[2];
+    const int Tn = T_ + gridDim.x;  // next tile of this CTA
+    double2 s[E], v[E];
+    // forward transform of B = xi_y A_1 + xi_z A_2
+    bulk::mbar_wait(&bar[1], par);
+    bulk::mbar_wait(&bar[2], par);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const double2 a1 = buf(1)[row_of(m) * TW + l], a2 = buf(2)[row_of(m) * TW + l];
+      v[m] = make_double2(fma(a1.x, xiy, a2.x * xiz), fma(a1.y, xiy, a2.y * xiz));
+    }
+    __syncthreads();  // C1, C2 consumed
+    if (Tn < tiles) issue(Tn, 2);
+    fwd(v, buf(1));
+    // C1 held the exchange: order those generic writes before the async refill
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (Tn < tiles) issue(Tn, 1);
+#pragma unroll
+    for (int m = 0; m < E; ++m) s[m] = v[m];
+    // forward transform of A_0
+    bulk::mbar_wait(&bar[0], par);
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = buf(0)[row_of(m) * TW + l];
+    __syncthreads();
+    fwd(v, buf(0));
+    // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int kx = kx_of(m);
+      const double xix = freq_of(kx, N) * g.invL[0];
+      const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
+      const bool zero = norm2 == 0.0 || nyq_yz || kx == N / 2;
+      const double iv = zero ? 0.0 : 1.0 / norm2;
+      s[m] = make_double2((v[m].x * xix + s[m].x) * iv, (v[m].y * xix + s[m].y) * iv);
+    }
+    // Bhat_i0 = IFFT(s xi_x); Bhat_i1 = xi_y IFFT(s), Bhat_i2 = xi_z IFFT(s)
+    double2* const rowp = base + l;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const double f = q == 0 ? freq_of(kx_of(m), N) * g.invL[0] : 1.0;
+        v[m] = make_double2(s[m].x * f, s[m].y * f);
+      }
+      inv(v, buf(0));
+#pragma unroll 1
+      for (int j = q; j < (q == 0 ? 1 : 3); ++j) {
+        const double f = j == 0 ? 1.0 : (j == 1 ? xiy : xiz);
+        if constexpr (!RT) {
+#pragma unroll
+          for (int m = 0; m < E; ++m)
+            rowp[(int64_t(j) * N + row_of(m)) * xstride] = make_double2(v[m].x * f, v[m].y * f);
+        } else {
+#pragma unroll
+          for (int m = 0; m < E; ++m)
+            store_xb(g, nullptr, i * 3 + j, row_of(m), y, kz, make_double2(v[m].x * f, v[m].y * f));
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();  // C0 (the inverse transforms' exchange) is free
+    if (Tn < tiles) issue(Tn, 0);
   }
 }
 
@@ -1041,9 +1209,8 @@ __global__ void __launch_bounds__(LPC*(M / E), MINB)
 namespace {
 
 template <typename K>
-void allow(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-  cudaGetLastError();
+void allow(K kernel, size_t bytes) {  // per device, memoised (set_smem_limit)
+  if (bytes > 48 * 1024) set_smem_limit(reinterpret_cast<const void*>(kernel), int(bytes));
 }
 
 int tw_of(int N) { return N >= 1024 ? 4 : 8; }
@@ -1051,6 +1218,7 @@ constexpr int tw_x(int N) { return N >= 1024 ? 2 : (N >= 512 ? 4 : 8); }
 
 int launched(fm_ctx* ctx, const char* what) {
   ctx->cnt.launches++;
+  ctx->cnt.note(what);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? FM_OK : check_cuda(ctx, e, what);
 }
@@ -1062,16 +1230,13 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
   const size_t smem = size_t(N) * TW * 16;
   const dim3 grid(ctx->nzh / TW, g.Nx, ctx->ncomp);
   if (sign < 0 && g.P > 1) {  // forward pass with the fused slab transpose
-    static bool a = (allow(k_y_fast<N, TW, -1, true>, smem), true);
-    (void)a;
+    allow(k_y_fast<N, TW, -1, true>, smem);
     k_y_fast<N, TW, -1, true><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
   } else if (sign < 0) {
-    static bool a = (allow(k_y_fast<N, TW, -1>, smem), true);
-    (void)a;
+    allow(k_y_fast<N, TW, -1>, smem);
     k_y_fast<N, TW, -1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
   } else {
-    static bool a = (allow(k_y_fast<N, TW, +1>, smem), true);
-    (void)a;
+    allow(k_y_fast<N, TW, +1>, smem);
     k_y_fast<N, TW, +1><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->py.tw, in, out);
   }
   *st = launched(ctx, "k_y_fast");
@@ -1083,8 +1248,7 @@ template <int N, int TW, int E, bool RT>
 void x3_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   constexpr int T = N / E;
   const size_t smem = size_t(3) * N * TW * 16;
-  static bool a = (allow(k_x_fast3<N, TW, E, RT>, smem), true);
-  (void)a;
+  allow(k_x_fast3<N, TW, E, RT>, smem);
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
   k_x_fast3<N, TW, E, RT><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
@@ -1097,8 +1261,7 @@ template <int N, int TW, int E, bool RT>
 void x4_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   constexpr int T = N / E;
   const size_t smem = size_t(2) * N * TW * 16;
-  static bool a = (allow(k_x_fast4<N, TW, E, RT>, smem), true);
-  (void)a;
+  allow(k_x_fast4<N, TW, E, RT>, smem);
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
   k_x_fast4<N, TW, E, RT><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
@@ -1110,17 +1273,103 @@ void x4_go(fm_ctx* ctx, const Geo& g, double2* spec) {
 template <int N, int TW, bool RT>
 void xd_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   const size_t smem = size_t(N) * TW * 16;
-  static bool a = (allow(k_x_direct<N, TW, RT>, smem), true);
-  (void)a;
+  allow(k_x_direct<N, TW, RT>, smem);
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
   k_x_direct<N, TW, RT><<<grid, TW * 32, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
 
-// FM_XDIRECT=0: the 512-point x pass falls back to the staged k_x_fast4
+// Tensor map of a spectral buffer viewed as [9 N][Ny][2 nzh] doubles with a
+// (2 TW, 1, 256) box -- the x pass's component-tile rows.  Encoded on the
+// host (cuTensorMapEncodeTiled through the runtime's driver entry point, no
+// libcuda link) and cached: the map is a pure function of its arguments.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, CUtensorMap* out) {
+  struct Entry {
+    const void* base;
+    int rows, Ny, nzh, TW;
+    CUtensorMap map;
+  };
+  static std::mutex mx;
+  static std::vector<Entry> cache;
+  static EncodeTiledFn enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  if (!enc) return false;
+  std::lock_guard<std::mutex> lk(mx);
+  for (const Entry& e : cache)
+    if (e.base == base && e.rows == rows && e.Ny == Ny && e.nzh == nzh && e.TW == TW) {
+      *out = e.map;
+      return true;
+    }
+  Entry e{base, rows, Ny, nzh, TW, {}};
+  const cuuint64_t dims[3] = {cuuint64_t(2 * nzh), cuuint64_t(Ny), cuuint64_t(rows)};
+  const cuuint64_t strides[2] = {cuuint64_t(nzh) * 16, cuuint64_t(Ny) * nzh * 16};
+  const cuuint32_t box[3] = {cuuint32_t(2 * TW), 1, 256};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  // L2 promotion (A/B: FM_TMA_PROMO 0 none, 1 64 B, 2 128 B, 3 256 B); a
+  // promotion wider than the 16 TW-byte row segment would fetch neighbours
+  static const int promo = [] {
+    const char* p = getenv("FM_TMA_PROMO");
+    return p ? atoi(p) : -1;
+  }();
+  const int pm = promo >= 0 ? promo : (TW >= 8 ? 2 : 1);
+  const CUtensorMapL2promotion pr = pm == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : pm == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : pm == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                              : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (enc(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return false;
+  if (cache.size() > 64) cache.clear();
+  cache.push_back(e);
+  *out = e.map;
+  return true;
+}
+
+template <int N, int TW, int E, bool PAIR, bool RT>
+bool xs_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
+  CUtensorMap map;
+  if (!x_tensor_map(spec, 9 * N, g.Ny, g.nzh, TW, &map)) return false;
+  const size_t smem = size_t(3) * N * TW * 16;
+  constexpr int THREADS = TW * (N / E);
+  allow(k_x_stream<N, TW, E, PAIR, RT>, smem);
+  static const int per_sm = [] {  // (occupancy: the same on every B200 of the node)
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_x_stream<N, TW, E, PAIR, RT>, THREADS, smem);
+    cudaGetLastError();
+    return b > 0 ? b : 1;
+  }();
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = (ctx->nzh / TW) * g.Ny * 3;
+  const int grid = std::min(tiles, std::max(sms, 1) * per_sm);
+  k_x_stream<N, TW, E, PAIR, RT><<<grid, THREADS, smem, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map);
+  return true;
+}
+template <int N, int TW, int E, bool PAIR>
+bool xs_go(fm_ctx* ctx, const Geo& g, double2* spec) {
+  return g.P > 1 ? xs_rt<N, TW, E, PAIR, true>(ctx, g, spec) : xs_rt<N, TW, E, PAIR, false>(ctx, g, spec);
+}
+
+// FM_XDIRECT=0: the 512-point x pass falls back to the staged k_x_fast4;
+// FM_XDIRECT=1: k_x_direct (register loads); 2: k_x_stream, TW 8; 3: TW 4
+// (two CTAs per SM); 4 (default): lane-pair k_x_stream, TW 8; 5: E = 8;
+// 6: lane pair, TW 4.  Measured at 512^3 (profiles/r2_x512_ab.md): 4.91 /
+// 5.11 / 7.27 / 4.91 / 4.98 / 7.47 ms against k_x_direct's 5.31.
 int xdirect_mode() {
   static int v = [] {
     const char* e = getenv("FM_XDIRECT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 4;
   }();
   return v;
 }
@@ -1138,42 +1387,52 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   const bool zc = ctx->mode == FM_NYQUIST_ZERO_COMPATIBLE;
   constexpr int X4TW = N >= 512 ? 4 : 8;
   bool done = false;
+  const char* name = "k_x_fast";
   if constexpr (N == 512) {  // 5.3 vs 6.0 ms at 512^3 (k_x_fast4, 4-column tiles)
     const bool fits = 3 * int64_t(N) * g.Ny * ctx->nzh < (int64_t(1) << 31);
     // (two thread groups transforming A_0 and B side by side without spills,
     // k_x_split, measured 6.0 ms at 4 columns / 2 CTAs per SM, 6.8 ms at 8 / 1)
-    if (zc && ctx->nzh % 8 == 0 && xdirect_mode() && fits) {
+    const int xm = xdirect_mode();
+    if (zc && ctx->nzh % 8 == 0 && xm >= 2 &&
+        (xm == 3   ? xs_go<N, 4, 16, false>(ctx, g, spec)
+         : xm == 4 ? xs_go<N, 8, 16, true>(ctx, g, spec)
+         : xm == 5 ? xs_go<N, 8, 8, false>(ctx, g, spec)
+         : xm == 6 ? xs_go<N, 4, 16, true>(ctx, g, spec)
+                   : xs_go<N, 8, 16, false>(ctx, g, spec))) {
+      done = true;
+      name = "k_x_stream";
+    } else if (zc && ctx->nzh % 8 == 0 && xm == 1 && fits) {
       // (streaming evict-first loads / stores, to keep the spills in L2: 5.8 vs 5.2 ms)
       g.P > 1 ? xd_rt<N, 8, true>(ctx, g, spec) : xd_rt<N, 8, false>(ctx, g, spec);
       done = true;
+      name = "k_x_direct";
     }
   }
   if (done) {
   } else if (zc && N >= 64 && ctx->nzh % X4TW == 0) {  // (8 elements/thread at 512: 6.5 vs 5.9 ms)
     x4_go<N, X4TW, e_line(N)>(ctx, g, spec);
+    name = "k_x_fast4";
   } else if (N <= 512 && ctx->nzh % 8 == 0 && !(zc && N < 64)) {
     x3_go<N, 8, e_line(N)>(ctx, g, spec);
+    name = "k_x_fast3";
   } else {
     const dim3 grid(ctx->nzh / TW, g.Ny, 3);
     if (g.P > 1) {
-      static bool a = (allow(k_x_fast<N, TW, 3, true>, smem), true);
-      (void)a;
+      allow(k_x_fast<N, TW, 3, true>, smem);
       k_x_fast<N, TW, 3, true><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
     } else {
-      static bool a = (allow(k_x_fast<N, TW, 3>, smem), true);
-      (void)a;
+      allow(k_x_fast<N, TW, 3>, smem);
       k_x_fast<N, TW, 3><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
     }
   }
-  *st = launched(ctx, "k_x_fast");
+  *st = launched(ctx, name);
   return true;
 }
 
 template <int M, int PRO, bool DIR, bool PAP>
 void zf_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   using S = ZShape<M, PRO != PRO_COPY>;
-  static bool a = (allow(k_zf_fast<M, PRO, DIR, PAP>, S::SMEM), true);
-  (void)a;
+  allow(k_zf_fast<M, PRO, DIR, PAP>, S::SMEM);
   const int nxy = g.Nx * g.Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
   k_zf_fast<M, PRO, DIR, PAP><<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
@@ -1233,8 +1492,8 @@ bool zpipe_go2(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   if constexpr ((!LB2 && smem > 100 * 1024) || pipe_per_sm<M, PRO, DIR, XUPD, LAB, LB2>() < 2 || M < 16) {
     return false;
   } else {
-    static const int per_sm = [] {
-      allow(k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB, LB2>, smem);
+    allow(k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB, LB2>, smem);
+    static const int per_sm = [] {  // (occupancy: the same on every B200 of the node)
       int b = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB, LB2>,
                                                     ZPipe<M>::THREADS, smem);
@@ -1309,8 +1568,7 @@ bool zf_reg_go(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
   if constexpr (!S::OK) {
     return false;
   } else {
-    static bool a = (allow(k_zf_reg<M, S::E, S::LPC, S::MINB>, S::SMEM), true);
-    (void)a;
+    allow(k_zf_reg<M, S::E, S::LPC, S::MINB>, S::SMEM);
     const int64_t nl = int64_t(9) * g.Nx * g.Ny;
     const dim3 grid(unsigned((nl + S::LPC - 1) / S::LPC));
     k_zf_reg<M, S::E, S::LPC, S::MINB>
@@ -1329,13 +1587,11 @@ bool zi_reg_go(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, doub
     const int64_t nl = int64_t(9) * g.Nx * g.Ny;
     const dim3 grid(unsigned((nl + S::LPC - 1) / S::LPC));
     if (epi.r || epi.partial) {
-      static bool a = (allow(k_zi_reg<M, S::E, S::LPC, S::MINB, true>, S::SMEM), true);
-      (void)a;
+      allow(k_zi_reg<M, S::E, S::LPC, S::MINB, true>, S::SMEM);
       k_zi_reg<M, S::E, S::LPC, S::MINB, true>
           <<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
     } else {
-      static bool a = (allow(k_zi_reg<M, S::E, S::LPC, S::MINB>, S::SMEM), true);
-      (void)a;
+      allow(k_zi_reg<M, S::E, S::LPC, S::MINB>, S::SMEM);
       k_zi_reg<M, S::E, S::LPC, S::MINB>
           <<<grid, S::THREADS, S::SMEM, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, spec, out, scale, epi);
     }
@@ -1372,8 +1628,7 @@ bool zf_launch(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec, int*
 template <int M, typename S>
 void zi_go(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi) {
   constexpr size_t kR = size_t(9) * S::G * 2 * M * 8;  // fused CG: staged residual lines
-  static bool a = (allow(k_zi_fast<M, S>, S::SMEM + kR), true);
-  (void)a;
+  allow(k_zi_fast<M, S>, S::SMEM + kR);
   const int nxy = g.Nx * g.Ny;
   const dim3 grid((nxy + S::G - 1) / S::G);
   const size_t smem = S::SMEM + (epi.r ? kR : 0);

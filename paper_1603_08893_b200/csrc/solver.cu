@@ -198,7 +198,7 @@ int cg_loop_graph(fm_ctx* ctx, const Op& op, double* x, int64_t count, int64_t c
                                         op.lab, x, ctx->r.d, ctx->p.d, ctx->Ap.d, reinterpret_cast<const void*>(cap),
                                         reinterpret_cast<const void*>(intptr_t(ctx->P * 2 + (ctx->virt ? 1 : 0)))};
   k_cg_init<<<1, 1, 0, ctx->stream>>>(ctx->d_scal, thr);
-  FM_LAUNCHED(ctx);
+  FM_LAUNCHED_K(ctx, "k_cg_init");
   bool built = false;
   if (!ctx->cg_exec || ctx->cg_key != key) {
     built = true;

@@ -1,0 +1,14 @@
+# Usage (on the GPU box): bash scripts/ncu_box.sh <tag> <kernel-regex> <skip> <count> <cmd...>
+# Runs the command plainly first (must exit 0), then under ncu --set full,
+# and leaves only the markdown summary + stall table in gpurun_out/ (the
+# .ncu-rep is deleted: gpurun brings back at most 64 MiB).
+tag=$1; rx=$2; skip=$3; cnt=$4; shift 4
+mkdir -p gpurun_out
+"$@" > gpurun_out/ncu_plain_$tag.log 2>&1 || { echo "plain run failed: $tag"; exit 1; }
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c $cnt -o /tmp/prof_$tag "$@" > gpurun_out/ncu_$tag.log 2>&1 || { echo "ncu failed: $tag"; tail -5 gpurun_out/ncu_$tag.log; exit 1; }
+python scripts/ncu_summary.py /tmp/prof_$tag.ncu-rep > gpurun_out/prof_$tag.md 2>&1
+ncu -i /tmp/prof_$tag.ncu-rep --page source --csv --print-source sass > /tmp/src_$tag.csv 2>/dev/null
+python scripts/ncu_stalls.py /tmp/src_$tag.csv 25 >> gpurun_out/prof_$tag.md 2>&1
+ncu -i /tmp/prof_$tag.ncu-rep --page raw --csv > gpurun_out/raw_$tag.csv 2>/dev/null
+rm -f /tmp/prof_$tag.ncu-rep /tmp/src_$tag.csv
+echo "ncu ok: $tag"

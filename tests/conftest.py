@@ -17,4 +17,5 @@ def pytest_configure(config):
 def oracle():
     from oracle import oracle as O
     O.lib()
+    O.set_threads()  # bit-identical to one thread; only independent work is split
     return O

@@ -172,3 +172,124 @@ def config3_reduced():
 
 if __name__ == "__main__" and "config3" in sys.argv[1:]:
     config3_reduced()
+
+
+# ---------------------------------------------------------------------------
+# Large-grid fixtures (BASELINE configs 2 and 3): too big to commit whole, so
+# the fixture holds the run record, full-field norms and checksums, and 2^20
+# fixed (component, node) samples of each field (tests/golden_util.py).
+# The oracle runs threaded here (bit-identical to one thread, see
+# oracle/fftmech_oracle.cpp par_for).
+NSAMP = 1 << 20
+
+
+def _record(reps):
+    pad = lambda v, z: list(v) + [z] * (64 - len(v))
+    return dict(passes=np.array([r["passes"] for r in reps]),
+                cg_it=np.array([pad(r["cg_it"], 0) for r in reps]),
+                cg_rel=np.array([pad(r["cg_rel"], 0.0) for r in reps]),
+                rel_update=np.array([pad(r["rel_update"], 0.0) for r in reps]),
+                eq_rel=np.array([r["eq_rel"] for r in reps]),
+                drift=np.array([r["drift"] for r in reps]),
+                wall=np.array([r["wall"] for r in reps]))
+
+
+def _fields(prefix, x, ncomp):
+    from golden_util import checksums, sample_index
+    idx = sample_index(min(NSAMP, x.size), x.size)
+    return {f"{prefix}_samp": x[idx], f"{prefix}_norm": np.linalg.norm(x),
+            f"{prefix}_sums": checksums(x, ncomp)}
+
+
+def config2():
+    """BASELINE config 2: 256^3 SVK, Bernoulli(0.3) from mt19937_64(2),
+    contrast 10, F_bar = I + 0.1 e_x e_y, one increment (~30 GB, ~40 min on 8
+    threads)."""
+    O.set_threads()
+    pts = (256, 256, 256)
+    pg = M.bernoulli(pts, 0.3, 2)
+    lam, mu, _, _ = M.bind_parameters(pg, [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)])
+    t = time.time()
+    F, P, reps, st, _ = O.run_program(pts, 3, 0, lam, mu, M.simple_shear_program(0.1, 1, 3))
+    assert st == 0, st
+    out = _record(reps)
+    out.update(_fields("F", F, 9))
+    out.update(_fields("P", P, 9))
+    np.savez_compressed(os.path.join(HERE, "config2.npz"), **out)
+    print("config2", time.time() - t, [r["cg_it"] for r in reps], [r["rel_update"] for r in reps])
+
+
+def matvec256():
+    """One config-2 matvec at 256^3 in the reference operator form: K4 from
+    hyperelastic_evaluate at F = I + 0.05 U(-1,1) (seed 41), dF = U(-1,1)
+    (seed 42), out = G(K4 : dF^T) (projection.cpp:173-194)."""
+    O.set_threads()
+    pts = (256, 256, 256)
+    pg = M.bernoulli(pts, 0.3, 2)
+    lam, mu, _, _ = M.bind_parameters(pg, [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)])
+    n = 256 ** 3
+    F = 0.05 * M.uniform_field(pts, 9, 41)
+    for i in range(3):
+        F[(4 * i) * n:(4 * i + 1) * n] += 1.0
+    dF = M.uniform_field(pts, 9, 42)
+    t = time.time()
+    P, K, st, bad = O.hyper_evaluate(F, lam, mu)
+    assert st == 0
+    del F
+    out, st = O.apply_projected_tangent(pts, 3, K, dF)
+    assert st == 0
+    res = {}
+    res.update(_fields("P", P, 9))
+    res.update(_fields("out", out, 9))
+    np.savez_compressed(os.path.join(HERE, "matvec256.npz"), **res)
+    print("matvec256", time.time() - t, res["out_norm"])
+
+
+def _config3_128_run(args):
+    which, eps = args[0], args[1]
+    O.set_threads(args[2] if len(args) > 2 else 1)
+    N, r = 128, 3
+    pg, frac, count = M.random_spheres(N, r, 0.25, 3)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    if which == "lam":
+        lam = lam * (1.0 + eps)
+    elif which == "mu":
+        mu = mu * (1.0 + eps)
+    t = time.time()
+    F, P, reps, st, epsp = O.run_program((N, N, N), 3, 1, lam, mu, M.simple_shear_program(0.05, 10, 3)[:1],
+                                         ty0=ty, hard=h)
+    print("config3_128", which, eps, time.time() - t, st, [r["cg_it"] for r in reps], flush=True)
+    return F, P, reps, st, epsp, frac, count
+
+
+def config3_128():
+    """Config 3's generator at 128^3 (radius 3 = 12 * 128 / 512, seed 3,
+    gamma 0.05 in 10 increments), increment 1: the run record, sampled F, P
+    and eps_p, and the CG-count envelope of the oracle itself under four
+    1e-15 relative perturbations of lambda / mu (run side by side)."""
+    from multiprocessing import Pool
+    jobs = [("none", 0.0, 4)] + [(w, e, 1) for w, e in PERTURB[:4]]
+    with Pool(len(jobs)) as pool:
+        runs = pool.map(_config3_128_run, jobs)
+    F, P, reps, st, epsp, frac, count = runs[0]
+    assert st == 0, st
+    out = _record(reps)
+    out.update(_fields("F", F, 9))
+    out.update(_fields("P", P, 9))
+    out.update(_fields("epsp", epsp, 1))
+    pad = lambda r: r["cg_it"] + [0] * (64 - len(r["cg_it"]))
+    out.update(fraction=frac, spheres=count,
+               band_status=np.array([run[3] for run in runs[1:]]),
+               band_passes=np.array([[r["passes"] for r in run[2]] for run in runs[1:]]),
+               band_cg_it=np.array([[pad(r) for r in run[2]] for run in runs[1:]]))
+    np.savez_compressed(os.path.join(HERE, "config3_128.npz"), **out)
+    print("config3_128 band", [[r["cg_it"] for r in run[2]] for run in runs])
+
+
+if __name__ == "__main__":
+    sys.path.insert(0, os.path.dirname(HERE))
+    for w in sys.argv[1:]:
+        if w in ("config2", "matvec256", "config3_128"):
+            globals()[w]()

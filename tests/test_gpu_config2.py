@@ -1,0 +1,90 @@
+"""BASELINE config 2 -- the headline configuration -- against the CPU oracle
+(tests/golden/make_golden.py config2 / matvec256, the oracle restating
+solver.cpp:73-160, projection.cpp:123-194, hyperelastic.cpp:10-65):
+
+* one 256^3 matvec G(K4 : dF^T) in the reference operator form (K4
+  materialised) and in the matrix-free form the bench times (the pipelined
+  SVK pass 1), against the oracle's K4 + apply_projected_tangent: 2^20 fixed
+  samples, the full-field norm and per-component checksums, 1e-12;
+* the full config-2 Newton solve (256^3 SVK, Bernoulli(0.3) seed 2, contrast
+  10, one increment to F_bar = I + 0.1 e_x e_y) through fm_solve_increment,
+  matrix-free with the fused CG iteration (the e2e path) and with K4: the
+  same Newton pass count, CG counts within +-1 per pass, rel_update per pass,
+  and F, P within 1e-9 (BASELINE.json parity bar) on the samples, norms and
+  checksums."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1603_08893_b200 import abi
+from paper_1603_08893_b200 import microstructure as M
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from golden_util import checksums, rel, sample_index  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+PTS = (256, 256, 256)
+N3 = 256 ** 3
+
+
+def _params():
+    lam, mu, _, _ = M.bind_parameters(M.bernoulli(PTS, 0.3, 2),
+                                      [M.ElasticParams(1.0, 0.3), M.ElasticParams(10.0, 0.3)])
+    return lam, mu
+
+
+def _check_field(x, g, prefix, tol):
+    idx = sample_index(g[f"{prefix}_samp"].size, x.size)
+    assert rel(x[idx], g[f"{prefix}_samp"]) <= tol, (prefix, rel(x[idx], g[f"{prefix}_samp"]))
+    assert abs(np.linalg.norm(x) - g[f"{prefix}_norm"]) <= tol * g[f"{prefix}_norm"]
+    cs, ref = checksums(x, 9), g[f"{prefix}_sums"]
+    scale = np.sqrt(ref[1] * N3)  # |sum| <= ||x_c|| sqrt(n)
+    assert np.all(np.abs(cs[0] - ref[0]) <= tol * scale), (prefix, cs[0], ref[0])
+    assert np.all(np.abs(cs[1] - ref[1]) <= tol * ref[1]), (prefix, cs[1], ref[1])
+
+
+@pytest.mark.parametrize("form", ["matrix_free", "K4"])
+def test_config2_matvec_matches_oracle(form):
+    g = np.load(os.path.join(GOLD, "matvec256.npz"))
+    lam, mu = _params()
+    F0 = 0.05 * M.uniform_field(PTS, 9, 41)
+    for i in range(3):
+        F0[(4 * i) * N3:(4 * i + 1) * N3] += 1.0
+    dF0 = M.uniform_field(PTS, 9, 42)
+    with abi.Context(PTS, 3) as ctx:
+        F, dF, P, out = ctx.field(9, F0), ctx.field(9, dF0), ctx.field(9), ctx.field(9)
+        model = abi.Model(ctx, "hyper", lam, mu, matrix_free=(form == "matrix_free"))
+        model.evaluate(F, P)
+        model.apply(dF, out)
+        got, Pg = out.download(), P.download()
+        names = ctx.kernel_names
+        model.close()
+    _check_field(Pg, g, "P", 1e-14)
+    _check_field(got, g, "out", 1e-12)
+    assert ("k_zf_pipe" if form == "matrix_free" else "k_zf_fast") in names, names
+
+
+@pytest.mark.parametrize("form", ["matrix_free", "K4"])
+def test_config2_newton_solve_matches_oracle(form):
+    g = np.load(os.path.join(GOLD, "config2.npz"))
+    lam, mu = _params()
+    with abi.Context(PTS, 3) as ctx:
+        model = abi.Model(ctx, "hyper", lam, mu, matrix_free=(form == "matrix_free"))
+        F = ctx.field(9, abi.identity_field(PTS, 3))
+        P = ctx.field(9)
+        rep = abi.run_program(model, F, M.simple_shear_program(0.1, 1, 3), P_out=P)[0]
+        Fh, Ph = F.download(), P.download()
+        model.close()
+    npass = int(g["passes"][0])
+    ref_cg = [int(v) for v in g["cg_it"][0][:npass]]
+    assert rep["passes"] == npass, (rep["cg_it"], ref_cg)
+    assert all(abs(a - b) <= 1 for a, b in zip(rep["cg_it"], ref_cg)), (rep["cg_it"], ref_cg)
+    # per-pass ||dF|| / ||F_entry||: the CG stopping point moves it at the
+    # eta_cg level, not more
+    for a, b in zip(rep["rel_update"], g["rel_update"][0][:npass]):
+        assert abs(a - b) <= 1e-6 * b + 1e-12, (rep["rel_update"], g["rel_update"][0][:npass])
+    _check_field(Fh, g, "F", 1e-9)
+    _check_field(Ph, g, "P", 1e-9)
