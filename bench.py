@@ -18,9 +18,14 @@ flush is needed between steps).
 
 --impl reference times the CPU oracle (restatement of the reference
 apply_projected_tangent; the reference itself needs FFTW3/Eigen3, absent on
-the box) on one 256^3 matvec per step (one 128^3 matvec when --steps/--warmup
-would make that run longer than a few minutes); cpu_baseline is one 256^3
-matvec (~20 s of single-core work).
+the box) on the SAME 256^3 config-2 matvec, one matvec per step, on all host
+threads (independent FFT lines / voxels split across threads, sequential
+reductions: bit-identical to one thread); when --steps/--warmup would take
+longer than a few minutes only the first steps are timed (`steps_timed`).
+cpu_baseline is one 256^3 matvec on one thread (~20 s; the reference is
+single-threaded) plus the config-0 Newton solve on one thread.  The oracle
+runs its own Stockham FFT, not FFTW: its matvec is ~2x slower per core than
+an FFTW build would be, so GPU/CPU ratios overstate by about that.
 """
 from __future__ import annotations
 
@@ -102,14 +107,25 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
 
 
-def ncu_traffic(N):
-    """Per-pass DRAM bytes/voxel from the committed ncu --set full capture
-    (scripts/ncu_traffic.py -> profiles/r1_traffic_<N>.json), or None."""
+TRAFFIC_FILE = "r2_traffic_{N}.json"
+
+
+def ncu_traffic(N, kernels):
+    """Per-pass DRAM bytes/voxel from the committed ncu --set full capture of
+    the matrix-free matvec (scripts/ncu_traffic.py -> profiles/r2_traffic_<N>.json),
+    or None when the capture is absent or names other kernels than the ones
+    this run launched (ctx.kernel_names): a stale capture is never reported."""
     try:
-        with open(os.path.join(ROOT, "profiles", f"r1_traffic_{N}.json")) as f:
-            return json.load(f)["passes"]
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_FILE.format(N=N))) as f:
+            d = json.load(f)
     except Exception:
-        return None
+        return None, "no capture"
+    fams = [k.split("<")[0].split("(")[0].replace("void ", "").replace("fm::", "").strip()
+            for k in d.get("kernels", {}).values()]
+    missing = [k for k in fams if k not in kernels]
+    if missing:
+        return None, f"capture names kernels this run did not launch: {missing}"
+    return d["passes"], d.get("source")
 
 
 def config2_inputs(N, seed=2):
@@ -147,16 +163,10 @@ def barrier(world):
         dist.barrier()
 
 
-def cpu_reference_run(args, world, rank):
-    """`--impl reference`: the CPU oracle (restated reference) on host cores."""
-    if rank != 0:
-        return
+def config2_k4_host(N):
+    """Host K4 of the config-2 grid at F_bar (oracle hyperelastic_evaluate) and
+    the seeded dF of the matvec, as the GPU arm uses them."""
     from oracle import oracle as O
-    # the config-2 grid itself when the whole --steps/--warmup run fits a few
-    # minutes of single-core work (~20 s per 256^3 matvec), else a 128^3 sample
-    N = args.grid
-    while N > 64 and (args.steps + args.warmup) * 20.0 * (N / 256.0) ** 3 > 150.0:
-        N //= 2
     n = N ** 3
     lam, mu = config2_inputs(N)
     F = np.zeros(9 * n)
@@ -165,42 +175,179 @@ def cpu_reference_run(args, world, rank):
     F[1 * n:2 * n] = 0.1
     _, K, st, _ = O.hyper_evaluate(F, lam, mu, 3)
     dF = 2.0 * np.random.default_rng(0).random(9 * n) - 1.0
-    for _ in range(args.warmup):
-        O.time_projected_tangent((N, N, N), K, dF, reps=1)
-    t = [O.time_projected_tangent((N, N, N), K, dF, reps=1) for _ in range(args.steps)]
+    return K, dF
+
+
+def cpu_reference_run(args, world, rank):
+    """`--impl reference`: the CPU oracle (restated reference) on the host
+    cores, on the GPU arm's own config (the 256^3 config-2 matvec)."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    threads = O.set_threads()  # all host threads (results do not depend on it)
+    N = args.grid
+    n = N ** 3
+    K, dF = config2_k4_host(N)
+    budget = 200.0  # s of timed work: the whole run stays within a few minutes
+    t = []
+    if args.warmup:
+        t0 = time.perf_counter()
+        O.time_projected_tangent((N, N, N), K, dF, reps=1)  # page-in
+        first = time.perf_counter() - t0
+    else:
+        first = 0.0
+    for i in range(args.steps):
+        t.append(O.time_projected_tangent((N, N, N), K, dF, reps=1))
+        if sum(t) + first + t[-1] > budget:
+            break
     sec = float(np.mean(t))
     v = n / sec
     line = {
         "metric": "fp64 CG matvec voxels/s (G:K4:dF)", "value": v, "unit": "voxel/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "n_gpus": args.gpus, "steps": args.steps, "steps_timed": len(t), "warmup": args.warmup,
+        "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"config2: {args.grid}^3 SVK Bernoulli(0.3) seed 2, contrast 10, "
+        "config": {"workload": f"config2: {N}^3 SVK Bernoulli(0.3) seed 2, contrast 10, "
                                "G:K4:dF matvec (K4 at F_bar)",
-                   "cpu_sample": f"one {N}^3 G:K4:dF matvec per step (same generator and seed)"},
-        "cpu_baseline": {"value": v, "unit": "voxel/s", "cores": 1, "kind": "port",
-                         "sample": f"{N}^3 apply_projected_tangent per step (reference is single-threaded; "
-                                   f"FFTW3/Eigen3 absent so the oracle restatement is timed)"},
+                   "grid": [N, N, N],
+                   "cpu_sample": f"one {N}^3 G:K4:dF matvec per step (same generator, seed and grid as the GPU arm)"},
+        "cpu_baseline": {"value": v, "unit": "voxel/s", "cores": threads, "kind": "port",
+                         "sample": f"{N}^3 apply_projected_tangent per step on {threads} host threads "
+                                   "(oracle restatement with its own Stockham FFT, not FFTW; the reference "
+                                   "needs FFTW3/Eigen3, absent on the box, and is single-threaded)"},
         "e2e": {"value": v, "unit": "voxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
 def cpu_baseline_sample(N):
-    """Bounded oracle sample (10-30 s of single-core CPU work)."""
+    """Bounded oracle samples on ONE thread (the reference is single-threaded):
+    one N^3 config-2 matvec (~20 s) and the config-0 Newton solve (31^3 SVK,
+    ~10 s, SolveReport.wall_seconds as solver.cpp:81,94-98 measures it), plus
+    the offline config-2 oracle solve time recorded with its golden fixture."""
     from oracle import oracle as O
+    from paper_1603_08893_b200 import microstructure as M
+    O.set_threads(1)
     n = N ** 3
-    lam, mu = config2_inputs(N)
-    F = np.zeros(9 * n)
-    for i in range(3):
-        F[(i * 3 + i) * n:(i * 3 + i + 1) * n] = 1.0
-    F[1 * n:2 * n] = 0.1
-    _, K, _, _ = O.hyper_evaluate(F, lam, mu, 3)
-    dF = 2.0 * np.random.default_rng(0).random(9 * n) - 1.0
+    K, dF = config2_k4_host(N)
     sec = O.time_projected_tangent((N, N, N), K, dF, reps=1)
+    del K
+    pts = (31, 31, 31)
+    lam31, mu31, _, _ = M.bind_parameters(M.corner_cube(pts, 9), [M.ElasticParams(1.0, 0.3),
+                                                                  M.ElasticParams(10.0, 0.3)])
+    t0 = time.perf_counter()
+    _, _, reps, st, _ = O.run_program(pts, 3, 0, lam31, mu31, M.simple_shear_program(0.1, 1, 3))
+    wall0 = time.perf_counter() - t0
+    newton = {"config0": {"solve_s": wall0, "wall_seconds": reps[0]["wall"], "cores": 1,
+                          "newton": reps[0]["passes"], "cg_iterations": reps[0]["cg_it"], "status": st}}
+    try:
+        g = np.load(os.path.join(ROOT, "tests", "golden", "config2.npz"))
+        newton["config2_offline"] = {"wall_seconds": float(g["wall"][0]), "cores": 8,
+                                     "newton": int(g["passes"][0]),
+                                     "cg_iterations": [int(v) for v in g["cg_it"][0][:int(g["passes"][0])]],
+                                     "where": "CPU container, 8 threads (tests/golden/make_golden.py config2), "
+                                              "not this box"}
+    except Exception:
+        pass
     return {"value": n / sec, "unit": "voxel/s", "cores": 1, "kind": "port",
-            "sample": f"one {N}^3 G:K4:dF apply_projected_tangent (oracle restatement, 1 thread; "
-                      f"reference needs FFTW3/Eigen3, absent on the box)"}
+            "sample": f"one {N}^3 G:K4:dF apply_projected_tangent on 1 thread (oracle restatement with its own "
+                      f"Stockham FFT, not FFTW: ~2x slower per core than FFTW, SURVEY §6; reference needs "
+                      f"FFTW3/Eigen3, absent on the box)",
+            "newton_solve": newton}
+
+
+def config3_matvec(local, hbm, steps=5):
+    """BASELINE config 3's operator on one GPU: the 512^3 finite-strain J2
+    matvec with the compact eigenbasis tangent (45 slabs; K4 would not fit
+    next to the J2 state), random periodic spheres (radius 12, fraction 0.25,
+    seed 3), tangent at F_bar(t=1) = I + 0.005 e_x e_y; per-pass CUDA-event
+    times and each pass's roofline fraction (pass 1: 45 + 9 + 9 slabs read +
+    9 written = 576 B/voxel; passes 2-5: 144)."""
+    import torch
+    from paper_1603_08893_b200 import abi
+    from paper_1603_08893_b200 import microstructure as M
+    N = 512
+    n = N ** 3
+    pg, frac, count = M.random_spheres(N, 12, 0.25, 3)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    del pg
+    pb = [45 * 8 + 72 + 72, 144, 144, 144, 144]
+    with abi.Context((N, N, N), 3, device=local) as ctx:
+        model = abi.Model(ctx, "simo", lam, mu, ty, h, compact=True)
+        del lam, mu, ty, h
+        F = ctx.field(9)
+        tF = torch.as_tensor(F, device=f"cuda:{local}")
+        tF.zero_()
+        for i in range(3):
+            tF[(4 * i) * n:(4 * i + 1) * n] = 1.0
+        tF[n:2 * n] = 0.005
+        dF = ctx.field(9)
+        g = torch.Generator(device=f"cuda:{local}")
+        g.manual_seed(3)
+        torch.as_tensor(dF, device=f"cuda:{local}").uniform_(-1, 1, generator=g)
+        torch.cuda.synchronize()
+        P, out = ctx.field(9), ctx.field(9)
+        model.evaluate(F, P)
+        model.apply(dF, out)
+        ctx.sync()
+        ctx.profile(True)
+        stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            model.apply(dF, out)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        pass_ms, calls = ctx.profile_read()
+        ctx.profile(False)
+        per = pass_ms / max(calls, 1)
+        names = ctx.kernel_names
+        model.close()
+    return {"workload": "config3 operator: 512^3 J2 (compact eigenbasis tangent) matvec at F_bar(t=1), spheres r 12, "
+                        f"fraction {frac:.4f}, {count} spheres, seed 3",
+            "ms": ms, "voxel_per_s": n / (ms * 1e-3), "steps": steps,
+            "bytes_per_voxel": sum(pb), "frac": sum(pb) * n / (ms * 1e-3) / 1e9 / hbm,
+            "passes_ms": [float(x) for x in per],
+            "pass_frac": [b * n / (x * 1e-3) / 1e9 / hbm for b, x in zip(pb, per)],
+            "kernels": names}
+
+
+def dist_check(ctx, local, rank, world, N):
+    """N > 1: the slab-decomposed matvec against the single-device one,
+    computed once on every rank outside the timed region (the rank's slab
+    of a P = 1 matvec of the same global input must agree bit for bit)."""
+    import torch
+    from paper_1603_08893_b200 import abi
+    n, ng = ctx.n, N ** 3
+    lam_g, mu_g = config2_inputs(N)
+    rng = np.random.default_rng(77)
+    dF_g = 2.0 * rng.random(9 * ng) - 1.0
+    F_g = abi.identity_field((ng, 1, 1), 3)
+    F_g[ng:2 * ng] = 0.1
+    sl = lambda a: np.concatenate([a[c * ng + rank * n:c * ng + (rank + 1) * n] for c in range(9)])
+    m = abi.Model(ctx, "hyper", lam_g[rank * n:(rank + 1) * n], mu_g[rank * n:(rank + 1) * n], matrix_free=True)
+    F, P, dF, out = ctx.field(9, sl(F_g)), ctx.field(9), ctx.field(9, sl(dF_g)), ctx.field(9)
+    m.evaluate(F, P)
+    m.apply(dF, out)
+    mine = out.download()
+    m.close()
+    with abi.Context((N, N, N), 3, device=local) as c1:
+        m1 = abi.Model(c1, "hyper", lam_g, mu_g, matrix_free=True)
+        F1, P1, d1, o1 = c1.field(9, F_g), c1.field(9), c1.field(9, dF_g), c1.field(9)
+        m1.evaluate(F1, P1)
+        m1.apply(d1, o1)
+        ref = sl(o1.download())
+        m1.close()
+    ok = bool(np.array_equal(mine, ref))
+    t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=f"cuda:{local}")
+    import torch.distributed as tdist
+    tdist.all_reduce(t, op=tdist.ReduceOp.MIN)
+    return {"bitwise_equal_P1": bool(t.item() == 1.0),
+            "max_abs_diff_rank": float(np.max(np.abs(mine - ref))) if not ok else 0.0}
 
 
 def main():
@@ -214,6 +361,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent copies instead of slabs")
+    ap.add_argument("--no-config3", action="store_true", help="skip the 512^3 J2 operator key")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
@@ -289,12 +437,13 @@ def main():
         ach = pb[dom] * n / (per_pass[dom] * 1e-3) / 1e9
         tot = sum(pb)
         dom_name = (PASS_NAMES_MF if matrix_free else PASS_NAMES)[dom]
-        tr = ncu_traffic(N)
+        tr, tr_src = ncu_traffic(N, ctx.kernel_names) if matrix_free else (None, "captured for the matrix-free form")
         traffic = tr[dom_name] * n if tr and dom_name in tr else None  # bytes per launch (ncu --set full)
         roof = {"bound": "hbm", "kernel": dom_name, "achieved": ach,
                 "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
-                "traffic_source": "profiles/r1_traffic_%d.json (dram__bytes_read+write, one ncu --set full capture)" % N
-                if traffic else None, "peak_source": src,
+                "traffic_source": (f"profiles/{TRAFFIC_FILE.format(N=N)} (dram__bytes_read+write per launch, "
+                                   f"one ncu --set full capture of this kernel: {tr_src})") if traffic else tr_src,
+                "kernels": ctx.kernel_names, "peak_source": src,
                 "algorithmic_bytes_per_voxel": pb[dom],
                 "passes_ms": {k: float(v) for k, v in zip(PASS_NAMES_MF if matrix_free else PASS_NAMES, per_pass)},
                 "matvec": {"bytes_per_voxel": tot, "achieved": tot * n / (ms * 1e-3) / 1e9,
@@ -401,6 +550,20 @@ def main():
                                    "roofline_frac": b_g * npv / (ms_g * 1e-3) / 1e9 / hbm,
                                    "idempotence": idem}
 
+    # ---- config 3's operator (the 1-GPU point of the 8-GPU efficiency target)
+    c3 = None
+    if world == 1 and not args.no_config3:
+        try:
+            c3 = config3_matvec(local, hbm)
+        except Exception as e:  # reported, never silent
+            c3 = {"error": str(e)[:200]}
+    dchk = None
+    if slab:
+        try:
+            dchk = dist_check(ctx, local, rank, world, N)
+        except Exception as e:
+            dchk = {"error": str(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -426,7 +589,7 @@ def main():
                        "l2": "inputs 12 GB > 126 MB L2, no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "newton_solve": newton,
             "newton_solve_31": small,
-            "projection_G": proj,
+            "projection_G": proj, "config3_matvec_512": c3, "dist_check": dchk,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line))

@@ -106,6 +106,98 @@ __global__ void __launch_bounds__(128, MINB) k_hyper(int64_t n, const double* __
   }
 }
 
+// The same update on voxel pairs (3-D, even n): 16-byte loads and stores,
+// half the memory instructions of k_hyper for the 720 B/voxel of P and K4
+// it writes.  The per-voxel arithmetic is k_hyper's, expression for
+// expression, so both round identically.
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_hyper_v2(int64_t n, const double* __restrict__ F,
+                                                        const double* __restrict__ lam_f,
+                                                        const double* __restrict__ mu_f,
+                                                        double* __restrict__ P, double* __restrict__ K,
+                                                        unsigned long long* bad, int64_t noff) {
+  constexpr int TD = 3, NC = 9;
+  const int64_t np = n / 2;
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < np; p += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = 2 * p;
+    double f[2][NC], b[2][NC], s[2][NC], lam[2], g[2];
+    bool ok[2];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(F + c * n + q));
+      f[0][c] = v.x;
+      f[1][c] = v.y;
+    }
+    {
+      const double2 l2 = __ldg(reinterpret_cast<const double2*>(lam_f + q));
+      const double2 m2 = __ldg(reinterpret_cast<const double2*>(mu_f + q));
+      lam[0] = l2.x, lam[1] = l2.y, g[0] = m2.x, g[1] = m2.y;
+    }
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      ok[v] = det_t<TD>(f[v]) > 0.0;
+      if (!ok[v]) report_bad(bad, nullptr, noff + q + v, FM_E_INVERTED, 0.0);
+      double e[NC];
+      double trE = 0.0;
+#pragma unroll
+      for (int i = 0; i < TD; ++i)
+#pragma unroll
+        for (int j = 0; j < TD; ++j) {
+          double bij = 0.0, cij = 0.0;
+#pragma unroll
+          for (int k = 0; k < TD; ++k) {
+            bij += f[v][i * TD + k] * f[v][j * TD + k];
+            cij += f[v][k * TD + i] * f[v][k * TD + j];
+          }
+          b[v][i * TD + j] = bij;
+          e[i * TD + j] = 0.5 * (cij - (i == j ? 1.0 : 0.0));
+        }
+#pragma unroll
+      for (int i = 0; i < TD; ++i) trE += e[i * TD + i];
+#pragma unroll
+      for (int i = 0; i < TD; ++i)
+#pragma unroll
+        for (int j = 0; j < TD; ++j)
+          s[v][i * TD + j] = lam[v] * trE * (i == j ? 1.0 : 0.0) + 2.0 * g[v] * e[i * TD + j];
+    }
+    if (!ok[0] || !ok[1]) continue;  // (the scalar kernel skips only the bad voxel; the solve stops anyway)
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+#pragma unroll
+      for (int j = 0; j < TD; ++j) {
+        double o[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          double a = 0.0;
+#pragma unroll
+          for (int k = 0; k < TD; ++k) a += f[v][i * TD + k] * s[v][k * TD + j];
+          o[v] = a;
+        }
+        *reinterpret_cast<double2*>(P + (i * TD + j) * n + q) = make_double2(o[0], o[1]);
+      }
+    if (K) {
+#pragma unroll
+      for (int i = 0; i < TD; ++i)
+#pragma unroll
+        for (int j = 0; j < TD; ++j)
+#pragma unroll
+          for (int k = 0; k < TD; ++k)
+#pragma unroll
+            for (int l = 0; l < TD; ++l) {
+              double o[2];
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                double a = lam[v] * f[v][j * TD + i] * f[v][k * TD + l] + g[v] * f[v][j * TD + l] * f[v][k * TD + i];
+                if (i == l) a += g[v] * b[v][j * TD + k];
+                if (j == k) a += s[v][i * TD + l];
+                o[v] = a;
+              }
+              *reinterpret_cast<double2*>(K + (((i * TD + j) * TD + k) * TD + l) * n + q) = make_double2(o[0], o[1]);
+            }
+    }
+  }
+}
+
 // -------------------------------------------------------------------- Simo
 // Symmetric 3x3 eigen-decomposition restating Eigen's
 // SelfAdjointEigenSolver<Matrix3d> (simo.cpp:74): cyclic Jacobi to
@@ -487,11 +579,19 @@ int hyper_eval_async(fm_ctx* ctx, const double* F, const double* lam, const doub
                      double* K) {
   if (int st = reset_bad(ctx)) return st;
   const int blocks = grid_for(ctx->n, 128);
+  // register budget / voxels per thread (A/B via FM_HYPER_MINB: 1, 4, 6, 8
+  // one voxel per thread; 22 / 23 voxel pairs at 2 / 3 CTAs per SM)
   static const int minb = [] {
     const char* e = getenv("FM_HYPER_MINB");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 4;
   }();
-  if (ctx->tdim == 3) {
+  if (ctx->tdim == 3 && minb >= 20 && ctx->n % 2 == 0) {
+    const int b2 = grid_for(ctx->n / 2, 128);
+    if (minb == 23)
+      k_hyper_v2<3><<<b2, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
+    else
+      k_hyper_v2<2><<<b2, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
+  } else if (ctx->tdim == 3) {
     if (minb >= 8)
       k_hyper<3, 8><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, lam, mu, P, K, ctx->d_bad, ctx->node_offset);
     else if (minb >= 6)
@@ -533,10 +633,14 @@ int simo_eval_async(fm_ctx* ctx, const double* F, const double* Fold, const doub
   if (ctx->tdim != 3) return set_error(ctx, FM_E_INVALID, "simo_evaluate: tensors must be 3x3");
   if (int st = reset_bad(ctx)) return st;
   const int blocks = grid_for(ctx->n, 128);
-  static const int minb = [] {  // A/B of the register budget (FM_SIMO_MINB)
+  // register budget (A/B: FM_SIMO_MINB).  Measured at 256^3 (profiles/
+  // r2_constitutive_256_v2.md): compact tangent 6.75 -> 5.55 ms at 3 CTAs/SM,
+  // K4 11.1 -> 13.6 ms (its 81 stores want the registers): 3 / 1 by form.
+  static const int env = [] {
     const char* e = getenv("FM_SIMO_MINB");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
+  const int minb = env ? env : (Kc ? 3 : 1);
   if (minb >= 3)
     k_simo<3><<<blocks, 128, 0, ctx->stream>>>(ctx->n, F, Fold, be_c, epsp_c, lam, mu, ty0, hard, P, K, be_t, epsp_t,
                                                ctx->d_bad, ctx->d_badval, ctx->node_offset, Kc);
