@@ -55,6 +55,29 @@ __device__ __forceinline__ void tma3d(void* dst, const void* map, int c0, int c1
       : "memory");
 }
 
+// Plain arrival (count 1, release at CTA scope) on an mbarrier.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// Orders this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA) accesses of the same locations.
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// 3-D tensor-map tile store (TMA) shared -> global, bulk-group completion.
+__device__ __forceinline__ void tma3d_store(const void* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// All of this thread's bulk groups have finished READING shared memory.
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// All of this thread's bulk groups are complete (writes performed).
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 // Bulk prefetch of [src, src + bytes) into L2 (no shared memory, no
 // completion tracking): bytes a multiple of 16, src 16-byte aligned.
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {

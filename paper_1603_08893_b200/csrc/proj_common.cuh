@@ -318,5 +318,10 @@ bool y_fast(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out
 bool x_fast(fm_ctx* ctx, const Geo& g, double2* spec, int* st);
 bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
              int* st);
+// Cached CUtensorMap (written to out_map) of a spectral buffer viewed as
+// [rows][Ny][2 nzh] doubles with a (2 TW, 1, 256) box (projection_fast.cu).
+bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, void* out_map);
+// 512-point x pass, one warp per line, TMA in and out (projection_xw.cu).
+bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg);
 
 }  // namespace fm

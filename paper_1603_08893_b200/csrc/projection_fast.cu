@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "bulk.cuh"
+#include "fft_pair.cuh"
 #include "proj_common.cuh"
 
 namespace fm {
@@ -336,46 +337,6 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
 // run the mirror image (decimation in frequency: the radix-2 split by
 // shuffle, then two H-point inverse FFTs whose outputs are rows 2n and
 // 2n + 1).
-__device__ __forceinline__ double2 shfl_xor2(double2 v, int mask) {
-  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
-}
-template <int TH, int H>
-__device__ __forceinline__ int kslot(int t, int h, int s) {  // frequency held in slot s (E = 16)
-  return t + TH * ((s & 7) + 8 * h) + H * ((s >> 3) ^ h);
-}
-// Forward radix-2 DIT combine of the lane pair (E = 16): lane h = 0 holds
-// E[t + TH m], h = 1 holds O[t + TH m]; h = 0 keeps slots m < 8 (gives
-// E[m + 8]), h = 1 keeps m >= 8 (gives O[m]); the kept slot ends as X[k],
-// the other as X[k + H] (kslot).  tw: the W_N table, N = 2H.
-template <int TH, int TW>
-__device__ __forceinline__ void pair_dit(double2 (&v)[16], int t, int h, const double2* __restrict__ tw) {
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const double2 got = shfl_xor2(h == 0 ? v[m + 8] : v[m], TW);
-    const double2 e = h == 0 ? v[m] : got, o = h == 0 ? got : v[m + 8];
-    const int k = t + TH * (m + 8 * h);
-    const double2 wo = reg::tw_mul(o, __ldg(&tw[k]), -1);
-    const double2 lo = make_double2(e.x + wo.x, e.y + wo.y), hi = make_double2(e.x - wo.x, e.y - wo.y);
-    v[m] = h == 0 ? lo : hi;
-    v[m + 8] = h == 0 ? hi : lo;
-  }
-}
-// Inverse radix-2 DIF split (the mirror image): from the kslot order, the
-// sums X[k] + X[k + H] go to lane h = 0 (even output rows), the differences
-// (X[k] - X[k + H]) W_N^-k to h = 1, each as slot m of k = t + TH m.
-template <int TH, int TW>
-__device__ __forceinline__ void pair_dif(double2 (&v)[16], int t, int h, const double2* __restrict__ tw) {
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const double2 xa = h == 0 ? v[m] : v[m + 8], xb = h == 0 ? v[m + 8] : v[m];  // X[k], X[k + H]
-    const int k = t + TH * (m + 8 * h);
-    const double2 sum = make_double2(xa.x + xb.x, xa.y + xb.y);
-    const double2 dif = reg::tw_mul(make_double2(xa.x - xb.x, xa.y - xb.y), __ldg(&tw[k]), +1);
-    const double2 got = shfl_xor2(h == 0 ? dif : sum, TW);
-    v[m] = h == 0 ? sum : got;
-    v[m + 8] = h == 0 ? got : dif;
-  }
-}
 // The same 512-point x pass without tile staging, shaped like the y pass:
 // 8-column tiles (one 128-byte segment per row and component, where the
 // staged pass's 64 KB double buffer only allows 4 columns = 64-byte
@@ -483,7 +444,7 @@ struct XsShape {
 template <int N, int TW, int E, bool PAIR, bool RT = false>
 __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const double2* __restrict__ tw,
                                                              double2* spec, int tiles,
-                                                             const __grid_constant__ CUtensorMap tmap) {
+                                                             const __grid_constant__ CUtensorMap tmap, int dbg) {
   using S = XsShape<N, E, PAIR>;
   constexpr int T = S::T, TH = S::TH, H = S::H;
   static_assert(!PAIR || (E == 16 && TH == 16 && TW * 2 <= 32), "lane pairs inside a warp");
@@ -506,7 +467,10 @@ __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const doubl
   // row of slot m; frequency held in slot m after the forward transform
   auto row_of = [&](int m) { return PAIR ? 2 * (t + TH * m) + h : t + T * m; };
   auto kx_of = [&](int m) { return PAIR ? kslot<TH, H>(t, h, m) : t + T * m; };
+  // dbg (FM_X_DBG, timing experiments only): bit 0 skips the transforms,
+  // bit 1 the stores
   auto fwd = [&](double2(&v)[E], double2* X) {
+    if (dbg & 1) return;
     if constexpr (PAIR) {
       reg::fft<H, E, -1, 2>(v, X + l + TW * h, 2 * TW, t, twp());
       pair_dit<TH, TW>(*reinterpret_cast<double2(*)[16]>(&v), t, h, twp());
@@ -515,6 +479,7 @@ __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const doubl
     }
   };
   auto inv = [&](double2(&v)[E], double2* X) {
+    if (dbg & 1) return;
     if constexpr (PAIR) {
       pair_dif<TH, TW>(*reinterpret_cast<double2(*)[16]>(&v), t, h, twp());
       reg::fft<H, E, +1, 2>(v, X + l + TW * h, 2 * TW, t, twp());
@@ -535,7 +500,7 @@ __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const doubl
   // boxes of 256 rows x TW columns (the map views the spectrum as
   // [comp * N + x][y][2 kz] doubles)
   auto issue = [&](int T_, int q) {
-    if (threadIdx.x != 0) return;
+    if (threadIdx.x != 0 || (dbg & 4)) return;
     int kz0, y, i;
     tile_base(T_, kz0, y, i);
     bulk::mbar_expect_tx(&bar[q], TILE * 16);
@@ -560,8 +525,10 @@ __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const doubl
     const int Tn = T_ + gridDim.x;  // next tile of this CTA
     double2 s[E], v[E];
     // forward transform of B = xi_y A_1 + xi_z A_2
-    bulk::mbar_wait(&bar[1], par);
-    bulk::mbar_wait(&bar[2], par);
+    if (!(dbg & 4)) {
+      bulk::mbar_wait(&bar[1], par);
+      bulk::mbar_wait(&bar[2], par);
+    }
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const double2 a1 = buf(1)[row_of(m) * TW + l], a2 = buf(2)[row_of(m) * TW + l];
@@ -577,7 +544,7 @@ __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const doubl
 #pragma unroll
     for (int m = 0; m < E; ++m) s[m] = v[m];
     // forward transform of A_0
-    bulk::mbar_wait(&bar[0], par);
+    if (!(dbg & 4)) bulk::mbar_wait(&bar[0], par);
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = buf(0)[row_of(m) * TW + l];
     __syncthreads();
@@ -593,7 +560,8 @@ __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const doubl
       s[m] = make_double2((v[m].x * xix + s[m].x) * iv, (v[m].y * xix + s[m].y) * iv);
     }
     // Bhat_i0 = IFFT(s xi_x); Bhat_i1 = xi_y IFFT(s), Bhat_i2 = xi_z IFFT(s)
-    double2* const rowp = base + l;
+    // (dbg bit 3: every tile stores over tile 0's rows -- L2-resident writes)
+    double2* const rowp = ((dbg & 8) ? spec : base) + l;
 #pragma unroll 1
     for (int q = 0; q < 2; ++q) {
 #pragma unroll
@@ -602,23 +570,47 @@ __global__ void __launch_bounds__(TW * (N / E), 1) k_x_stream(Geo g, const doubl
         v[m] = make_double2(s[m].x * f, s[m].y * f);
       }
       inv(v, buf(0));
-#pragma unroll 1
-      for (int j = q; j < (q == 0 ? 1 : 3); ++j) {
-        const double f = j == 0 ? 1.0 : (j == 1 ? xiy : xiz);
-        if constexpr (!RT) {
+      if (q == 1) {
+        // C0 (the inverse transforms' exchange) is free: refill it before the
+        // last two components are stored, so that neither the fence nor the
+        // next tile's load waits behind those stores
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (Tn < tiles) issue(Tn, 0);
+        // every store reads its own registers (component 1 scaled into s, dead
+        // by now; component 2 in place): a shared temporary would chain each
+        // store behind the previous one's operand read
 #pragma unroll
-          for (int m = 0; m < E; ++m)
-            rowp[(int64_t(j) * N + row_of(m)) * xstride] = make_double2(v[m].x * f, v[m].y * f);
+        for (int m = 0; m < E; ++m) {
+          s[m] = make_double2(v[m].x * xiy, v[m].y * xiy);
+          v[m] = make_double2(v[m].x * xiz, v[m].y * xiz);
+        }
+      }
+      if (dbg & 2) continue;
+      if constexpr (!RT) {
+        double2* const o = rowp + (int64_t(q) * N + row_of(0)) * xstride;
+        const int64_t ms = int64_t(row_of(1) - row_of(0)) * xstride;
+        if (q == 0) {
+#pragma unroll
+          for (int m = 0; m < E; ++m) o[m * ms] = v[m];
         } else {
 #pragma unroll
-          for (int m = 0; m < E; ++m)
-            store_xb(g, nullptr, i * 3 + j, row_of(m), y, kz, make_double2(v[m].x * f, v[m].y * f));
+          for (int m = 0; m < E; ++m) o[m * ms] = s[m];
+#pragma unroll
+          for (int m = 0; m < E; ++m) o[int64_t(N) * xstride + m * ms] = v[m];
+        }
+      } else {
+        if (q == 0) {
+#pragma unroll
+          for (int m = 0; m < E; ++m) store_xb(g, nullptr, i * 3, row_of(m), y, kz, v[m]);
+        } else {
+#pragma unroll
+          for (int m = 0; m < E; ++m) store_xb(g, nullptr, i * 3 + 1, row_of(m), y, kz, s[m]);
+#pragma unroll
+          for (int m = 0; m < E; ++m) store_xb(g, nullptr, i * 3 + 2, row_of(m), y, kz, v[m]);
         }
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    __syncthreads();  // C0 (the inverse transforms' exchange) is free
-    if (Tn < tiles) issue(Tn, 0);
   }
 }
 
@@ -1282,13 +1274,18 @@ void xd_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
 // (2 TW, 1, 256) box -- the x pass's component-tile rows.  Encoded on the
 // host (cuTensorMapEncodeTiled through the runtime's driver entry point, no
 // libcuda link) and cached: the map is a pure function of its arguments.
+// swz128: rows laid out in shared memory with the 128-byte swizzle (16-byte
+// chunk c of row r at chunk c ^ (r & 7); needs 2 TW doubles = 128 bytes).
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, CUtensorMap* out) {
+}  // namespace
+bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, void* out_map) {
+  CUtensorMap* out = static_cast<CUtensorMap*>(out_map);
   struct Entry {
     const void* base;
     int rows, Ny, nzh, TW;
+    bool swz;
     CUtensorMap map;
   };
   static std::mutex mx;
@@ -1305,11 +1302,11 @@ bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, CUtensorM
   if (!enc) return false;
   std::lock_guard<std::mutex> lk(mx);
   for (const Entry& e : cache)
-    if (e.base == base && e.rows == rows && e.Ny == Ny && e.nzh == nzh && e.TW == TW) {
+    if (e.base == base && e.rows == rows && e.Ny == Ny && e.nzh == nzh && e.TW == TW && e.swz == swz128) {
       *out = e.map;
       return true;
     }
-  Entry e{base, rows, Ny, nzh, TW, {}};
+  Entry e{base, rows, Ny, nzh, TW, swz128, {}};
   const cuuint64_t dims[3] = {cuuint64_t(2 * nzh), cuuint64_t(Ny), cuuint64_t(rows)};
   const cuuint64_t strides[2] = {cuuint64_t(nzh) * 16, cuuint64_t(Ny) * nzh * 16};
   const cuuint32_t box[3] = {cuuint32_t(2 * TW), 1, 256};
@@ -1326,19 +1323,20 @@ bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, CUtensorM
                                     : pm == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                               : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (enc(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
+          CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, pr,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   if (cache.size() > 64) cache.clear();
   cache.push_back(e);
   *out = e.map;
   return true;
 }
+namespace {
 
 template <int N, int TW, int E, bool PAIR, bool RT>
 bool xs_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   CUtensorMap map;
-  if (!x_tensor_map(spec, 9 * N, g.Ny, g.nzh, TW, &map)) return false;
+  if (!x_tensor_map(spec, 9 * N, g.Ny, g.nzh, TW, false, &map)) return false;
   const size_t smem = size_t(3) * N * TW * 16;
   constexpr int THREADS = TW * (N / E);
   allow(k_x_stream<N, TW, E, PAIR, RT>, smem);
@@ -1353,7 +1351,11 @@ bool xs_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = (ctx->nzh / TW) * g.Ny * 3;
   const int grid = std::min(tiles, std::max(sms, 1) * per_sm);
-  k_x_stream<N, TW, E, PAIR, RT><<<grid, THREADS, smem, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map);
+  static const int dbg = [] {
+    const char* e = getenv("FM_X_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  k_x_stream<N, TW, E, PAIR, RT><<<grid, THREADS, smem, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map, dbg);
   return true;
 }
 template <int N, int TW, int E, bool PAIR>
@@ -1363,13 +1365,14 @@ bool xs_go(fm_ctx* ctx, const Geo& g, double2* spec) {
 
 // FM_XDIRECT=0: the 512-point x pass falls back to the staged k_x_fast4;
 // FM_XDIRECT=1: k_x_direct (register loads); 2: k_x_stream, TW 8; 3: TW 4
-// (two CTAs per SM); 4 (default): lane-pair k_x_stream, TW 8; 5: E = 8;
-// 6: lane pair, TW 4.  Measured at 512^3 (profiles/r2_x512_ab.md): 4.91 /
-// 5.11 / 7.27 / 4.91 / 4.98 / 7.47 ms against k_x_direct's 5.31.
+// (two CTAs per SM); 4: lane-pair k_x_stream, TW 8 (the routed P > 1 pass);
+// 5: E = 8; 6: lane pair, TW 4; 7 (default): k_x_warp (projection_xw.cu).
+// Measured at 512^3 (profiles/r2_x512_ab.md): 5.81 / 5.31 / 5.11 / 7.27 / 4.91 /
+// 4.98 / 7.47 / 3.75 ms.
 int xdirect_mode() {
   static int v = [] {
     const char* e = getenv("FM_XDIRECT");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 7;
   }();
   return v;
 }
@@ -1393,9 +1396,16 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
     // (two thread groups transforming A_0 and B side by side without spills,
     // k_x_split, measured 6.0 ms at 4 columns / 2 CTAs per SM, 6.8 ms at 8 / 1)
     const int xm = xdirect_mode();
-    if (zc && ctx->nzh % 8 == 0 && xm >= 2 &&
+    static const int xdbg = [] {
+      const char* e = getenv("FM_X_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    if (zc && xm == 7 && g.P == 1 && xw_launch(ctx, g, spec, xdbg)) {
+      done = true;
+      name = "k_x_warp";
+    } else if (zc && ctx->nzh % 8 == 0 && xm >= 2 &&
         (xm == 3   ? xs_go<N, 4, 16, false>(ctx, g, spec)
-         : xm == 4 ? xs_go<N, 8, 16, true>(ctx, g, spec)
+         : (xm == 4 || xm == 7) ? xs_go<N, 8, 16, true>(ctx, g, spec)
          : xm == 5 ? xs_go<N, 8, 8, false>(ctx, g, spec)
          : xm == 6 ? xs_go<N, 4, 16, true>(ctx, g, spec)
                    : xs_go<N, 8, 16, false>(ctx, g, spec))) {

@@ -1,0 +1,370 @@
+// 512-point x pass (projection.cpp:137-155: x FFT, ghat, inverse x FFT), one
+// warp per x-line, all HBM traffic by TMA in both directions.
+//
+// Why (profiles/r2_x512_dbg.md): the streamed pass k_x_stream (one CTA per SM,
+// 8 warps walking its tiles in lock-step) took 4.5 ms at 512^3 whatever was
+// removed from the memory side -- its transforms alone took 3.2 ms (block
+// barriers around every exchange, so the fp64 pipe, shared memory and the
+// barriers take turns), and its register stores blocked the warps for as long
+// as the 192 KB of a tile took to drain.  Here
+//
+//  * a tile is (row i of the tensor, y, 8 kz columns) = 3 components x 512 rows
+//    x 128 bytes; warp w owns column w and holds its whole 512-point line in
+//    registers (lane = 2 t + h: h = 0 the even rows, h = 1 the odd rows, two
+//    256-point half-line transforms of 16 lanes x 16 elements joined by the
+//    lane-pair radix-2 step of fft_pair.cuh).  The half-line exchange goes
+//    through a warp-private 4 KB scratch (real parts, then imaginary parts) with
+//    warp-level syncs only, so the eight warps run out of phase and overlap
+//    each other's fp64, shared-memory and shuffle phases;
+//  * the three 64 KB component buffers are written by tensor-map TMA loads with
+//    the 128-byte swizzle (a warp reads its 16-byte column of 8 consecutive
+//    rows from 8 different bank groups) and results go back IN PLACE into the
+//    warp's own column of a buffer it has already consumed -- no cross-warp
+//    dependency -- from where a TMA store writes the tile back;
+//  * a ninth warp (its warp group gives its registers to the transform warps,
+//    setmaxnreg) issues every load and store: it waits for "all 8 warps have
+//    staged this buffer" (mbarrier), stores it, waits until the store has read
+//    shared memory and refills the buffer with the next tile's component.
+//
+// Buffer schedule per tile k (P, Q, R the three buffers):
+//   P, Q: A_1(k), A_2(k) arrive -> every warp forms B = xi_y A_1 + xi_z A_2 from
+//         its column and writes the PREVIOUS tile's outputs 1 and 2 (still in
+//         registers) into the same columns -> staged -> store -> load
+//         A_1(k+1), A_2(k+1), almost a whole tile ahead of their use;
+//   R:    A_0(k) arrives -> consumed after the first forward transform; output 0
+//         goes back into R after the first inverse transform -> staged -> store
+//         -> load A_0(k+1), two transforms ahead of its use.
+// Same arithmetic, in the same order, as the lane-pair k_x_stream: results are
+// bit-identical (tests/test_gpu_projection.py compares the digests).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "bulk.cuh"
+#include "fft_pair.cuh"
+#include "proj_common.cuh"
+
+namespace fm {
+namespace {
+
+constexpr int XN = 512, XH = 256, XTW = 8, XE = 16, XTH = 16;
+constexpr int XTILE = XN * XTW * 16;          // bytes of one component tile
+constexpr int XSCR = 4096;                    // exchange scratch per warp
+// 8 transform warps (two warp groups) + the copy warp's group: 3 warps per SM
+// sub-partition would cap every thread at 168 registers, so the copy group
+// hands its registers back (setmaxnreg) and the transform groups take 232
+constexpr int XTHREADS = 384;
+constexpr size_t XSMEM = 1024 + 3 * size_t(XTILE) + XTW * size_t(XSCR) + 64;
+
+// Transposing exchange of the two half-lines of a warp: lane (t, h) hands its
+// a[k] to lane (k, h), slot t.  One double per element and round; element p of
+// half-line h sits at double index 2 (p ^ ((p >> 4) & 7)) + h, which makes both
+// the strided writes (p = 16 t + k) and the unit-stride reads (p = t + 16 m)
+// conflict-free for the 16 lanes a 64-bit access serves per wavefront.
+__device__ __forceinline__ void exchange(double2 (&v)[XE], char* wr0, const char* rd0) {
+#pragma unroll
+  for (int part = 0; part < 2; ++part) {
+#pragma unroll
+    for (int k = 0; k < XE; ++k) {
+      char* a = reinterpret_cast<char*>(reinterpret_cast<uintptr_t>(wr0) ^ uintptr_t((k & 7) << 4)) + ((k >> 3) << 7);
+      *reinterpret_cast<double*>(a) = part == 0 ? v[k].x : v[k].y;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < XE; ++m) {
+      const char* a =
+          reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(rd0) ^ uintptr_t((m & 7) << 4)) + (m << 8);
+      const double x = *reinterpret_cast<const double*>(a);
+      if (part == 0) v[m].x = x; else v[m].y = x;
+    }
+    __syncwarp();
+  }
+}
+
+// 256-point transform of a half-line held as v[m] = x[t + 16 m] by its 16
+// lanes: the two Stockham radix-16 stages of reg::fft<256, 16, SIGN, 2> (same
+// butterflies, same twiddles W_512^(2 t r)), exchanged as above.
+template <int SIGN>
+__device__ __forceinline__ void fft256(double2 (&v)[XE], int t, char* wr0, const char* rd0,
+                                       const double2* __restrict__ tw) {
+  reg::Dft<16, SIGN>::run(v);
+  exchange(v, wr0, rd0);
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = reg::tw_mul(v[r], __ldg(&tw[2 * t * r]), SIGN);
+  reg::Dft<16, SIGN>::run(v);
+}
+
+// FM_X_DBG bit 4: cycle counts summed over the CTAs -- [0], [1] transform warp
+// 0 waiting for A_1/A_2 and A_0; [2], [3] store drain (issue -> shared memory
+// read) of P/Q and R; [4], [5] the copy threads waiting for staged buffers;
+// [6] loop cycles of warp 0; [7] tiles.
+__device__ unsigned long long xw_prof[8];
+
+template <bool LSU>
+__global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, double2* spec, int tiles,
+                                                        const __grid_constant__ CUtensorMap tmap, int dbg) {
+  extern __shared__ unsigned char smraw[];
+  // 1024-byte alignment: the swizzle pattern is a function of the address
+  unsigned char* const sm0 =
+      smraw + ((1024u - (bulk::smem_addr(smraw) & 1023u)) & 1023u);
+  unsigned char* const scr0 = sm0 + 3 * XTILE;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(scr0 + XTW * XSCR);
+  uint64_t* const full_p = bars + 0;     // A_1 of a tile has arrived (tx bytes)
+  uint64_t* const full_q = bars + 1;     // A_2
+  uint64_t* const full_r = bars + 2;     // A_0
+  uint64_t* const staged_pq = bars + 3;  // all 8 warps are done with P and Q (count 8)
+  uint64_t* const staged_r = bars + 4;   // all 8 warps have written output 0 into R
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    bulk::mbar_init(full_p, 1);
+    bulk::mbar_init(full_q, 1);
+    bulk::mbar_init(full_r, 1);
+    bulk::mbar_init(staged_pq, XTW);
+    bulk::mbar_init(staged_r, XTW);
+  }
+  __syncthreads();
+  const int kzb = g.nzh / XTW;
+  const int K = blockIdx.x < tiles ? (tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+  // tile -> (kz block fastest, y, row i)
+  auto tile_of = [&](int k, int& kz0, int& y, int& i) {
+    const int T_ = blockIdx.x + k * gridDim.x;
+    kz0 = (T_ % kzb) * XTW;
+    const int r = T_ / kzb;
+    y = r % g.Ny;
+    i = r / g.Ny;
+  };
+
+  if (w >= XTW) {  // --------------------------------------------- copy warps
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::);
+    // warp 8: P (component 1), warp 9: Q (component 2), warp 10: R (component 0)
+    const int buf = w - XTW;
+    if (buf > 2 || K == 0) return;
+    const int q = buf == 2 ? 0 : buf + 1;
+    const bool late = buf < 2;  // P, Q: phase k stages the outputs of tile k - 1
+    uint64_t* const full = buf == 0 ? full_p : (buf == 1 ? full_q : full_r);
+    uint64_t* const staged = buf == 2 ? staged_r : staged_pq;
+    unsigned char* const tile = sm0 + buf * XTILE;
+    auto load = [&](int k) {  // lane 0
+      int kz0, y, i;
+      tile_of(k, kz0, y, i);
+      bulk::mbar_expect_tx(full, XTILE);
+#pragma unroll
+      for (int r0 = 0; r0 < XN; r0 += 256)
+        bulk::tma3d(tile + r0 * 128, &tmap, 2 * kz0, y, (i * 3 + q) * XN + r0, full);
+    };
+    auto store = [&](int k) {
+      int kz0, y, i;
+      tile_of(k, kz0, y, i);
+      if constexpr (LSU) {
+        // 8 lanes per 128-byte row, 4 rows per instruction, straight from the
+        // swizzled tile: the warp blocks on the stores, nobody else does
+        const int rr = lane >> 3, c = lane & 7;
+        const int64_t xstride = int64_t(g.Ny) * g.nzh;
+        double2* const dst = spec + int64_t(i * 3 + q) * XN * xstride + int64_t(y) * g.nzh + kz0 + c;
+#pragma unroll 4
+        for (int it = 0; it < XN / 4; ++it) {
+          const int r = it * 4 + rr;
+          dst[int64_t(r) * xstride] = *reinterpret_cast<const double2*>(tile + (r << 7) + ((c ^ (r & 7)) << 4));
+        }
+        __syncwarp();  // every lane's reads of the tile are done
+        bulk::fence_async_smem();
+      } else if (lane == 0) {
+#pragma unroll
+        for (int r0 = 0; r0 < XN; r0 += 256)
+          bulk::tma3d_store(&tmap, 2 * kz0, y, (i * 3 + q) * XN + r0, tile + r0 * 128);
+        bulk::bulk_commit();
+      }
+    };
+    long long t_idle = 0, t_drain = 0;
+    const bool prof = (dbg & 16) && lane == 0;
+    if (lane == 0) load(0);
+    const int phases = late ? K + 1 : K;
+    for (int k = 0; k < phases; ++k) {
+      const long long c0 = prof ? clock64() : 0;
+      bulk::mbar_wait(staged, k & 1);
+      const long long c1 = prof ? clock64() : 0;
+      const int out = late ? k - 1 : k;  // the tile whose output sits in the buffer
+      if (out >= 0) {
+        store(out);
+        if (!LSU && lane == 0 && out + 1 < K) bulk::bulk_wait_read();
+      }
+      if (prof) t_idle += c1 - c0, t_drain += clock64() - c1;
+      if (lane == 0) {
+        const int next = k + 1;  // tile to load into the buffer now
+        if (next < K) load(next);
+        else if (late && next == K) bulk::mbar_arrive(full);  // nothing to load: free for the flush
+      }
+    }
+    if (prof) atomicAdd(&xw_prof[2 + (buf == 2)], (unsigned long long)t_drain),
+        atomicAdd(&xw_prof[4 + (buf == 2)], (unsigned long long)t_idle);
+    if (!LSU && lane == 0) bulk::bulk_wait_all();  // the stores are performed before the CTA retires
+    return;
+  }
+
+  // --------------------------------------------------------- transform warps
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::);
+  const int h = lane & 1, t = lane >> 1;
+  // this lane's 16 bytes of row (lane + 32 m) of a buffer: column w, swizzled
+  const int col = (lane << 7) + ((w ^ (lane & 7)) << 4);
+  unsigned char* const P = sm0 + col;
+  unsigned char* const Q = sm0 + XTILE + col;
+  unsigned char* const R = sm0 + 2 * XTILE + col;
+  auto at = [](unsigned char* b, int m) { return reinterpret_cast<double2*>(b + (m << 12)); };
+  // exchange addresses of slot 0 (see exchange())
+  char* const scr = reinterpret_cast<char*>(scr0) + w * XSCR;
+  char* const wr0 = scr + (t << 8) + (h << 3) + ((t & 7) << 4);
+  const char* const rd0 = scr + (t << 4) + (h << 3);
+  // The twiddles only depend on the lane: through an opaque copy of the table
+  // pointer each transform reloads them instead of keeping ~90 registers live
+  // across the tile loop.
+  auto twp = [&]() {
+    const double2* p;
+    asm volatile("mov.b64 %0, %1;\n" : "=l"(p) : "l"(tw));
+    return p;
+  };
+  auto fwd = [&](double2(&v)[XE]) {
+    if (dbg & 1) return;
+    fft256<-1>(v, t, wr0, rd0, twp());
+    pair_dit<XTH, 1>(v, t, h, twp());
+  };
+  auto inv = [&](double2(&v)[XE]) {
+    if (dbg & 1) return;
+    pair_dif<XTH, 1>(v, t, h, twp());
+    fft256<+1>(v, t, wr0, rd0, twp());
+  };
+  double2 X[XE], v[XE];
+  double xiy_p = 0.0, xiz_p = 0.0;
+  const bool prof = (dbg & 16) && w == 0 && lane == 0;
+  long long t_pq = 0, t_r = 0;
+  const long long t_begin = prof ? clock64() : 0;
+  for (int k = 0; k < K; ++k) {
+    int kz0, y, i;
+    tile_of(k, kz0, y, i);
+    const int kz = kz0 + w;
+    const int yg = g.y0 + y;
+    const int qy = freq_of(yg, g.Nyg), qz = freq_of(kz, g.Nz);
+    const bool nyq_yz = ((g.Nyg % 2 == 0) && (yg == g.Nyg / 2)) || ((g.Nz % 2 == 0) && (kz == g.Nz / 2));
+    const double xiy = qy * g.invL[1], xiz = qz * g.invL[2];
+    // B = xi_y A_1 + xi_z A_2 from this warp's column; the previous tile's
+    // outputs 1 and 2 go back into the same 16 bytes
+    {
+      const long long c0 = prof ? clock64() : 0;
+      bulk::mbar_wait(full_p, k & 1);
+      bulk::mbar_wait(full_q, k & 1);
+      if (prof) t_pq += clock64() - c0;
+    }
+#pragma unroll
+    for (int m = 0; m < XE; ++m) {
+      const double2 a1 = *at(P, m), a2 = *at(Q, m);
+      X[m] = make_double2(fma(a1.x, xiy, a2.x * xiz), fma(a1.y, xiy, a2.y * xiz));
+    }
+    if (k > 0) {
+#pragma unroll
+      for (int m = 0; m < XE; ++m) {
+        *at(P, m) = make_double2(v[m].x * xiy_p, v[m].y * xiy_p);
+        *at(Q, m) = make_double2(v[m].x * xiz_p, v[m].y * xiz_p);
+      }
+    }
+    bulk::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) bulk::mbar_arrive(staged_pq);
+    fwd(X);
+    // forward transform of A_0
+    {
+      const long long c0 = prof ? clock64() : 0;
+      bulk::mbar_wait(full_r, k & 1);
+      if (prof) t_r += clock64() - c0;
+    }
+#pragma unroll
+    for (int m = 0; m < XE; ++m) v[m] = *at(R, m);
+    fwd(v);
+    // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
+#pragma unroll
+    for (int m = 0; m < XE; ++m) {
+      const int kx = kslot<XTH, XH>(t, h, m);
+      const double xix = freq_of(kx, XN) * g.invL[0];
+      const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
+      const bool zero = norm2 == 0.0 || nyq_yz || kx == XN / 2;
+      const double iv = zero ? 0.0 : 1.0 / norm2;
+      X[m] = make_double2((v[m].x * xix + X[m].x) * iv, (v[m].y * xix + X[m].y) * iv);
+    }
+    // Bhat_i0 = IFFT(s xi_x) -> back into R
+#pragma unroll
+    for (int m = 0; m < XE; ++m) {
+      const double f = freq_of(kslot<XTH, XH>(t, h, m), XN) * g.invL[0];
+      v[m] = make_double2(X[m].x * f, X[m].y * f);
+    }
+    inv(v);
+#pragma unroll
+    for (int m = 0; m < XE; ++m) *at(R, m) = v[m];
+    bulk::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) bulk::mbar_arrive(staged_r);
+    // IFFT(s): Bhat_i1 = xi_y IFFT(s), Bhat_i2 = xi_z IFFT(s), written at the
+    // start of the next tile (or below, after the last one)
+#pragma unroll
+    for (int m = 0; m < XE; ++m) v[m] = make_double2(X[m].x * 1.0, X[m].y * 1.0);
+    inv(v);
+    xiy_p = xiy;
+    xiz_p = xiz;
+  }
+  if (K > 0) {
+    bulk::mbar_wait(full_p, K & 1);  // the stores of tile K - 2's outputs have read P and Q
+    bulk::mbar_wait(full_q, K & 1);
+#pragma unroll
+    for (int m = 0; m < XE; ++m) {
+      *at(P, m) = make_double2(v[m].x * xiy_p, v[m].y * xiy_p);
+      *at(Q, m) = make_double2(v[m].x * xiz_p, v[m].y * xiz_p);
+    }
+    bulk::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) bulk::mbar_arrive(staged_pq);
+  }
+  if (prof) {
+    atomicAdd(&xw_prof[0], (unsigned long long)t_pq);
+    atomicAdd(&xw_prof[1], (unsigned long long)t_r);
+    atomicAdd(&xw_prof[6], (unsigned long long)(clock64() - t_begin));
+    atomicAdd(&xw_prof[7], (unsigned long long)K);
+  }
+}
+
+}  // namespace
+
+bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
+  if (g.Nx != XN || g.P != 1 || g.nzh % XTW != 0) return false;
+  CUtensorMap map;
+  if (!x_tensor_map(spec, 9 * XN, g.Ny, g.nzh, XTW, true, &map)) return false;
+  // FM_XW_TMA_STORE=0: the copy warps write the tiles back with their own
+  // (coalesced, blocking) stores instead of TMA stores.  Measured at 512^3:
+  // 6.64 against 3.75 ms -- one warp per buffer cannot keep 64 KB of stores
+  // in flight next to the transform warps.
+  static const bool tma_store = [] {
+    const char* e = getenv("FM_XW_TMA_STORE");
+    return !e || atoi(e) != 0;
+  }();
+  const void* kern = tma_store ? reinterpret_cast<const void*>(k_x_warp<false>) : reinterpret_cast<const void*>(k_x_warp<true>);
+  set_smem_limit(kern, int(XSMEM));
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = (g.nzh / XTW) * g.Ny * 3;
+  const int grid = std::min(tiles, std::max(sms, 1));
+  if (tma_store) k_x_warp<false><<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map, dbg);
+  else k_x_warp<true><<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map, dbg);
+  if (dbg & 16) {  // timing experiments only: per-tile averages to stderr
+    unsigned long long h[8] = {}, z[8] = {};
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpyFromSymbol(h, xw_prof, sizeof(h));
+    cudaMemcpyToSymbol(xw_prof, z, sizeof(z));
+    const double n = double(h[7] ? h[7] : 1);
+    fprintf(stderr,
+            "k_x_warp cycles/tile: loop %.0f  wait A1A2 %.0f  wait A0 %.0f | drain PQ %.0f R %.0f | copy idle PQ %.0f R "
+            "%.0f\n",
+            h[6] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n);
+  }
+  return true;
+}
+
+}  // namespace fm

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+for d in 0 1 2 3; do for m in 4 6 2; do
+FM_X_DBG=$d FM_XDIRECT=$m python scripts/x_stride.py 512x512x512 5 | python -c "
+import sys,json
+for l in sys.stdin:
+    r=json.loads(l); print(json.dumps({'dbg':$d,'mode':$m,'x_ms':r['passes_ms'][2],'x_frac':r['pass_frac'][2]}))"
+done; done > gpurun_out/x_dbg_r2k.jsonl 2>&1; cat gpurun_out/x_dbg_r2k.jsonl

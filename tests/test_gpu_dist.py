@@ -17,7 +17,9 @@ pytestmark = pytest.mark.gpu
                                    ((128, 64, 32), 8), ((12, 10, 14), 2), ((16, 24, 9), 4),
                                    ((256, 256, 32), 8),
                                    # long routed x lines (512: direct lane-pair pass, 1024: 4-column tiles) and y lines
-                                   ((512, 32, 16), 4), ((1024, 16, 32), 2), ((32, 512, 16), 2),
+                                   # (P = 1 at 512: the warp-per-line TMA pass k_x_warp, one tile per CTA and,
+                                   # at 64 x 32, two to three tiles per CTA, against the routed k_x_stream)
+                                   ((512, 32, 16), 4), ((512, 64, 32), 2), ((1024, 16, 32), 2), ((32, 512, 16), 2),
                                    ((16, 1024, 32), 4)])
 def test_virtual_ranks_bitwise_equal(pts, P):
     A = M.uniform_field(pts, 9, seed=3)
