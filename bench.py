@@ -257,26 +257,30 @@ def cpu_baseline_sample(N):
             "newton_solve": newton}
 
 
-def config3_matvec(local, hbm, steps=5):
-    """BASELINE config 3's operator on one GPU: the 512^3 finite-strain J2
+def config3_matvec(local, hbm, steps=5, dist=None, world=1, rank=0):
+    """BASELINE config 3's operator on the grid the 8-GPU target names: the 512^3 J2
     matvec with the compact eigenbasis tangent (45 slabs; K4 would not fit
     next to the J2 state), random periodic spheres (radius 12, fraction 0.25,
     seed 3), tangent at F_bar(t=1) = I + 0.005 e_x e_y; per-pass CUDA-event
     times and each pass's roofline fraction (pass 1: 45 + 9 + 9 slabs read +
-    9 written = 576 B/voxel; passes 2-5: 144)."""
+    9 written = 576 B/voxel; passes 2-5: 144).  dist = (world, rank, nccl id):
+    the slab-decomposed operator (this rank's x-slab), timed between barriers,
+    max over ranks; FM_TRANSPOSE selects the transpose arm of the context."""
     import torch
     from paper_1603_08893_b200 import abi
     from paper_1603_08893_b200 import microstructure as M
     N = 512
-    n = N ** 3
+    ng = N ** 3
     pg, frac, count = M.random_spheres(N, 12, 0.25, 3)
     phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
               M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
     lam, mu, ty, h = M.bind_parameters(pg, phases)
     del pg
     pb = [45 * 8 + 72 + 72, 144, 144, 144, 144]
-    with abi.Context((N, N, N), 3, device=local) as ctx:
-        model = abi.Model(ctx, "simo", lam, mu, ty, h, compact=True)
+    with abi.Context((N, N, N), 3, device=local, dist=dist) as ctx:
+        n = ctx.n  # nodes held here: the x-slab when distributed
+        lo = rank * n if dist else 0
+        model = abi.Model(ctx, "simo", lam[lo:lo + n], mu[lo:lo + n], ty[lo:lo + n], h[lo:lo + n], compact=True)
         del lam, mu, ty, h
         F = ctx.field(9)
         tF = torch.as_tensor(F, device=f"cuda:{local}")
@@ -286,13 +290,14 @@ def config3_matvec(local, hbm, steps=5):
         tF[n:2 * n] = 0.005
         dF = ctx.field(9)
         g = torch.Generator(device=f"cuda:{local}")
-        g.manual_seed(3)
+        g.manual_seed(3 + rank)
         torch.as_tensor(dF, device=f"cuda:{local}").uniform_(-1, 1, generator=g)
         torch.cuda.synchronize()
         P, out = ctx.field(9), ctx.field(9)
         model.evaluate(F, P)
         model.apply(dF, out)
         ctx.sync()
+        barrier(world)
         ctx.profile(True)
         stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -301,7 +306,8 @@ def config3_matvec(local, hbm, steps=5):
             model.apply(dF, out)
         e1.record(stream)
         e1.synchronize()
-        ms = e0.elapsed_time(e1) / steps
+        barrier(world)
+        ms = max_over_ranks(e0.elapsed_time(e1) / steps, world)
         pass_ms, calls = ctx.profile_read()
         ctx.profile(False)
         per = pass_ms / max(calls, 1)
@@ -309,10 +315,12 @@ def config3_matvec(local, hbm, steps=5):
         model.close()
     return {"workload": "config3 operator: 512^3 J2 (compact eigenbasis tangent) matvec at F_bar(t=1), spheres r 12, "
                         f"fraction {frac:.4f}, {count} spheres, seed 3",
-            "ms": ms, "voxel_per_s": n / (ms * 1e-3), "steps": steps,
-            "bytes_per_voxel": sum(pb), "frac": sum(pb) * n / (ms * 1e-3) / 1e9 / hbm,
+            "ms": ms, "voxel_per_s": ng / (ms * 1e-3), "steps": steps, "n_gpus": world,
+            "transposes": None if not dist else ("staged ncclSend/ncclRecv all-to-all" if os.environ.get("FM_TRANSPOSE")
+                                                 else "fused NVLink peer stores"),
+            "bytes_per_voxel": sum(pb), "frac": sum(pb) * ng / world / (ms * 1e-3) / 1e9 / hbm,
             "passes_ms": [float(x) for x in per],
-            "pass_frac": [b * n / (x * 1e-3) / 1e9 / hbm for b, x in zip(pb, per)],
+            "pass_frac": [b * ng / world / (x * 1e-3) / 1e9 / hbm for b, x in zip(pb, per)],
             "kernels": names}
 
 
@@ -557,6 +565,25 @@ def main():
             c3 = config3_matvec(local, hbm)
         except Exception as e:  # reported, never silent
             c3 = {"error": str(e)[:200]}
+    elif slab and not args.no_config3:
+        # N > 1: the slab-decomposed 512^3 operator with both transpose arms
+        # (the driver's efficiency for the 8-GPU target = these ms against the N = 1 run's)
+        import torch.distributed as tdist
+        c3 = {}
+        for arm, env in (("peer_stores", None), ("nccl_all_to_all", "nccl")):
+            try:
+                if env:
+                    os.environ["FM_TRANSPOSE"] = env
+                uid3 = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+                if rank == 0:
+                    uid3.copy_(torch.frombuffer(bytearray(abi.nccl_unique_id()), dtype=torch.uint8))
+                tdist.broadcast(uid3, 0)
+                c3[arm] = config3_matvec(local, hbm, dist=(world, rank, bytes(uid3.cpu().numpy())), world=world,
+                                         rank=rank)
+            except Exception as e:
+                c3[arm] = {"error": str(e)[:200]}
+            finally:
+                os.environ.pop("FM_TRANSPOSE", None)
     dchk = None
     if slab:
         try:

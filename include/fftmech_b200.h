@@ -126,6 +126,16 @@ int fm_nccl_unique_id(void* out, int bytes);
  * by side, the same transpose-fused kernels storing across them) -- validates
  * the decomposition against P = 1 bit for bit. */
 int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P);
+/* How the two slab transposes of a P > 1 projection are done (replaces the
+ * single-process FFTW plans of projection.cpp:106-119 across ranks):
+ * 0 (default) fused into the forward y pass and the x pass as stores into the
+ * peers' buffers (NVLink, CUDA IPC); 1 the textbook form -- local passes,
+ * pack, grouped ncclSend/ncclRecv all-to-all, unpack (SURVEY.md §8(e) steps 2
+ * and 4) -- kept as the arm to measure the fused form against and for ranks
+ * without peer access.  Distributed contexts take their mode from the
+ * environment (FM_TRANSPOSE=nccl) at creation; virtual-rank contexts can
+ * switch at any time. */
+int fm_ctx_set_transpose(fm_ctx* ctx, int mode);
 int fm_ctx_ranks(const fm_ctx* ctx, int* nranks, int* rank, int* virtual_mode);
 /* Route of the fused transpose (host only, no device needed), the same
  * function the kernels evaluate.  dir +1 (forward y pass of x-slab `src`):

@@ -116,6 +116,7 @@ _SIGS = {
     "fm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_int]),
     "fm_model_set_tangent_form": (C.c_int, [_P, _P, C.c_int]),
     "fm_ctx_set_virtual_ranks": (C.c_int, [_P, C.c_int]),
+    "fm_ctx_set_transpose": (C.c_int, [_P, C.c_int]),
     "fm_ctx_ranks": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fm_dist_route": (C.c_int, [C.c_int] * 11 + [C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
 }
@@ -197,6 +198,10 @@ class Context:
     def set_virtual_ranks(self, P):
         """Run the slab-decomposed projection with P ranks emulated on this device."""
         self.check(lib().fm_ctx_set_virtual_ranks(self.h, P))
+
+    def set_transpose(self, mode):
+        """0: slab transposes fused into passes 2 and 3 as peer stores; 1: staged all-to-all."""
+        self.check(lib().fm_ctx_set_transpose(self.h, mode))
 
     def ranks(self):
         nr, r, v = C.c_int(), C.c_int(), C.c_int()

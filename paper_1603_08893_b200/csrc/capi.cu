@@ -222,6 +222,7 @@ int fm_ctx_destroy(fm_ctx* ctx) {
   if (ctx->d_epi2) cudaFree(ctx->d_epi2);
   if (ctx->d_fold) cudaFree(ctx->d_fold);
   if (ctx->spec2) cudaFree(ctx->spec2);
+  if (ctx->spec3) cudaFree(ctx->spec3);
   if (ctx->d_gather) cudaFree(ctx->d_gather);
   dist_destroy(ctx);
   if (ctx->d_scal) cudaFree(ctx->d_scal);
@@ -246,8 +247,33 @@ static int setup_slabs(fm_ctx* ctx, int P) {
     const size_t bytes = size_t(ctx->spec_rank_elems) * (ctx->virt ? P : 1) * sizeof(double2);
     FM_CUDA(ctx, cudaMalloc(&ctx->spec2, bytes));
   }
+  if (P > 1 && ctx->transpose == 1 && !ctx->spec3) {
+    const size_t bytes = size_t(ctx->spec_rank_elems) * (ctx->virt ? P : 1) * sizeof(double2);
+    FM_CUDA(ctx, cudaMalloc(&ctx->spec3, bytes));
+  }
   if (!ctx->d_gather) FM_CUDA(ctx, cudaMalloc(&ctx->d_gather, sizeof(double) * 64 * size_t(P)));
   return dist_setup_routes(ctx);
+}
+
+// FM_TRANSPOSE=nccl (or "staged"): new contexts start with the staged
+// all-to-all transposes instead of the fused peer stores.
+static int transpose_from_env() {
+  const char* e = getenv("FM_TRANSPOSE");
+  return e && (!strcmp(e, "nccl") || !strcmp(e, "staged") || !strcmp(e, "1")) ? 1 : 0;
+}
+
+int fm_ctx_set_transpose(fm_ctx* ctx, int mode) {
+  FM_DEVICE_SCOPE(ctx);
+  if (!ctx || (mode != 0 && mode != 1)) return FM_E_INVALID;
+  if (ctx->transpose == mode) return FM_OK;
+  if (distributed(ctx))  // the peer mappings are made (or not) when the context is created
+    return set_error(ctx, FM_E_INVALID, "the transpose mode of a distributed context is fixed at creation (FM_TRANSPOSE)");
+  ctx->transpose = mode;
+  if (ctx->P > 1) {  // virtual ranks already set up: add the staging buffer
+    FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return setup_slabs(ctx, ctx->P);
+  }
+  return FM_OK;
 }
 
 int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P) {
@@ -283,6 +309,7 @@ int fm_ctx_create_dist(int dim, const int32_t* points, const double* lengths, in
   ctx->spec = nullptr;
   const size_t rank_elems = size_t(ctx->ncomp) * (ctx->Nx / nranks) * ctx->Ny * ctx->nzh;
   if (cudaMalloc(&ctx->spec, rank_elems * sizeof(double2)) != cudaSuccess) st = FM_E_OOM;
+  ctx->transpose = transpose_from_env();
   if (!st) st = dist_init_nccl(ctx, nccl_unique_id, nranks, rank);
   if (!st) st = setup_slabs(ctx, nranks);
   if (st) {

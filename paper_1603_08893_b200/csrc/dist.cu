@@ -28,6 +28,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <string>
 
 #include <vector>
 
@@ -50,9 +51,80 @@ int rank_barrier(fm_ctx* ctx) {
   return nccl_check(ctx, ncclAllReduce(flag, flag, 1, ncclDouble, ncclSum, comm, ctx->stream), "ncclAllReduce");
 }
 
+// Staged transposes, the textbook form: the y
+// and x passes run locally and in place; between them every rank packs, per
+// destination d, the block of its spectrum that d owns next into a dense
+// staging area (strided 2-D copies), exchanges the blocks with grouped
+// ncclSend / ncclRecv over NVLink, and unpacks.  With XY = Xl Yl nzh:
+//   forward  A_r [c][xl][y][kz]  --pack-->  S_r [d][c][xl][yl][kz]
+//            --all-to-all-->  B_d [c][r Xl + xl][yl][kz]      (received in place)
+//   backward B_d [c][x][yl][kz] = [c][s][xl][yl][kz]          (sent in place)
+//            --all-to-all-->  S_s [d][c][xl][yl][kz]  --unpack-->  A_s [c][xl][d Yl + yl][kz]
+// The send / receive pairs order the ranks; no barrier is needed.  In the
+// virtual mode the all-to-all is the same set of block copies on this device.
+// This is the arm the peer-store transposes are measured against.
+int dist_transpose_staged(fm_ctx* ctx, int dir) {
+  const int P = ctx->P, nc = ctx->ncomp;
+  const int64_t Xl = ctx->Nx / P, Yl = ctx->Ny / P, nzh = ctx->nzh, Ny = ctx->Ny;
+  const int64_t XY = Xl * Yl * nzh;                  // complex elements of one (component, source, destination) block
+  const size_t row = size_t(Yl) * nzh * sizeof(double2);     // one (c, xl) row of a block
+  const size_t pitch_a = size_t(Ny) * nzh * sizeof(double2);  // the same row inside A
+  const int r0 = ctx->virt ? 0 : ctx->rank, r1 = ctx->virt ? P : ctx->rank + 1;
+  auto A = [&](int r) { return ctx->spec + (ctx->virt ? int64_t(r) * ctx->spec_rank_elems : 0); };
+  auto B = [&](int r) { return ctx->spec2 + (ctx->virt ? int64_t(r) * ctx->spec_rank_elems : 0); };
+  auto S = [&](int r) { return ctx->spec3 + (ctx->virt ? int64_t(r) * ctx->spec_rank_elems : 0); };
+  if (!ctx->spec3) return set_error(ctx, FM_E_INVALID, "staged transpose without its staging buffer");
+  ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl);
+  if (dir > 0) {
+    for (int r = r0; r < r1; ++r)
+      for (int d = 0; d < P; ++d)
+        FM_CUDA(ctx, cudaMemcpy2DAsync(S(r) + int64_t(d) * nc * XY, row, A(r) + int64_t(d) * Yl * nzh, pitch_a, row,
+                                       size_t(nc) * Xl, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->virt) {
+      for (int r = 0; r < P; ++r)
+        for (int d = 0; d < P; ++d)
+          for (int c = 0; c < nc; ++c)
+            FM_CUDA(ctx, cudaMemcpyAsync(B(d) + (int64_t(c) * P + r) * XY, S(r) + (int64_t(d) * nc + c) * XY,
+                                         size_t(XY) * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      const int r = ctx->rank;
+      if (int st = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart")) return st;
+      for (int d = 0; d < P; ++d)
+        for (int c = 0; c < nc; ++c) {
+          ncclSend(S(r) + (int64_t(d) * nc + c) * XY, size_t(2 * XY), ncclDouble, d, comm, ctx->stream);
+          ncclRecv(B(r) + (int64_t(c) * P + d) * XY, size_t(2 * XY), ncclDouble, d, comm, ctx->stream);
+        }
+      if (int st = nccl_check(ctx, ncclGroupEnd(), "ncclGroupEnd(forward transpose)")) return st;
+    }
+  } else {
+    if (ctx->virt) {
+      for (int d = 0; d < P; ++d)
+        for (int s = 0; s < P; ++s)
+          for (int c = 0; c < nc; ++c)
+            FM_CUDA(ctx, cudaMemcpyAsync(S(s) + (int64_t(d) * nc + c) * XY, B(d) + (int64_t(c) * P + s) * XY,
+                                         size_t(XY) * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      const int d = ctx->rank;
+      if (int st = nccl_check(ctx, ncclGroupStart(), "ncclGroupStart")) return st;
+      for (int s = 0; s < P; ++s)
+        for (int c = 0; c < nc; ++c) {
+          ncclSend(B(d) + (int64_t(c) * P + s) * XY, size_t(2 * XY), ncclDouble, s, comm, ctx->stream);
+          ncclRecv(S(d) + (int64_t(s) * nc + c) * XY, size_t(2 * XY), ncclDouble, s, comm, ctx->stream);
+        }
+      if (int st = nccl_check(ctx, ncclGroupEnd(), "ncclGroupEnd(backward transpose)")) return st;
+    }
+    for (int r = r0; r < r1; ++r)
+      for (int d = 0; d < P; ++d)
+        FM_CUDA(ctx, cudaMemcpy2DAsync(A(r) + int64_t(d) * Yl * nzh, pitch_a, S(r) + int64_t(d) * nc * XY, row, row,
+                                       size_t(nc) * Xl, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return FM_OK;
+}
+
 int dist_setup_routes(fm_ctx* ctx) {
   const int P = ctx->P;
   if (P > kMaxRanks) return set_error(ctx, FM_E_UNSUPPORTED, "more slab ranks than kMaxRanks");
+  if (ctx->transpose == 1) return FM_OK;  // staged all-to-all: nothing is mapped
   if (!ctx->d_dst_a) FM_CUDA(ctx, cudaMalloc(&ctx->d_dst_a, sizeof(double2*) * kMaxRanks));
   if (!ctx->d_dst_b) FM_CUDA(ctx, cudaMalloc(&ctx->d_dst_b, sizeof(double2*) * kMaxRanks));
   std::vector<double2*> a(kMaxRanks, nullptr), b(kMaxRanks, nullptr);
@@ -66,8 +138,11 @@ int dist_setup_routes(fm_ctx* ctx) {
     // the communicator), map every peer's buffers into this process
     struct Handles {
       cudaIpcMemHandle_t a, b;
+      char bus[32];  // PCI bus id of the rank's device
     };
     Handles mine;
+    std::memset(&mine, 0, sizeof(mine));
+    FM_CUDA(ctx, cudaDeviceGetPCIBusId(mine.bus, int(sizeof(mine.bus)), ctx->device));
     FM_CUDA(ctx, cudaIpcGetMemHandle(&mine.a, ctx->spec));
     FM_CUDA(ctx, cudaIpcGetMemHandle(&mine.b, ctx->spec2));
     char* d_h = nullptr;
@@ -86,6 +161,29 @@ int dist_setup_routes(fm_ctx* ctx) {
       st = set_error(ctx, FM_E_CUDA, "IPC handle download");
     cudaFree(d_h);
     if (st) return st;
+    // every peer must be a device this process can map: same node, visible,
+    // peer access possible -- checked before any handle is opened
+    for (int r = 0; r < P; ++r) {
+      if (r == ctx->rank) continue;
+      all[r].bus[sizeof(all[r].bus) - 1] = 0;
+      int dev = -1, ok = 0;
+      if (cudaDeviceGetByPCIBusId(&dev, all[r].bus) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(ctx, FM_E_UNSUPPORTED,
+                         "slab rank " + std::to_string(r) + " runs on device " + all[r].bus +
+                             ", which this process cannot see: the peer-store transposes need every rank's "
+                             "device visible (or use FM_TRANSPOSE=nccl)");
+      }
+      if (dev == ctx->device)
+        return set_error(ctx, FM_E_UNSUPPORTED, "slab ranks " + std::to_string(ctx->rank) + " and " +
+                                                    std::to_string(r) + " share device " + all[r].bus);
+      if (cudaDeviceCanAccessPeer(&ok, ctx->device, dev) != cudaSuccess || !ok) {
+        cudaGetLastError();
+        return set_error(ctx, FM_E_UNSUPPORTED,
+                         "no peer access from device " + std::string(mine.bus) + " to " + all[r].bus +
+                             " (slab rank " + std::to_string(r) + "): use FM_TRANSPOSE=nccl");
+      }
+    }
     for (int r = 0; r < P; ++r) {
       if (r == ctx->rank) {
         a[r] = ctx->spec;

@@ -97,6 +97,8 @@ struct fm_ctx {
   double2* d_tw = nullptr;        // all twiddle tables
   double2* spec = nullptr;        // ncomp * Nx * Ny * nzh  (A: z/y side; also the x-pass buffer)
   double2* spec2 = nullptr;       // x-pass input B (y-slab), only when P > 1
+  double2* spec3 = nullptr;       // pack / unpack staging of the staged all-to-all transposes (transpose == 1)
+  int transpose = 0;              // P > 1: 0 = transposes fused into passes 2, 3 as peer stores, 1 = staged all-to-all
   // slab decomposition over P ranks; P = 1: single device
   int P = 1, rank = 0;
   bool virt = false;              // all P ranks emulated on this one device
@@ -250,6 +252,10 @@ int cg_small_run(fm_ctx* ctx, const ProArgs& op, double* x, double* r, double* p
 int rank_barrier(fm_ctx* ctx);
 // route tables of the fused transpose: virtual ranks, or IPC-mapped peers
 int dist_setup_routes(fm_ctx* ctx);
+// staged slab transposes (FM_TRANSPOSE=nccl / fm_ctx_set_transpose(ctx, 1)):
+// x-slabs A -> y-slabs B after a local forward y pass (dir +1), and back
+// before the inverse y pass (dir -1)
+int dist_transpose_staged(fm_ctx* ctx, int dir);
 // Ordered cross-rank sum of `count` device scalars (no-op unless distributed).
 int combine_ranks(fm_ctx* ctx, double* d_vals, int count);
 int combine_min_u64(fm_ctx* ctx, unsigned long long* d_key);

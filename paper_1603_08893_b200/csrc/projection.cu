@@ -601,13 +601,20 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   prof_mark(ctx);
   // P > 1: the forward y pass stores into the ranks' x-pass inputs B, the x
   // pass into the ranks' spectra A (the fused slab transposes, dist.cu)
+  // (transpose == 1, the A/B arm: both passes run locally in place and staged
+  // all-to-all transposes sit between them, dist_transpose_staged)
+  const bool staged = ctx->P > 1 && ctx->transpose == 1;
+  auto local = [&](Geo g) {  // the pass's own extents, stores in place
+    if (staged) g.P = 1;
+    return g;
+  };
   for (int r = r0; r < r1; ++r)
-    if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), -1, spec_a(ctx, r), spec_a(ctx, r))) return st;
-  if (int st = rank_barrier(ctx)) return st;
+    if (int st = pass_y<TD>(ctx, local(geo_zy(ctx, r)), -1, spec_a(ctx, r), spec_a(ctx, r))) return st;
+  if (int st = staged ? dist_transpose_staged(ctx, +1) : rank_barrier(ctx)) return st;
   prof_mark(ctx);
   for (int r = r0; r < r1; ++r)
-    if (int st = pass_x<TD>(ctx, geo_x(ctx, r), spec_b(ctx, r))) return st;
-  if (int st = rank_barrier(ctx)) return st;
+    if (int st = pass_x<TD>(ctx, local(geo_x(ctx, r)), spec_b(ctx, r))) return st;
+  if (int st = staged ? dist_transpose_staged(ctx, -1) : rank_barrier(ctx)) return st;
   prof_mark(ctx);
   for (int r = r0; r < r1; ++r)
     if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), +1, spec_a(ctx, r), spec_a(ctx, r))) return st;

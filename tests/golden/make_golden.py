@@ -170,8 +170,45 @@ def config3_reduced():
     print("config3_64", time.time() - t, rec)
 
 
+def _config3_64_run(args):
+    which, eps = args
+    O.set_threads(1)
+    N, r = 64, 2
+    pg, _, _ = M.random_spheres(N, r, 0.25, 3)
+    phases = [M.PlasticParams(M.ElasticParams(1.0, 0.3), 0.003, 0.003),
+              M.PlasticParams(M.ElasticParams(2.0, 0.3), 0.006, 0.006)]
+    lam, mu, ty, h = M.bind_parameters(pg, phases)
+    if which == "lam":
+        lam = lam * (1.0 + eps)
+    elif which == "mu":
+        mu = mu * (1.0 + eps)
+    _, _, reps, st, _ = O.run_program((N, N, N), 3, 1, lam, mu, M.simple_shear_program(0.05, 10, 3)[:1],
+                                      ty0=ty, hard=h)
+    return st, reps[0]["passes"], reps[0]["cg_it"]
+
+
+def config3_64_band():
+    """The oracle's own CG counts of config3_64's increment 1 under four 1e-15
+    relative perturbations of lambda / mu, added to config3_64.json as
+    `band`: the envelope tests/test_gpu_config3_reduced.py allows on top of
+    BASELINE's +-1 is measured on the case itself."""
+    import json
+    from multiprocessing import Pool
+    with Pool(4) as pool:
+        runs = pool.map(_config3_64_run, PERTURB[:4])
+    path = os.path.join(HERE, "config3_64.json")
+    rec = json.load(open(path))
+    rec["band"] = [{"perturb": list(pw), "status": st, "passes": npass, "cg_it": cg}
+                   for pw, (st, npass, cg) in zip(PERTURB[:4], runs)]
+    with open(path, "w") as f:
+        json.dump(rec, f, indent=1)
+    print("config3_64 band", rec["band"])
+
+
 if __name__ == "__main__" and "config3" in sys.argv[1:]:
     config3_reduced()
+if __name__ == "__main__" and "config3_64_band" in sys.argv[1:]:
+    config3_64_band()
 
 
 # ---------------------------------------------------------------------------

@@ -3,7 +3,7 @@ random periodic spheres to volume fraction 0.25, J2 phases 1x / 2x, simple
 shear to gamma 0.05 in 10 increments), first two increments, against the CPU
 oracle's run record (tests/golden/config3_64.json, tests/golden/make_golden.py
 config3): increment 1 converges in the same number of Newton passes with CG
-counts in the J2 sensitivity band, and increment 2 stops with
+counts within +-1 plus the band the oracle shows on this very case, and increment 2 stops with
 InvertedElement at the same node on the GPU and in the oracle (DESIGN.md §7b:
 the prescribed load stepping does not converge with the reference algorithm)."""
 import json
@@ -37,9 +37,12 @@ def test_config3_reduced_matches_oracle_record(compact):
         model.close()
     ref1 = rec["increments"][0]
     assert rep1["passes"] == ref1["passes"]
-    # +-1 plus the J2 band: the oracle's own counts move by up to 6 under
-    # 1e-15 relative input perturbations on the 16^3 J2 case
+    # BASELINE's +-1 plus the oracle's own deviation from itself under 1e-15
+    # relative perturbations of lambda / mu, measured on THIS case
+    # (tests/golden/make_golden.py config3_64_band; it is zero here)
+    band = max(abs(a - b) for run in rec["band"] for a, b in zip(run["cg_it"], ref1["cg_it"]))
+    assert all(run["status"] == 0 and run["passes"] == ref1["passes"] for run in rec["band"])
     for a, b in zip(rep1["cg_it"], ref1["cg_it"]):
-        assert abs(a - b) <= 1 + 6, (rep1["cg_it"], ref1["cg_it"])
+        assert abs(a - b) <= 1 + band, (rep1["cg_it"], ref1["cg_it"], band)
     assert e.value.status == 4  # FM_E_INVERTED -> InvertedElement(node)
     assert e.value.info.get("node") == rec["increments"][1]["err_node"], (e.value.info, rec["increments"][1])

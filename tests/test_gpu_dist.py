@@ -37,6 +37,32 @@ def test_virtual_ranks_bitwise_equal(pts, P):
     assert np.array_equal(m1, mp)
 
 
+@pytest.mark.parametrize("pts,P", [((64, 64, 64), 2), ((64, 64, 64), 8), ((12, 10, 14), 2), ((16, 24, 9), 4),
+                                   ((128, 64, 32), 8), ((512, 64, 32), 2), ((32, 512, 16), 2)])
+def test_staged_all_to_all_bitwise_equal(pts, P):
+    """The A/B arm (fm_ctx_set_transpose(ctx, 1), FM_TRANSPOSE=nccl on devices):
+    local y and x passes with pack / all-to-all / unpack transposes between
+    them.  In the virtual mode the all-to-all is the same block copies on one
+    device, so the pack and unpack index maps are checked exactly: bit-equal to
+    P = 1 and to the fused peer-store form."""
+    A = M.uniform_field(pts, 9, seed=5)
+    n = int(np.prod(pts))
+    K = np.random.default_rng(2).uniform(-1, 1, 81 * n)
+    with abi.Context(pts, 3) as ctx:
+        fa, fk = ctx.field(9, A), ctx.field(81, K)
+        g1 = ctx.projection(fa).download()
+        m1 = ctx.projected_tangent(fk, fa).download()
+        ctx.set_transpose(1)
+        ctx.set_virtual_ranks(P)
+        gs = ctx.projection(fa).download()
+        ms = ctx.projected_tangent(fk, fa).download()
+        ctx.set_transpose(0)  # back to the fused form on the same context
+        gf = ctx.projection(fa).download()
+    assert np.array_equal(g1, gs)
+    assert np.array_equal(m1, ms)
+    assert np.array_equal(g1, gf)
+
+
 def test_virtual_ranks_solve_matches_single_rank():
     pts = (32, 32, 32)
     pg = M.bernoulli(pts, 0.3, seed=2)
