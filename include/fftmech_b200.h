@@ -59,7 +59,7 @@ typedef struct fm_error_info {
 typedef struct fm_solver_params {
   double eta_newton;  /* default 1e-5 */
   double eta_cg;      /* default 1e-8 */
-  int32_t max_newton; /* default 30, <= FM_MAX_PASSES */
+  int32_t max_newton; /* default 30; any value >= 1 */
   int32_t max_cg;     /* 0 = n * tdim^2 */
 } fm_solver_params;
 
@@ -67,7 +67,7 @@ typedef struct fm_solver_params {
 
 /* SolveReport + NewtonPass, solver.hpp:34-58 */
 typedef struct fm_report {
-  int32_t n_passes;
+  int32_t n_passes; /* true pass count; the arrays record the first FM_MAX_PASSES passes */
   int32_t converged;
   int32_t cg_iterations[FM_MAX_PASSES];
   double cg_rel_residual[FM_MAX_PASSES];
@@ -125,6 +125,13 @@ int fm_nccl_unique_id(void* out, int bytes);
 /* Virtual ranks: run all P slab ranks on this one device (their buffers side
  * by side, the same transpose-fused kernels storing across them) -- validates
  * the decomposition against P = 1 bit for bit. */
+/* Debug mode (also FM_DEBUG_RESIDUE=1 at creation): every projection checks
+ * the imaginary residue that apply_projection checks after its c2c inverse
+ * transform (projection.cpp:157-169) and fails with FM_E_COMPLEX_RESIDUE above
+ * 1e-10 ||A||.  With the half spectrum kept here the residue can only come from
+ * the self-conjugate kz planes, whose lines must be real before the c2r pass;
+ * fm_last_error_info().value then holds the residue of the last projection. */
+int fm_ctx_set_debug(fm_ctx* ctx, int residue_check);
 int fm_ctx_set_virtual_ranks(fm_ctx* ctx, int P);
 /* How the two slab transposes of a P > 1 projection are done (replaces the
  * single-process FFTW plans of projection.cpp:106-119 across ranks):

@@ -54,8 +54,8 @@ class Report(C.Structure):
                 ("wall_seconds", C.c_double), ("matvecs", C.c_int64)]
 
     def as_dict(self):
-        n = self.n_passes
-        return {"passes": n, "converged": bool(self.converged),
+        n = min(self.n_passes, MAX_PASSES)  # per-pass records exist for the first MAX_PASSES passes
+        return {"passes": self.n_passes, "converged": bool(self.converged),
                 "cg_it": list(self.cg_iterations[:n]), "cg_rel": list(self.cg_rel_residual[:n]),
                 "rel_update": list(self.rel_update[:n]),
                 "eq_rel": self.equilibrium_rel_residual, "drift": self.max_mean_drift,
@@ -117,6 +117,7 @@ _SIGS = {
     "fm_model_set_tangent_form": (C.c_int, [_P, _P, C.c_int]),
     "fm_ctx_set_virtual_ranks": (C.c_int, [_P, C.c_int]),
     "fm_ctx_set_transpose": (C.c_int, [_P, C.c_int]),
+    "fm_ctx_set_debug": (C.c_int, [_P, C.c_int]),
     "fm_ctx_ranks": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fm_dist_route": (C.c_int, [C.c_int] * 11 + [C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
 }
@@ -198,6 +199,15 @@ class Context:
     def set_virtual_ranks(self, P):
         """Run the slab-decomposed projection with P ranks emulated on this device."""
         self.check(lib().fm_ctx_set_virtual_ranks(self.h, P))
+
+    def set_debug(self, residue_check=True):
+        """Imaginary-residue check of every projection (projection.cpp:157-169)."""
+        self.check(lib().fm_ctx_set_debug(self.h, 1 if residue_check else 0))
+
+    def last_info(self):
+        info = ErrorInfo()
+        lib().fm_last_error_info(self.h, C.byref(info))
+        return {"status": info.status, "cg_iterations": info.cg_iterations, "node": info.node, "value": info.value}
 
     def set_transpose(self, mode):
         """0: slab transposes fused into passes 2 and 3 as peer stores; 1: staged all-to-all."""

@@ -198,7 +198,8 @@ int fm_ctx_create(int dim, const int32_t* points, const double* lengths, int tdi
   if (cudaMemset(ctx->d_scal, 0, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_CUDA);
   if (cudaMallocHost(&ctx->h_scal, sizeof(double) * 64) != cudaSuccess) return fail(FM_E_OOM);
   if (cudaMalloc(&ctx->d_bad, sizeof(unsigned long long)) != cudaSuccess) return fail(FM_E_OOM);
-  if (cudaMalloc(&ctx->d_badval, sizeof(double)) != cudaSuccess) return fail(FM_E_OOM);
+  if (cudaMalloc(&ctx->d_badval, 2 * sizeof(double)) != cudaSuccess) return fail(FM_E_OOM);  // value + its key
+  if (const char* dbg = getenv("FM_DEBUG_RESIDUE")) fm_ctx_set_debug(ctx, atoi(dbg));
   *out = ctx;
   return FM_OK;
 }
@@ -260,6 +261,14 @@ static int setup_slabs(fm_ctx* ctx, int P) {
 static int transpose_from_env() {
   const char* e = getenv("FM_TRANSPOSE");
   return e && (!strcmp(e, "nccl") || !strcmp(e, "staged") || !strcmp(e, "1")) ? 1 : 0;
+}
+
+int fm_ctx_set_debug(fm_ctx* ctx, int residue_check) {
+  if (!ctx) return FM_E_INVALID;
+  ctx->debug_residue = residue_check != 0;
+  const char* inj = getenv("FM_DEBUG_RESIDUE_INJECT");
+  ctx->debug_inject = inj ? atof(inj) : 0.0;
+  return FM_OK;
 }
 
 int fm_ctx_set_transpose(fm_ctx* ctx, int mode) {

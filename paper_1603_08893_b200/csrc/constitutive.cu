@@ -9,11 +9,28 @@
 
 namespace fm {
 
+// badval: two words, [0] the value reported with the error (the offending
+// eigenvalue of NotPositiveDefinite) and [1] the key it belongs to.  The pair
+// is updated under a one-word lock (key word = 0 while held) and only towards
+// smaller keys, so after the launch it holds the value of the LOWEST node even
+// when several nodes fail at once (a plain store after the atomicMin could be
+// overtaken by a loser's).
 __device__ __forceinline__ void report_bad(unsigned long long* bad, double* badval, int64_t node,
                                            int status, double value) {
   const unsigned long long key = (static_cast<unsigned long long>(node) << 4) | unsigned(status);
   const unsigned long long old = atomicMin(bad, key);
-  if (key < old && badval) *badval = value;
+  if (!badval || key >= old) return;
+  unsigned long long* vkey = reinterpret_cast<unsigned long long*>(badval + 1);
+  unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(vkey);
+  while (cur == 0ull || key < cur) {
+    if (cur != 0ull && atomicCAS(vkey, cur, 0ull) == cur) {
+      badval[0] = value;
+      __threadfence();
+      atomicExch(vkey, key);
+      return;
+    }
+    cur = *reinterpret_cast<volatile unsigned long long*>(vkey);
+  }
 }
 
 template <int TD>
@@ -548,20 +565,32 @@ __global__ void __launch_bounds__(256) k_eq_stress(int64_t n, const double* __re
 // -------------------------------------------------------------------- host
 int reset_bad(fm_ctx* ctx) {
   FM_CUDA(ctx, cudaMemsetAsync(ctx->d_bad, 0xFF, sizeof(unsigned long long), ctx->stream));
+  FM_CUDA(ctx, cudaMemsetAsync(ctx->d_badval + 1, 0xFF, sizeof(unsigned long long), ctx->stream));  // no value yet
   return FM_OK;
 }
 
 int check_bad(fm_ctx* ctx) {
   if (int st = combine_min_u64(ctx, ctx->d_bad)) return st;  // lowest offending node over all ranks
   unsigned long long key = 0;
-  double val = 0.0;
+  struct {
+    double val;
+    unsigned long long key;
+  } rec{0.0, ~0ull};
   FM_CUDA(ctx, cudaMemcpyAsync(&key, ctx->d_bad, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream));
-  FM_CUDA(ctx, cudaMemcpyAsync(&val, ctx->d_badval, sizeof(val), cudaMemcpyDeviceToHost, ctx->stream));
+  FM_CUDA(ctx, cudaMemcpyAsync(&rec, ctx->d_badval, sizeof(rec), cudaMemcpyDeviceToHost, ctx->stream));
   FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   if (key == ~0ull) return FM_OK;
   const int status = int(key & 15ull);
   const int64_t node = int64_t(key >> 4);
-  ctx->last_info = fm_error_info{status, 0, node, val};
+  // the value travels with its key: only the rank that owns the lowest node holds it
+  double val = rec.key == key ? rec.val : 0.0;
+  if (distributed(ctx)) {
+    double* slot = ctx->d_scal + 62;
+    FM_CUDA(ctx, cudaMemcpyAsync(slot, &val, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (int st = combine_ranks(ctx, slot, 1)) return st;  // ordered sum: one rank contributes, the others 0
+    FM_CUDA(ctx, cudaMemcpyAsync(&val, slot, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
   const char* what = status == FM_E_INVERTED   ? "non-positive det(F) at node "
                      : status == FM_E_NOT_SPD ? "tensor log requires a positive-definite argument (node "
                                               : "singular tensor at node ";

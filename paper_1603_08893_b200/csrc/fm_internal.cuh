@@ -99,6 +99,10 @@ struct fm_ctx {
   double2* spec2 = nullptr;       // x-pass input B (y-slab), only when P > 1
   double2* spec3 = nullptr;       // pack / unpack staging of the staged all-to-all transposes (transpose == 1)
   int transpose = 0;              // P > 1: 0 = transposes fused into passes 2, 3 as peer stores, 1 = staged all-to-all
+  // debug mode (FM_DEBUG_RESIDUE=1 / fm_ctx_set_debug): every projection checks the imaginary residue the
+  // reference checks after its c2c inverse transform (projection.cpp:157-169); inject: test hook
+  bool debug_residue = false;
+  double debug_inject = 0.0;
   // slab decomposition over P ranks; P = 1: single device
   int P = 1, rank = 0;
   bool virt = false;              // all P ranks emulated on this one device
@@ -162,6 +166,7 @@ int check_cuda(fm_ctx* ctx, cudaError_t e, const char* what);
   } while (0)
 
 int ensure_field(fm_ctx* ctx, fm_field& f, int ncomp);
+int norm_sync(fm_ctx* ctx, const double* a, int64_t count, double* out);  // solver.cu
 
 // Function attributes are per device: raise a kernel's dynamic shared-memory
 // limit on the CURRENT device once (memoised per (device, kernel)).

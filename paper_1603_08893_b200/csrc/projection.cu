@@ -577,6 +577,61 @@ int pass_zi(fm_ctx* ctx, const Geo& g, const double2* A, double* out, double sca
   return FM_OK;
 }
 
+// Debug mode: the imaginary residue of the reference's c2c inverse transform
+// (projection.cpp:157-169).  With a half spectrum the other half is DEFINED by
+// Hermitian symmetry, so the only imaginary output a c2c transform of the same
+// data could produce comes from the self-conjugate kz planes (kz = 0, and
+// kz = Nz/2 when stored): after the inverse x and y transforms their lines must
+// be real, and what pass 5 discards there is Im b(x, y), the same at every z.
+// residue^2 = Nz * sum_{c,x,y} Im b^2 / n^2.
+__global__ void k_im_residue(const double2* __restrict__ spec, int64_t lines, int nzh, int nyq, double inject,
+                             double* __restrict__ sum) {
+  double s = 0.0;
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < lines; l += int64_t(gridDim.x) * blockDim.x) {
+    double im = spec[l * nzh].y;
+    if (l == 0) im += inject;  // test hook (FM_DEBUG_RESIDUE_INJECT): a Hermitian violation on purpose
+    s += im * im;
+    if (nyq > 0) {
+      const double in = spec[l * nzh + nyq].y;
+      s += in * in;
+    }
+  }
+  s = block_sum_any(s);
+  if (threadIdx.x == 0 && s != 0.0) atomicAdd(sum, s);
+}
+
+int residue_accumulate(fm_ctx* ctx, int r0, int r1) {
+  double* slot = ctx->d_scal + 61;
+  FM_CUDA(ctx, cudaMemsetAsync(slot, 0, sizeof(double), ctx->stream));
+  const int nyq = (ctx->Nz % 2 == 0 && ctx->nzh == ctx->Nz / 2 + 1) ? ctx->Nz / 2 : 0;
+  for (int r = r0; r < r1; ++r) {
+    const int64_t lines = int64_t(ctx->ncomp) * (ctx->Nx / ctx->P) * ctx->Ny;
+    k_im_residue<<<int(std::min<int64_t>((lines + 255) / 256, 148 * 8)), 256, 0, ctx->stream>>>(
+        spec_a(ctx, r), lines, ctx->nzh, nyq, (r == 0 && ctx->rank == 0) ? ctx->debug_inject : 0.0, slot);
+    FM_LAUNCHED_K(ctx, "k_im_residue");
+  }
+  return combine_ranks(ctx, slot, 1);
+}
+
+// tolerance 1e-10 ||A|| as the reference for apply_projection; the fused
+// operator forms never materialise their A = K : dF, so they use ||G(A)|| <= ||A||.
+int residue_check(fm_ctx* ctx, const ProArgs& pa, const double* out, double scale) {
+  double s = 0.0, ref = 0.0;
+  FM_CUDA(ctx, cudaMemcpyAsync(&s, ctx->d_scal + 61, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  const int64_t count = int64_t(ctx->ncomp) * ctx->n;
+  if (int st = norm_sync(ctx, pa.kind == PRO_COPY && pa.A ? pa.A : out, count, &ref)) return st;
+  const double residue = std::sqrt(double(ctx->Nz) * s) * std::abs(scale) / double(ctx->n_global);
+  const double tol = 1e-10 * std::max(ref, 1e-300);
+  if (residue > tol) {
+    const int st = set_error(ctx, FM_E_COMPLEX_RESIDUE, "complex residue " + std::to_string(residue) +
+                                                            " exceeds tolerance " + std::to_string(tol));
+    ctx->last_info = fm_error_info{FM_E_COMPLEX_RESIDUE, 0, -1, residue};
+    return st;
+  }
+  ctx->last_info = fm_error_info{FM_OK, 0, -1, residue};  // the residue of the last checked projection
+  return FM_OK;
+}
+
 template <int TD>
 int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiArgs& epi, int* nparts) {
   init_generic<TD>();
@@ -619,6 +674,9 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   for (int r = r0; r < r1; ++r)
     if (int st = pass_y<TD>(ctx, geo_zy(ctx, r), +1, spec_a(ctx, r), spec_a(ctx, r))) return st;
   prof_mark(ctx);
+  const bool residue = ctx->debug_residue && !ctx->capturing;
+  if (residue)
+    if (int st = residue_accumulate(ctx, r0, r1)) return st;
   int total = 0;
   for (int r = r0; r < r1; ++r) {
     EpiArgs e = epi;
@@ -630,6 +688,7 @@ int run_td(fm_ctx* ctx, const ProArgs& pa, double* out, double scale, const EpiA
   if (nparts) *nparts = total;
   prof_mark(ctx);
   if (ctx->prof.on) ctx->prof.calls++;
+  if (residue) return residue_check(ctx, pa, out, scale);
   return FM_OK;
 }
 }  // namespace

@@ -63,20 +63,22 @@ constexpr size_t XSMEM = 1024 + 3 * size_t(XTILE) + XTW * size_t(XSCR) + 64;
 // half-line h sits at double index 2 (p ^ ((p >> 4) & 7)) + h, which makes both
 // the strided writes (p = 16 t + k) and the unit-stride reads (p = t + 16 m)
 // conflict-free for the 16 lanes a 64-bit access serves per wavefront.
-__device__ __forceinline__ void exchange(double2 (&v)[XE], char* wr0, const char* rd0) {
+// (32-bit shared-space addresses and explicit ld/st.shared: with generic pointers the
+// XOR hides the address space and the accesses compile to generic LD / ST.)
+__device__ __forceinline__ void exchange(double2 (&v)[XE], unsigned wr0, unsigned rd0) {
 #pragma unroll
   for (int part = 0; part < 2; ++part) {
 #pragma unroll
     for (int k = 0; k < XE; ++k) {
-      char* a = reinterpret_cast<char*>(reinterpret_cast<uintptr_t>(wr0) ^ uintptr_t((k & 7) << 4)) + ((k >> 3) << 7);
-      *reinterpret_cast<double*>(a) = part == 0 ? v[k].x : v[k].y;
+      const unsigned a = (wr0 ^ unsigned((k & 7) << 4)) + unsigned((k >> 3) << 7);
+      asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(part == 0 ? v[k].x : v[k].y) : "memory");
     }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < XE; ++m) {
-      const char* a =
-          reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(rd0) ^ uintptr_t((m & 7) << 4)) + (m << 8);
-      const double x = *reinterpret_cast<const double*>(a);
+      const unsigned a = (rd0 ^ unsigned((m & 7) << 4)) + unsigned(m << 8);
+      double x;
+      asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(x) : "r"(a) : "memory");
       if (part == 0) v[m].x = x; else v[m].y = x;
     }
     __syncwarp();
@@ -87,7 +89,7 @@ __device__ __forceinline__ void exchange(double2 (&v)[XE], char* wr0, const char
 // lanes: the two Stockham radix-16 stages of reg::fft<256, 16, SIGN, 2> (same
 // butterflies, same twiddles W_512^(2 t r)), exchanged as above.
 template <int SIGN>
-__device__ __forceinline__ void fft256(double2 (&v)[XE], int t, char* wr0, const char* rd0,
+__device__ __forceinline__ void fft256(double2 (&v)[XE], int t, unsigned wr0, unsigned rd0,
                                        const double2* __restrict__ tw) {
   reg::Dft<16, SIGN>::run(v);
   exchange(v, wr0, rd0);
@@ -183,7 +185,10 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     const int phases = late ? K + 1 : K;
     for (int k = 0; k < phases; ++k) {
       const long long c0 = prof ? clock64() : 0;
-      bulk::mbar_wait(staged, k & 1);
+      // (the copy warps idle most of a tile: sleep between polls so that their
+      // spinning does not take issue slots from the transform warps they share
+      // schedulers with)
+      while (!bulk::mbar_test(staged, k & 1)) __nanosleep(256);
       const long long c1 = prof ? clock64() : 0;
       const int out = late ? k - 1 : k;  // the tile whose output sits in the buffer
       if (out >= 0) {
@@ -213,9 +218,9 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
   unsigned char* const R = sm0 + 2 * XTILE + col;
   auto at = [](unsigned char* b, int m) { return reinterpret_cast<double2*>(b + (m << 12)); };
   // exchange addresses of slot 0 (see exchange())
-  char* const scr = reinterpret_cast<char*>(scr0) + w * XSCR;
-  char* const wr0 = scr + (t << 8) + (h << 3) + ((t & 7) << 4);
-  const char* const rd0 = scr + (t << 4) + (h << 3);
+  const unsigned scr = bulk::smem_addr(scr0) + w * XSCR;
+  const unsigned wr0 = scr + (t << 8) + (h << 3) + ((t & 7) << 4);
+  const unsigned rd0 = scr + (t << 4) + (h << 3);
   // The twiddles only depend on the lane: through an opaque copy of the table
   // pointer each transform reloads them instead of keeping ~90 registers live
   // across the tile loop.

@@ -391,8 +391,10 @@ int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
   if (!(prm.eta_newton > 0.0 && prm.eta_newton < 1.0))
     return set_error(ctx, FM_E_INVALID, "eta_newton must be in (0,1)");
   if (!(prm.eta_cg > 0.0 && prm.eta_cg < 1.0)) return set_error(ctx, FM_E_INVALID, "eta_cg must be in (0,1)");
-  if (prm.max_newton < 1 || prm.max_newton > FM_MAX_PASSES)
-    return set_error(ctx, FM_E_INVALID, "max_newton must be in [1, 64]");
+  // (any max_newton >= 1, as SolverParams::validate, solver.hpp: the report
+  // keeps the per-pass record of the first FM_MAX_PASSES passes and the true
+  // pass count)
+  if (prm.max_newton < 1) return set_error(ctx, FM_E_INVALID, "max_newton must be >= 1");
   if (prm.max_cg < 0) return set_error(ctx, FM_E_INVALID, "max_cg must be >= 0");
   const int d = ctx->tdim, nc = ctx->ncomp;
   if (Ff->ncomp != nc) return set_error(ctx, FM_E_INVALID, "increment dimension does not match the state field");
@@ -474,9 +476,11 @@ int solve_increment(fm_ctx* ctx, fm_model* m, fm_field* Ff, const double* fbar,
     if (int st = norm_sync(ctx, ctx->dF.d, count, &ndf)) return st;
     const double ru = ndf / norm_ref;
     const int k = rep->n_passes++;
-    rep->cg_iterations[k] = it;
-    rep->cg_rel_residual[k] = rel;
-    rep->rel_update[k] = ru;
+    if (k < FM_MAX_PASSES) {
+      rep->cg_iterations[k] = it;
+      rep->cg_rel_residual[k] = rel;
+      rep->rel_update[k] = ru;
+    }
     double dr;
     if (int st = drift(&dr)) return st;
     rep->max_mean_drift = std::max(rep->max_mean_drift, dr);

@@ -29,7 +29,10 @@ SolveReport to_report(const fm_report& r, const Increment& inc) {
   SolveReport out;
   out.label = inc.label;
   out.fbar = inc.fbar;
-  for (int k = 0; k < r.n_passes; ++k) out.passes.push_back({r.cg_iterations[k], r.cg_rel_residual[k], r.rel_update[k]});
+  // the ABI records the first FM_MAX_PASSES passes in detail; later ones count as passes without a record
+  for (int k = 0; k < r.n_passes; ++k)
+    out.passes.push_back(k < FM_MAX_PASSES ? NewtonPass{r.cg_iterations[k], r.cg_rel_residual[k], r.rel_update[k]}
+                                           : NewtonPass{0, 0.0, 0.0});
   out.equilibrium_rel_residual = r.equilibrium_rel_residual;
   out.max_mean_drift = r.max_mean_drift;
   out.wall_seconds = r.wall_seconds;

@@ -37,6 +37,19 @@ def test_set_overrides_take_precedence():
     assert cli("validate", good, "--set", "bogus").returncode == 2
 
 
+def test_run_section_places_the_gpu_run():
+    """device selection and the slab-rank count are config keys
+    (`run` section) with command-line shorthands."""
+    good = os.path.join(DATA, "hyperelastic_cube_small.json")
+    assert cli("validate", good, "--set", "run.device=0", "--set", "run.ranks=2",
+               "--set", "run.transpose=nccl").returncode == 0
+    assert cli("validate", good, "--device", "1", "--ranks", "4", "--transpose", "peer").returncode == 0
+    r = cli("validate", good, "--device", "-1", "--ranks", "0", "--transpose", "mpi")
+    assert r.returncode == 2
+    for key in ("run.device", "run.ranks", "run.transpose"):
+        assert f"config error: {key}" in r.stderr, r.stderr
+
+
 def test_usage_and_missing_file():
     assert cli("frobnicate", "x").returncode == 1
     r = cli("validate", "/nonexistent/config.json")
@@ -51,6 +64,32 @@ def test_run_then_info(tmp_path):
     assert (out / "report.csv").exists() and (out / "meta_1.json").exists()
     i = cli("info", str(out))
     assert i.returncode == 0 and "1 snapshot(s)" in i.stdout and "fields F P eq" in i.stdout, i.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transpose", ["peer", "nccl"])
+def test_slab_run_from_the_cli_matches_single_rank(tmp_path, transpose):
+    """`fftmech run --ranks 2`: the slab-decomposed kernels (two ranks emulated
+    on the device, either transpose arm) write the same converged field and
+    the same Newton / CG record as the plain run."""
+    import numpy as np
+    cfg = {"grid": {"points": [8, 8, 8]}, "microstructure": {"kind": "cube", "volume_fraction": 0.125},
+           "model": {"kind": "hyperelastic", "phases": [{"youngs": 1.0, "poisson": 0.3},
+                                                       {"youngs": 10.0, "poisson": 0.3}]},
+           "loading": {"mode": "simple_shear", "gamma": 0.1, "increments": 1}}
+    p = tmp_path / "cfg.json"
+    p.write_text(json.dumps(cfg))
+    outs = []
+    for name, extra in (("plain", []), ("slab", ["--device", "0", "--ranks", "2", "--transpose", transpose])):
+        out = tmp_path / name
+        r = cli("run", str(p), "--set", f"output.directory={out}", *extra)
+        assert r.returncode == 0, r.stdout + r.stderr
+        outs.append((np.fromfile(out / "F_1.bin", dtype="<f8"), (out / "report.csv").read_text().splitlines()))
+    (F1, rep1), (F2, rep2) = outs
+    assert np.max(np.abs(F1 - F2)) < 1e-12
+    # same Newton and CG counts; the residual is a reduction in another order
+    assert [l.split(",")[:3] for l in rep1] == [l.split(",")[:3] for l in rep2]
+    assert abs(float(rep1[1].split(",")[3]) - float(rep2[1].split(",")[3])) < 1e-6 * float(rep1[1].split(",")[3])
 
 
 @pytest.mark.gpu
