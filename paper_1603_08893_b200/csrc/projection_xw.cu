@@ -104,7 +104,11 @@ __device__ __forceinline__ void fft256(double2 (&v)[XE], int t, unsigned wr0, un
 // [6] loop cycles of warp 0; [7] tiles.
 __device__ unsigned long long xw_prof[8];
 
-template <bool LSU>
+// PARK: while A_0 is transformed and during the first inverse transform the
+// other register array (FFT(B), then s) waits in the warp's column of R, which
+// is free from the moment A_0 has been read until output 0 is written: one
+// 16-element array live per transform instead of two.
+template <bool LSU, bool PARK>
 __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, double2* spec, int tiles,
                                                         const __grid_constant__ CUtensorMap tmap, int dbg) {
   extern __shared__ unsigned char smraw[];
@@ -284,7 +288,15 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     }
 #pragma unroll
     for (int m = 0; m < XE; ++m) v[m] = *at(R, m);
+    if constexpr (PARK) {
+#pragma unroll
+      for (int m = 0; m < XE; ++m) *at(R, m) = X[m];
+    }
     fwd(v);
+    if constexpr (PARK) {
+#pragma unroll
+      for (int m = 0; m < XE; ++m) X[m] = *at(R, m);
+    }
     // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
 #pragma unroll
     for (int m = 0; m < XE; ++m) {
@@ -301,7 +313,15 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
       const double f = freq_of(kslot<XTH, XH>(t, h, m), XN) * g.invL[0];
       v[m] = make_double2(X[m].x * f, X[m].y * f);
     }
+    if constexpr (PARK) {
+#pragma unroll
+      for (int m = 0; m < XE; ++m) *at(R, m) = X[m];
+    }
     inv(v);
+    if constexpr (PARK) {
+#pragma unroll
+      for (int m = 0; m < XE; ++m) X[m] = *at(R, m);
+    }
 #pragma unroll
     for (int m = 0; m < XE; ++m) *at(R, m) = v[m];
     bulk::fence_async_smem();
@@ -349,15 +369,20 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
     const char* e = getenv("FM_XW_TMA_STORE");
     return !e || atoi(e) != 0;
   }();
-  const void* kern = tma_store ? reinterpret_cast<const void*>(k_x_warp<false>) : reinterpret_cast<const void*>(k_x_warp<true>);
-  set_smem_limit(kern, int(XSMEM));
+  static const bool park = [] {
+    const char* e = getenv("FM_XW_PARK");
+    return e && atoi(e) != 0;
+  }();
+  using Kern = void (*)(Geo, const double2*, double2*, int, const CUtensorMap, int);
+  const Kern kern = tma_store ? (park ? k_x_warp<false, true> : k_x_warp<false, false>)
+                              : (park ? k_x_warp<true, true> : k_x_warp<true, false>);
+  set_smem_limit(reinterpret_cast<const void*>(kern), int(XSMEM));
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = (g.nzh / XTW) * g.Ny * 3;
   const int grid = std::min(tiles, std::max(sms, 1));
-  if (tma_store) k_x_warp<false><<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map, dbg);
-  else k_x_warp<true><<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map, dbg);
+  kern<<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map, dbg);
   if (dbg & 16) {  // timing experiments only: per-tile averages to stderr
     unsigned long long h[8] = {}, z[8] = {};
     cudaStreamSynchronize(ctx->stream);
