@@ -200,6 +200,7 @@ int dist_setup_routes(fm_ctx* ctx) {
       b[r] = static_cast<double2*>(pb);
     }
   }
+  ctx->h_dst_a = a;
   FM_CUDA(ctx, cudaMemcpy(ctx->d_dst_a, a.data(), sizeof(double2*) * kMaxRanks, cudaMemcpyHostToDevice));
   FM_CUDA(ctx, cudaMemcpy(ctx->d_dst_b, b.data(), sizeof(double2*) * kMaxRanks, cudaMemcpyHostToDevice));
   return FM_OK;

@@ -114,6 +114,7 @@ struct fm_ctx {
   // memory mapped through CUDA IPC when the ranks are devices
   double2** d_dst_a = nullptr;
   double2** d_dst_b = nullptr;
+  std::vector<double2*> h_dst_a;  // host copy of d_dst_a (tensor maps of the routed TMA stores)
   std::vector<void*> ipc_open;    // peer buffers opened with cudaIpcOpenMemHandle
   double* d_gather = nullptr;     // all-gather staging of per-rank scalars
   // CG loop as one CUDA graph (a while-conditional node around the fused

@@ -71,6 +71,17 @@ __device__ __forceinline__ void store_xb(const Geo& g, double2* local, int c, in
   }
 }
 
+// The same store for the register-resident passes, whose extents are powers of
+// two (Xl = 2^sh): the owner and the local x are a shift and a mask, and the
+// per-line part of route_xb, base = ((c Xl) Nyg + rank Yl + yl) nzh + kz, is
+// computed once per line instead of per element.
+__device__ __forceinline__ int64_t xb_base(const Geo& g, int c, int yl, int kz) {
+  return ((int64_t(c) * g.Xl) * g.Nyg + int64_t(g.rank) * g.Ny + yl) * g.nzh + kz;
+}
+__device__ __forceinline__ void store_xb_pow2(const Geo& g, int sh, int64_t base, int x, double2 v) {
+  g.dst[x >> sh][base + int64_t(x & (g.Xl - 1)) * g.Nyg * g.nzh] = v;
+}
+
 __device__ __forceinline__ int freq_of(int i, int n) { return (i < (n + 1) / 2) ? i : i - n; }
 
 // ------------------------------------------------------------------ pass 1
@@ -319,8 +330,8 @@ bool x_fast(fm_ctx* ctx, const Geo& g, double2* spec, int* st);
 bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double scale, const EpiArgs& epi,
              int* st);
 // Cached CUtensorMap (written to out_map) of a spectral buffer viewed as
-// [rows][Ny][2 nzh] doubles with a (2 TW, 1, 256) box (projection_fast.cu).
-bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, void* out_map);
+// [rows][Ny][2 nzh] doubles with a (2 TW, 1, box_rows) box (projection_fast.cu).
+bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, int box_rows, void* out_map);
 // 512-point x pass, one warp per line, TMA in and out (projection_xw.cu).
 bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg);
 

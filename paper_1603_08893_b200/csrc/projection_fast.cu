@@ -34,8 +34,15 @@ using reg::e_x;
 // In place on one device.  P > 1: SIGN -1 stores each element into the x-pass
 // input of the rank that owns its y (the fused forward slab transpose,
 // store_yf); SIGN +1 runs in place on the spectrum of the x-slab.
+// (Register budget of 128 for every instantiation: the routed forward pass
+// otherwise takes 146 registers at 512 points and loses its second CTA per SM
+// -- 6.5 instead of 3.2 ms at 512^3 with 8 ranks.)
+template <int N, int TW>
+constexpr int y_minb() {
+  return std::max(1, 512 / (TW * (N / e_line(N))));
+}
 template <int N, int TW, int SIGN, bool RT = false>
-__global__ void __launch_bounds__(TW*(N / e_line(N))) k_y_fast(Geo g, const double2* __restrict__ tw,
+__global__ void __launch_bounds__(TW*(N / e_line(N)), y_minb<N, TW>()) k_y_fast(Geo g, const double2* __restrict__ tw,
                                                                const double2* in, double2* out) {
   constexpr int E = e_line(N), T = N / E;
   extern __shared__ double2 sm[];
@@ -50,8 +57,17 @@ __global__ void __launch_bounds__(TW*(N / e_line(N))) k_y_fast(Geo g, const doub
 #pragma unroll
     for (int m = 0; m < E; ++m) out[spec_std(g, c, x, t + T * m, kz)] = v[m];
   } else {
+    // route_yf (proj_common.cuh) with the per-line part hoisted: element y goes
+    // to rank d = y / Yl at base + yl nzh, base = ((c Nxg + rank Xl + x) Yl) nzh + kz.
+    // Yl is a power of two here (N is, and P divides it), so d and yl are a
+    // shift and a mask instead of a division per element.
+    const int64_t base = ((int64_t(c) * g.Nxg + int64_t(g.rank) * g.Nx + x) * g.Yl) * g.nzh + kz;
+    const int sh = 31 - __clz(g.Yl);
 #pragma unroll
-    for (int m = 0; m < E; ++m) store_yf(g, out, c, x, t + T * m, kz, v[m]);
+    for (int m = 0; m < E; ++m) {
+      const int y = t + T * m;
+      g.dst[y >> sh][base + int64_t(y & (g.Yl - 1)) * g.nzh] = v[m];
+    }
   }
 }
 
@@ -314,9 +330,11 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
         for (int m = 0; m < E; ++m)
           base[(int64_t(j) * N + t + T * m) * xstride] = make_double2(v[m].x * f, v[m].y * f);
       } else {
+        const int sh = 31 - __clz(g.Xl);
+        const int64_t rb = xb_base(g, i * 3 + j, y, kz);
 #pragma unroll
         for (int m = 0; m < E; ++m)
-          store_xb(g, nullptr, i * 3 + j, t + T * m, y, kz, make_double2(v[m].x * f, v[m].y * f));
+          store_xb_pow2(g, sh, rb, t + T * m, make_double2(v[m].x * f, v[m].y * f));
       }
     }
   }
@@ -1280,12 +1298,13 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 }  // namespace
-bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, void* out_map) {
+bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, int box_rows, void* out_map) {
   CUtensorMap* out = static_cast<CUtensorMap*>(out_map);
   struct Entry {
     const void* base;
     int rows, Ny, nzh, TW;
     bool swz;
+    int box_rows;
     CUtensorMap map;
   };
   static std::mutex mx;
@@ -1302,14 +1321,14 @@ bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz1
   if (!enc) return false;
   std::lock_guard<std::mutex> lk(mx);
   for (const Entry& e : cache)
-    if (e.base == base && e.rows == rows && e.Ny == Ny && e.nzh == nzh && e.TW == TW && e.swz == swz128) {
+    if (e.base == base && e.rows == rows && e.Ny == Ny && e.nzh == nzh && e.TW == TW && e.swz == swz128 && e.box_rows == box_rows) {
       *out = e.map;
       return true;
     }
-  Entry e{base, rows, Ny, nzh, TW, swz128, {}};
+  Entry e{base, rows, Ny, nzh, TW, swz128, box_rows, {}};
   const cuuint64_t dims[3] = {cuuint64_t(2 * nzh), cuuint64_t(Ny), cuuint64_t(rows)};
   const cuuint64_t strides[2] = {cuuint64_t(nzh) * 16, cuuint64_t(Ny) * nzh * 16};
-  const cuuint32_t box[3] = {cuuint32_t(2 * TW), 1, 256};
+  const cuuint32_t box[3] = {cuuint32_t(2 * TW), 1, cuuint32_t(box_rows)};
   const cuuint32_t estr[3] = {1, 1, 1};
   // L2 promotion (A/B: FM_TMA_PROMO 0 none, 1 64 B, 2 128 B, 3 256 B); a
   // promotion wider than the 16 TW-byte row segment would fetch neighbours
@@ -1326,7 +1345,7 @@ bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz1
           CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, pr,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
-  if (cache.size() > 64) cache.clear();
+  if (cache.size() > 256) cache.clear();
   cache.push_back(e);
   *out = e.map;
   return true;
@@ -1336,7 +1355,7 @@ namespace {
 template <int N, int TW, int E, bool PAIR, bool RT>
 bool xs_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   CUtensorMap map;
-  if (!x_tensor_map(spec, 9 * N, g.Ny, g.nzh, TW, false, &map)) return false;
+  if (!x_tensor_map(spec, 9 * N, g.Ny, g.nzh, TW, false, 256, &map)) return false;
   const size_t smem = size_t(3) * N * TW * 16;
   constexpr int THREADS = TW * (N / E);
   allow(k_x_stream<N, TW, E, PAIR, RT>, smem);
@@ -1400,7 +1419,7 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
       const char* e = getenv("FM_X_DBG");
       return e ? atoi(e) : 0;
     }();
-    if (zc && xm == 7 && g.P == 1 && xw_launch(ctx, g, spec, xdbg)) {
+    if (zc && xm == 7 && xw_launch(ctx, g, spec, xdbg)) {
       done = true;
       name = "k_x_warp";
     } else if (zc && ctx->nzh % 8 == 0 && xm >= 2 &&

@@ -21,10 +21,11 @@
 //    rows from 8 different bank groups) and results go back IN PLACE into the
 //    warp's own column of a buffer it has already consumed -- no cross-warp
 //    dependency -- from where a TMA store writes the tile back;
-//  * a ninth warp (its warp group gives its registers to the transform warps,
-//    setmaxnreg) issues every load and store: it waits for "all 8 warps have
-//    staged this buffer" (mbarrier), stores it, waits until the store has read
-//    shared memory and refills the buffer with the next tile's component.
+//  * one copy warp per buffer (their warp group gives its registers to the
+//    transform warps, setmaxnreg) issues the buffer's loads and stores: it waits
+//    for "all 8 warps have staged this buffer" (mbarrier), stores it, waits until
+//    the store has read shared memory and refills the buffer with the next
+//    tile's component.
 //
 // Buffer schedule per tile k (P, Q, R the three buffers):
 //   P, Q: A_1(k), A_2(k) arrive -> every warp forms B = xi_y A_1 + xi_z A_2 from
@@ -35,7 +36,7 @@
 //         goes back into R after the first inverse transform -> staged -> store
 //         -> load A_0(k+1), two transforms ahead of its use.
 // Same arithmetic, in the same order, as the lane-pair k_x_stream: results are
-// bit-identical (tests/test_gpu_projection.py compares the digests).
+// bit-identical (tests/test_gpu_projection.py compares the two kernels' outputs).
 #include <cuda.h>
 
 #include <algorithm>
@@ -104,13 +105,25 @@ __device__ __forceinline__ void fft256(double2 (&v)[XE], int t, unsigned wr0, un
 // [6] loop cycles of warp 0; [7] tiles.
 __device__ unsigned long long xw_prof[8];
 
-// PARK: while A_0 is transformed and during the first inverse transform the
-// other register array (FFT(B), then s) waits in the warp's column of R, which
-// is free from the moment A_0 has been read until output 0 is written: one
-// 16-element array live per transform instead of two.
-template <bool LSU, bool PARK>
-__global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, double2* spec, int tiles,
-                                                        const __grid_constant__ CUtensorMap tmap, int dbg) {
+// Tensor maps of a launch: the input (this rank's x-pass input, or the
+// spectrum itself on one device) and one output map per destination rank.
+struct XwMaps {
+  CUtensorMap in;
+  CUtensorMap out[kMaxRanks];
+};
+
+// RT (P > 1): the fused backward slab transpose -- the rows [s Xl, (s+1) Xl) of
+// every output tile are TMA-stored straight into the spectrum of the rank s
+// that owns them (peer memory over NVLink when the ranks are devices), at this
+// rank's global y: the routed form of store_xb, a box at a time.
+// Measured and dropped (512^3, profiles/r2_x512_dbg.md): the copy warps writing
+// the tiles back with st.global instead of TMA stores (6.64 vs 3.75 ms), and
+// parking the idle register array in the free column of R during two of the
+// four transforms (20 700 vs 20 100 cycles per tile: register pressure is not
+// what limits the transform warps).
+template <bool RT>
+__global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, int tiles,
+                                                        const __grid_constant__ XwMaps maps, int dbg) {
   extern __shared__ unsigned char smraw[];
   // 1024-byte alignment: the swizzle pattern is a function of the address
   unsigned char* const sm0 =
@@ -158,30 +171,23 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
       bulk::mbar_expect_tx(full, XTILE);
 #pragma unroll
       for (int r0 = 0; r0 < XN; r0 += 256)
-        bulk::tma3d(tile + r0 * 128, &tmap, 2 * kz0, y, (i * 3 + q) * XN + r0, full);
+        bulk::tma3d(tile + r0 * 128, &maps.in, 2 * kz0, y, (i * 3 + q) * XN + r0, full);
     };
-    auto store = [&](int k) {
+    auto store = [&](int k) {  // lane 0
       int kz0, y, i;
       tile_of(k, kz0, y, i);
-      if constexpr (LSU) {
-        // 8 lanes per 128-byte row, 4 rows per instruction, straight from the
-        // swizzled tile: the warp blocks on the stores, nobody else does
-        const int rr = lane >> 3, c = lane & 7;
-        const int64_t xstride = int64_t(g.Ny) * g.nzh;
-        double2* const dst = spec + int64_t(i * 3 + q) * XN * xstride + int64_t(y) * g.nzh + kz0 + c;
-#pragma unroll 4
-        for (int it = 0; it < XN / 4; ++it) {
-          const int r = it * 4 + rr;
-          dst[int64_t(r) * xstride] = *reinterpret_cast<const double2*>(tile + (r << 7) + ((c ^ (r & 7)) << 4));
-        }
-        __syncwarp();  // every lane's reads of the tile are done
-        bulk::fence_async_smem();
-      } else if (lane == 0) {
+      if constexpr (!RT) {
 #pragma unroll
         for (int r0 = 0; r0 < XN; r0 += 256)
-          bulk::tma3d_store(&tmap, 2 * kz0, y, (i * 3 + q) * XN + r0, tile + r0 * 128);
-        bulk::bulk_commit();
+          bulk::tma3d_store(&maps.out[0], 2 * kz0, y, (i * 3 + q) * XN + r0, tile + r0 * 128);
+      } else {
+        const int box = g.Xl < 256 ? g.Xl : 256;  // rows per store: never across two owners
+        for (int r0 = 0; r0 < XN; r0 += box) {
+          const int s = r0 / g.Xl;
+          bulk::tma3d_store(&maps.out[s], 2 * kz0, g.y0 + y, (i * 3 + q) * g.Xl + (r0 - s * g.Xl), tile + r0 * 128);
+        }
       }
+      bulk::bulk_commit();
     };
     long long t_idle = 0, t_drain = 0;
     const bool prof = (dbg & 16) && lane == 0;
@@ -195,9 +201,9 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
       while (!bulk::mbar_test(staged, k & 1)) __nanosleep(256);
       const long long c1 = prof ? clock64() : 0;
       const int out = late ? k - 1 : k;  // the tile whose output sits in the buffer
-      if (out >= 0) {
+      if (out >= 0 && lane == 0) {
         store(out);
-        if (!LSU && lane == 0 && out + 1 < K) bulk::bulk_wait_read();
+        if (out + 1 < K) bulk::bulk_wait_read();
       }
       if (prof) t_idle += c1 - c0, t_drain += clock64() - c1;
       if (lane == 0) {
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     }
     if (prof) atomicAdd(&xw_prof[2 + (buf == 2)], (unsigned long long)t_drain),
         atomicAdd(&xw_prof[4 + (buf == 2)], (unsigned long long)t_idle);
-    if (!LSU && lane == 0) bulk::bulk_wait_all();  // the stores are performed before the CTA retires
+    if (lane == 0) bulk::bulk_wait_all();  // the stores are performed before the CTA retires
     return;
   }
 
@@ -288,15 +294,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     }
 #pragma unroll
     for (int m = 0; m < XE; ++m) v[m] = *at(R, m);
-    if constexpr (PARK) {
-#pragma unroll
-      for (int m = 0; m < XE; ++m) *at(R, m) = X[m];
-    }
     fwd(v);
-    if constexpr (PARK) {
-#pragma unroll
-      for (int m = 0; m < XE; ++m) X[m] = *at(R, m);
-    }
     // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
 #pragma unroll
     for (int m = 0; m < XE; ++m) {
@@ -313,15 +311,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
       const double f = freq_of(kslot<XTH, XH>(t, h, m), XN) * g.invL[0];
       v[m] = make_double2(X[m].x * f, X[m].y * f);
     }
-    if constexpr (PARK) {
-#pragma unroll
-      for (int m = 0; m < XE; ++m) *at(R, m) = X[m];
-    }
     inv(v);
-    if constexpr (PARK) {
-#pragma unroll
-      for (int m = 0; m < XE; ++m) X[m] = *at(R, m);
-    }
 #pragma unroll
     for (int m = 0; m < XE; ++m) *at(R, m) = v[m];
     bulk::fence_async_smem();
@@ -358,31 +348,35 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
 }  // namespace
 
 bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
-  if (g.Nx != XN || g.P != 1 || g.nzh % XTW != 0) return false;
-  CUtensorMap map;
-  if (!x_tensor_map(spec, 9 * XN, g.Ny, g.nzh, XTW, true, &map)) return false;
-  // FM_XW_TMA_STORE=0: the copy warps write the tiles back with their own
-  // (coalesced, blocking) stores instead of TMA stores.  Measured at 512^3:
-  // 6.64 against 3.75 ms -- one warp per buffer cannot keep 64 KB of stores
-  // in flight next to the transform warps.
-  static const bool tma_store = [] {
-    const char* e = getenv("FM_XW_TMA_STORE");
-    return !e || atoi(e) != 0;
-  }();
-  static const bool park = [] {
-    const char* e = getenv("FM_XW_PARK");
-    return e && atoi(e) != 0;
-  }();
-  using Kern = void (*)(Geo, const double2*, double2*, int, const CUtensorMap, int);
-  const Kern kern = tma_store ? (park ? k_x_warp<false, true> : k_x_warp<false, false>)
-                              : (park ? k_x_warp<true, true> : k_x_warp<true, false>);
+  if (g.Nx != XN || g.nzh % XTW != 0) return false;
+  const bool routed = g.P > 1;
+  if (routed) {
+    // FM_XW_ROUTED=0: P > 1 keeps the routed k_x_stream (per-element peer stores)
+    static const bool on = [] {
+      const char* e = getenv("FM_XW_ROUTED");
+      return !e || atoi(e) != 0;
+    }();
+    if (!on || g.P > kMaxRanks || g.Xl % 8 != 0 || XN % g.Xl != 0 || int(ctx->h_dst_a.size()) < g.P) return false;
+  }
+  XwMaps maps;
+  if (!x_tensor_map(spec, 9 * XN, g.Ny, g.nzh, XTW, true, 256, &maps.in)) return false;
+  if (!routed) {
+    maps.out[0] = maps.in;
+  } else {
+    const int box = g.Xl < 256 ? g.Xl : 256;
+    for (int s = 0; s < g.P; ++s)  // A_s viewed as [9 Xl][Ny global][2 nzh]
+      if (!ctx->h_dst_a[s] || !x_tensor_map(ctx->h_dst_a[s], 9 * g.Xl, g.Nyg, g.nzh, XTW, true, box, &maps.out[s]))
+        return false;
+  }
+  using Kern = void (*)(Geo, const double2*, int, const XwMaps, int);
+  const Kern kern = routed ? k_x_warp<true> : k_x_warp<false>;
   set_smem_limit(reinterpret_cast<const void*>(kern), int(XSMEM));
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = (g.nzh / XTW) * g.Ny * 3;
   const int grid = std::min(tiles, std::max(sms, 1));
-  kern<<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, spec, tiles, map, dbg);
+  kern<<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, tiles, maps, dbg);
   if (dbg & 16) {  // timing experiments only: per-tile averages to stderr
     unsigned long long h[8] = {}, z[8] = {};
     cudaStreamSynchronize(ctx->stream);

@@ -1,6 +1,8 @@
 """GPU parity of the projection G and the projected tangent G(K : dF^T)
 against the CPU oracle (restating projection.cpp:123-194), plus the
 reference's own property assertions (test_projection.cpp:96-244) on the GPU."""
+import os
+
 import numpy as np
 import pytest
 
@@ -193,3 +195,32 @@ def test_config4_oracle_equality_128():
     with abi.Context(pts, 3) as ctx:
         got = ctx.projection(ctx.field(9, x)).download()
     assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def _digest_child(pts, env):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, hashlib; sys.path.insert(0, %r)\n"
+        "from paper_1603_08893_b200 import abi, microstructure as M\n"
+        "pts = %r\n"
+        "A = M.uniform_field(pts, 9, seed=21)\n"
+        "with abi.Context(pts, 3) as ctx:\n"
+        "    out = ctx.projection(ctx.field(9, A)).download()\n"
+        "    print(hashlib.sha1(out.tobytes()).hexdigest(), ','.join(ctx.kernel_names))\n" % (root, pts))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return r.stdout.split()
+
+
+@pytest.mark.parametrize("pts", [(512, 64, 32), (512, 16, 128)])
+def test_warp_per_line_x_pass_is_bit_identical_to_the_lockstep_one(pts):
+    """The 512-point x pass k_x_warp (one warp per line, TMA in and out,
+    projection_xw.cu) against the lane-pair k_x_stream it replaced
+    (FM_XDIRECT=4): same butterflies in the same order, so the same bits."""
+    new, names_new = _digest_child(pts, {})
+    old, names_old = _digest_child(pts, {"FM_XDIRECT": "4"})
+    assert "k_x_warp" in names_new and "k_x_stream" in names_old, (names_new, names_old)
+    assert new == old
