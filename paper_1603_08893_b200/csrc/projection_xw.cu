@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     pair_dit<XTH, 1>(v, t, h, twp());
   };
   auto inv = [&](double2(&v)[XE]) {
-    if (dbg & 1) return;
+    if (dbg & 33) return;  // (bit 5: only the inverse transforms skipped -- how far the TMA pipeline can follow)
     pair_dif<XTH, 1>(v, t, h, twp());
     fft256<+1>(v, t, wr0, rd0, twp());
   };
