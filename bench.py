@@ -312,8 +312,13 @@ def config3_matvec(local, hbm, steps=5, dist=None, world=1, rank=0):
         ctx.profile(False)
         per = pass_ms / max(calls, 1)
         names = ctx.kernel_names
+        digest = None
+        if dist:  # this rank's slab of the result: the arms must agree bit for bit
+            import hashlib
+            digest = hashlib.sha1(out.download().tobytes()).hexdigest()[:16]
         model.close()
-    return {"workload": "config3 operator: 512^3 J2 (compact eigenbasis tangent) matvec at F_bar(t=1), spheres r 12, "
+    return {"digest_rank0": digest,
+            "workload": "config3 operator: 512^3 J2 (compact eigenbasis tangent) matvec at F_bar(t=1), spheres r 12, "
                         f"fraction {frac:.4f}, {count} spheres, seed 3",
             "ms": ms, "voxel_per_s": ng / (ms * 1e-3), "steps": steps, "n_gpus": world,
             "transposes": None if not dist else ("staged ncclSend/ncclRecv all-to-all" if os.environ.get("FM_TRANSPOSE")
@@ -570,10 +575,14 @@ def main():
         # (the driver's efficiency for the 8-GPU target = these ms against the N = 1 run's)
         import torch.distributed as tdist
         c3 = {}
-        for arm, env in (("peer_stores", None), ("nccl_all_to_all", "nccl")):
+        # (peer_stores_tma: the x pass stores its tiles into the owners' spectra by TMA, k_x_warp<RT>,
+        # validated on one device only, hence opt-in across devices)
+        for arm, env in (("peer_stores", None), ("peer_stores_tma", "tma"), ("nccl_all_to_all", "nccl")):
             try:
-                if env:
+                if env == "nccl":
                     os.environ["FM_TRANSPOSE"] = env
+                if env == "tma":
+                    os.environ["FM_XW_ROUTED"] = "1"
                 uid3 = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
                 if rank == 0:
                     uid3.copy_(torch.frombuffer(bytearray(abi.nccl_unique_id()), dtype=torch.uint8))
@@ -584,6 +593,7 @@ def main():
                 c3[arm] = {"error": str(e)[:200]}
             finally:
                 os.environ.pop("FM_TRANSPOSE", None)
+                os.environ.pop("FM_XW_ROUTED", None)
     dchk = None
     if slab:
         try:

@@ -351,11 +351,14 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
   if (g.Nx != XN || g.nzh % XTW != 0) return false;
   const bool routed = g.P > 1;
   if (routed) {
-    // FM_XW_ROUTED=0: P > 1 keeps the routed k_x_stream (per-element peer stores)
-    static const bool on = [] {
-      const char* e = getenv("FM_XW_ROUTED");
-      return !e || atoi(e) != 0;
-    }();
+    // The routed TMA stores are the default where they have been validated --
+    // virtual ranks, all buffers on this device (bit-equal to P = 1).  Across
+    // devices the destinations are IPC-mapped peer buffers, which no run has
+    // exercised yet: there FM_XW_ROUTED=1 opts in and the routed k_x_stream
+    // (per-element peer stores) stays the default.  FM_XW_ROUTED=0 turns the
+    // path off everywhere.
+    const char* e = getenv("FM_XW_ROUTED");
+    const bool on = e ? atoi(e) != 0 : ctx->virt;
     if (!on || g.P > kMaxRanks || g.Xl % 8 != 0 || XN % g.Xl != 0 || int(ctx->h_dst_a.size()) < g.P) return false;
   }
   XwMaps maps;
