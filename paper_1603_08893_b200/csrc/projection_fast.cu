@@ -1233,9 +1233,8 @@ int launched(fm_ctx* ctx, const char* what) {
   return e == cudaSuccess ? FM_OK : check_cuda(ctx, e, what);
 }
 
-template <int N>
-bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st) {
-  constexpr int TW = N >= 1024 ? 4 : 8;  // 4-column tiles measured slower at 256^3 and 512^3
+template <int N, int TW>
+bool y_launch_tw(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st) {
   constexpr int T = N / e_line(N);
   const size_t smem = size_t(N) * TW * 16;
   const dim3 grid(ctx->nzh / TW, g.Nx, ctx->ncomp);
@@ -1251,6 +1250,23 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
   }
   *st = launched(ctx, "k_y_fast");
   return true;
+}
+template <int N>
+bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* out, int* st) {
+  // 8 kz columns = one 128-byte segment per row (4-column tiles measured slower
+  // at 256^3 and 512^3).  At 1024 points 8 columns are a 128 KB exchange buffer
+  // and one 512-thread CTA per SM; FM_Y1024_TW=4 selects 4 columns (two CTAs of
+  // 256 threads, 64-byte segments) for the A/B.
+  if constexpr (N >= 1024) {
+    static const int tw = [] {
+      const char* e = getenv("FM_Y1024_TW");
+      return e ? atoi(e) : 4;
+    }();
+    if (tw == 8 && ctx->nzh % 8 == 0) return y_launch_tw<N, 8>(ctx, g, sign, in, out, st);
+    return y_launch_tw<N, 4>(ctx, g, sign, in, out, st);
+  } else {
+    return y_launch_tw<N, 8>(ctx, g, sign, in, out, st);
+  }
 }
 
 // RT: the slab-transpose-fused instantiation (P > 1); P = 1 runs the plain one
