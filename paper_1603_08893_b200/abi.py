@@ -14,7 +14,8 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfftmech_b200.so")
+# (FM_LIB: another build of the same library, for A/B runs of compile-time variants)
+LIB_PATH = os.environ.get("FM_LIB") or os.path.join(_HERE, "lib", "libfftmech_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "fftmech_b200.h")
 
 FM_OK = 0

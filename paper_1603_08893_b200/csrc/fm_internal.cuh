@@ -217,6 +217,9 @@ struct ProArgs {
   // where p_old is loaded anyway (pipelined SVK pass 1 only)
   double* x = nullptr;
   const double* alpha = nullptr;
+  // timing experiments only (FM_ZP_DBG, pipelined pass 1): bit 0 skips the SVK
+  // action, bit 1 the transforms, bit 2 the stores, bit 3 the TMA loads
+  int dbg = 0;
 };
 // Epilogue of the last pass: per-block partial sums of <pdot, out>
 // (the CG curvature <p, Ap>, solver.cpp:37) written to `partial`.

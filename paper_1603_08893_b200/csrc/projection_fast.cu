@@ -778,8 +778,25 @@ constexpr int kPipeCopyMinB = FM_PIPE_COPY_MINB;
 // 96-register budget spills (256^3 pass 1: 0.83 ms at 4, 0.69 ms at 3 CTAs/SM)
 constexpr int kPipeLabMinB = FM_PIPE_LAB_MINB;
 
+// FM_ZP_DBG (timing experiments: parts of the pipelined pass switched off) only
+// exists in builds with -DFM_ZP_DEBUG: the run-time tests cost the SVK pass 7 %.
+#ifdef FM_ZP_DEBUG
+#define ZP_DBG(pa, bit) ((pa).dbg & (bit))
+#else
+#define ZP_DBG(pa, bit) 0
+#endif
+
+// FM_ZPIPE_EF: elements per lane of the pipelined pass's transforms at M = 128
+// (8: 16 lanes per component line, all 144 threads transform, 128 = 8 x 8 x 2
+// with two exchanges; 16: 8 lanes per line, 128 = 16 x 8 with one exchange, the
+// 72 lanes of lines 0..8 in three warps).
+#ifndef FM_ZPIPE_EF
+#define FM_ZPIPE_EF 8
+#endif
 template <int M>
 struct ZPipe {
+  static constexpr int EF = (M == 128) ? FM_ZPIPE_EF : reg::e_z(M);  // transform shape
+  static constexpr int TF = M / EF;
   static constexpr int E = reg::e_z(M), T = M / E;
   static constexpr int LSP = 9;  // one line per CTA: 9 component lines (line-major, swizzled)
   static constexpr int THREADS = 9 * T;
@@ -807,8 +824,9 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   using S = ZPipe<M>;
   constexpr int N = 2 * M, T = S::T, E = S::E, NCH = pipe_chunks<PRO, DIR, XUPD, LAB>();
   static_assert(!LAB || PRO == PRO_SVK, "phase labels replace the SVK lambda / mu chunks");
-  constexpr int SW = reg::ilog2(E);  // line-major swizzled line buffer (reg::fft_swz)
-  static_assert(32 % T == 0, "a component line must not straddle a warp");
+  constexpr int EF = S::EF, TF = S::TF;
+  constexpr int SW = reg::ilog2(EF);  // line-major swizzled line buffer (reg::fft_swz)
+  static_assert(32 % T == 0 && 32 % TF == 0, "a component line must not straddle a warp");
   static_assert(!XUPD || (DIR && PRO == PRO_SVK), "x update rides on the SVK direction prologue");
   extern __shared__ __align__(16) double2 sm[];
   double* stage = reinterpret_cast<double*>(sm + (LB2 ? 2 : 1) * M * S::LSP);  // NCH chunks of N doubles
@@ -816,6 +834,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   const int nxy = g.Nx * g.Ny;
   const int64_t n = g.n;
   auto issue = [&](int L) {
+    if (ZP_DBG(pa, 8)) return;
     const int64_t node0 = g.roff + int64_t(L) * N;
     bulk::mbar_expect_tx(&bar, NCH * N * 8 + (LAB ? N : 0));
     int q = 0;
@@ -847,7 +866,7 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
   if (threadIdx.x == 0 && L < nxy) issue(L);
   unsigned phase = 0;
   for (; L < nxy; L += gridDim.x) {
-    bulk::mbar_wait(&bar, phase);
+    if (!ZP_DBG(pa, 8)) bulk::mbar_wait(&bar, phase);
     double2* const lsm = sm + (LB2 && phase ? M * S::LSP : 0);  // this line's buffer
     phase ^= 1;
     // prologue on voxel pairs (z, z+1) out of the staging area
@@ -903,8 +922,13 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
           lm = *reinterpret_cast<const double2*>(stage + (FB + 9) * N + 2 * m);
           mu = *reinterpret_cast<const double2*>(stage + (FB + 10) * N + 2 * m);
         }
-        svk_action<3>(f0, d0, lm.x, mu.x, v0);
-        svk_action<3>(f1, d1, lm.y, mu.y, v1);
+        if (ZP_DBG(pa, 1)) {
+#pragma unroll
+          for (int c = 0; c < 9; ++c) v0[c] = d0[c] + f0[c] * lm.x, v1[c] = d1[c] + f1[c] * mu.y;
+        } else {
+          svk_action<3>(f0, d0, lm.x, mu.x, v0);
+          svk_action<3>(f1, d1, lm.y, mu.y, v1);
+        }
         if constexpr (PAP) {
 #pragma unroll
           for (int c = 0; c < 9; ++c) pap += d0[c] * v0[c];
@@ -923,26 +947,34 @@ __global__ void __launch_bounds__(ZPipe<M>::THREADS, MINB) k_zf_pipe(Geo g, cons
     }
     __syncthreads();  // staging consumed, packed line in lsm
     if (threadIdx.x == 0 && L + int(gridDim.x) < nxy) issue(L + gridDim.x);
-    {
-      // component c's line in the T lanes of one warp: swizzled exchange with
-      // warp syncs, untangling by shuffle, spectrum stored from registers
-      const int c = threadIdx.x / T, t = threadIdx.x % T;
+    // component c's line in the TF lanes of one warp: swizzled exchange with
+    // warp syncs, untangling by shuffle, spectrum stored from registers.  With
+    // TF < T only the first 9 TF lanes hold lines; the rest of their last warp
+    // redoes line 8 (same values to the same addresses) so that the warp-level
+    // syncs stay full, and stores nothing.
+    constexpr int FT = ((9 * TF + 31) / 32) * 32;  // transform threads: whole warps
+    if (int(threadIdx.x) < FT) {
+      const int cs = threadIdx.x / TF, c = cs < 9 ? cs : 8, t = threadIdx.x % TF;
       double2* line = lsm + c * M;
-      double2 v[E];
+      double2 v[EF];
 #pragma unroll
-      for (int m = 0; m < E; ++m) v[m] = line[reg::xaddr<SW>(t + T * m, 0)];
+      for (int m = 0; m < EF; ++m) v[m] = line[reg::xaddr<SW>(t + TF * m, 0)];
       __syncwarp();
-      reg::fft_swz<M, E, -1>(v, line, t, twM);
+      if (!ZP_DBG(pa, 2)) reg::fft_swz<M, EF, -1>(v, line, t, twM);
       double2* dst = spec + (int64_t(c) * nxy + L) * M;
 #pragma unroll
-      for (int m = 0; m < E; ++m) {
-        const int k = t + T * m;
+      for (int m = 0; m < EF; ++m) {
+        const int k = t + TF * m;
         const double2 a = v[m];
-        const double2 b = cconj(mirror_take<T>(mirror_give<E>(v, t, m), t));
-        const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
-        const double2 D = csub(a, b);
-        const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
-        dst[k] = cadd(Ev, cmul(O, __ldg(&twN[k])));
+        double2 res = a;
+        if (!ZP_DBG(pa, 2)) {
+          const double2 b = cconj(mirror_take<TF>(mirror_give<EF>(v, t, m), t));
+          const double2 Ev = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+          const double2 D = csub(a, b);
+          const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+          res = cadd(Ev, cmul(O, __ldg(&twN[k])));
+        }
+        if (!ZP_DBG(pa, 4) && cs < 9) dst[k] = res;
       }
     }
     // one buffer: wait until every warp is done with it; two: the next
@@ -1550,8 +1582,14 @@ bool zpipe_go2(fm_ctx* ctx, const Geo& g, const ProArgs& pa, double2* spec) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int nxy = g.Nx * g.Ny;
     const int grid = std::min(nxy, std::max(sms, 1) * per_sm);
+    static const int zdbg = [] {
+      const char* e = getenv("FM_ZP_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    ProArgs pad = pa;
+    pad.dbg = zdbg;
     k_zf_pipe<M, PRO, DIR, MB, PAP, XUPD, LAB, LB2>
-        <<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pa, spec);
+        <<<grid, ZPipe<M>::THREADS, smem, ctx->stream>>>(g, ctx->pzh.tw, ctx->pz.tw, pad, spec);
     ctx->zf_partials = grid;
     return true;
   }
