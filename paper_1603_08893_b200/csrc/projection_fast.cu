@@ -682,9 +682,12 @@ using ZShape = typename ZShapeSel<M, HEAVY>::type;
 #ifndef FM_ZF_J2C_MINB
 #define FM_ZF_J2C_MINB 3
 #endif
+#ifndef FM_ZF_SVK_MINB
+#define FM_ZF_SVK_MINB 3  // (4: 96 registers, measured with FM_ZPIPE=0 at 256^3: see profiles/r2_svk_pass1_dbg.md)
+#endif
 template <int PRO, int M>
 constexpr int zf_minb() {
-  return std::min(PRO == PRO_K4 ? 4 : (PRO == PRO_COPY ? 1 : (PRO == PRO_J2C ? FM_ZF_J2C_MINB : 3)),
+  return std::min(PRO == PRO_K4 ? 4 : (PRO == PRO_COPY ? 1 : (PRO == PRO_J2C ? FM_ZF_J2C_MINB : FM_ZF_SVK_MINB)),
                   std::max(1, 65536 / (ZShape<M, PRO != PRO_COPY>::THREADS * 96)));
 }
 template <int M, int PRO, bool DIR, bool PAP = false>
