@@ -325,8 +325,27 @@ def config3_128():
     print("config3_128 band", [[r["cg_it"] for r in run[2]] for run in runs])
 
 
+def _proj(N):
+    """BASELINE config 4: G applied to a seeded i.i.d. U(-1,1) 3x3 tensor field
+    (projection.cpp:123-171) at N^3; samples, norm and checksums of the output."""
+    O.set_threads()
+    pts = (N, N, N)
+    A = M.uniform_field(pts, 9, 4)
+    t = time.time()
+    out, st, _ = O.apply_projection(pts, 3, A)
+    assert st == 0
+    del A
+    res = _fields("out", out, 9)
+    np.savez_compressed(os.path.join(HERE, f"proj{N}.npz"), **res)
+    print(f"proj{N}", time.time() - t, res["out_norm"])
+
+
+def proj256():
+    _proj(256)  # (512^3 needs more than the 62 GB of this container: the oracle keeps ghat and a complex copy)
+
+
 if __name__ == "__main__":
     sys.path.insert(0, os.path.dirname(HERE))
     for w in sys.argv[1:]:
-        if w in ("config2", "matvec256", "config3_128"):
+        if w in ("config2", "matvec256", "config3_128", "proj256"):
             globals()[w]()

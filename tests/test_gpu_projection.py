@@ -224,3 +224,29 @@ def test_warp_per_line_x_pass_is_bit_identical_to_the_lockstep_one(pts):
     old, names_old = _digest_child(pts, {"FM_XDIRECT": "4"})
     assert "k_x_warp" in names_new and "k_x_stream" in names_old, (names_new, names_old)
     assert new == old
+
+
+def test_projection_256_matches_oracle_golden():
+    """BASELINE config 4 at 256^3 against the CPU oracle (tests/golden/make_golden.py
+    proj256 -> proj256.npz: 2^20 fixed samples, norm and per-component checksums of
+    G applied to the seeded U(-1,1) field), 1e-12; the 512^3 run of the oracle does
+    not fit the CPU container, where the analytic known-answer test
+    (test_gpu_config4_known_answer.py) and the idempotence check take over."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from golden_util import checksums, rel, sample_index
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "proj256.npz"))
+    pts = (256, 256, 256)
+    A = M.uniform_field(pts, 9, 4)
+    with abi.Context(pts, 3) as ctx:
+        fa = ctx.field(9, A)
+        out = ctx.projection(fa)
+        x = out.download()
+        again = ctx.projection(out).download()  # compatibility: G(G(x)) = G(x)
+    idx = sample_index(g["out_samp"].size, x.size)
+    assert rel(x[idx], g["out_samp"]) <= 1e-12
+    assert abs(np.linalg.norm(x) - g["out_norm"]) <= 1e-12 * g["out_norm"]
+    cs, ref = checksums(x, 9), g["out_sums"]
+    assert np.all(np.abs(cs[1] - ref[1]) <= 1e-12 * ref[1])
+    assert np.all(np.abs(cs[0] - ref[0]) <= 1e-12 * np.sqrt(ref[1] * 256 ** 3))
+    assert np.linalg.norm(again - x) <= 1e-13 * np.linalg.norm(x)
