@@ -240,6 +240,14 @@ template <int N, int TW, int E>
 constexpr int x4_minb() {  // CTAs/SM the register budget targets: capped by the two tile buffers
   return std::max(1, std::min(E >= 16 ? 3 : 2, int((227 * 1024) / (2 * size_t(N) * TW * 16 + 1024))));
 }
+// FM_X4_DBG (builds with -DFM_X4_DEBUG only; timing experiments): bit 0 skips
+// the transforms, bit 1 the stores, bit 2 the tile loads.
+#ifdef FM_X4_DEBUG
+__device__ int x4_dbg_bits;
+#define X4_DBG(bit) (x4_dbg_bits & (bit))
+#else
+#define X4_DBG(bit) 0
+#endif
 template <int N, int TW, int E, bool RT = false>
 __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo g, const double2* __restrict__ tw,
                                                        double2* __restrict__ spec) {
@@ -252,6 +260,7 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
   double2* tile = spec + int64_t(i * 3) * N * xstride + int64_t(y) * g.nzh + blockIdx.x * TW;
   auto fetch = [&](int q, double2* buf) {
     const double2* src = tile + int64_t(q) * N * xstride;
+    if (X4_DBG(4)) return;
     for (int w = threadIdx.x; w < N * TW; w += blockDim.x) {
       const int row = w / TW, ll = w - row * TW;
       cp_async16(buf + w, src + int64_t(row) * xstride + ll);
@@ -288,7 +297,8 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
     }
     __syncthreads();
     double2* X = q == 0 ? buf0 : buf1;
-    reg::fft<N, E, -1>(v, X + l, TW, t, tw);  // ends past a barrier: X is free again
+    if (!X4_DBG(1)) reg::fft<N, E, -1>(v, X + l, TW, t, tw);  // ends past a barrier: X is free again
+    else __syncthreads();
     if (q == 0) {
       fetch(2, buf0);
 #pragma unroll
@@ -321,10 +331,11 @@ __global__ void __launch_bounds__(TW*(N / E), x4_minb<N, TW, E>()) k_x_fast4(Geo
       const double f = q == 0 ? freq_of(t + T * m, N) * g.invL[0] : 1.0;
       v[m] = make_double2(s[m].x * f, s[m].y * f);
     }
-    reg::fft<N, E, +1>(v, (q == 0 ? buf0 : buf1) + l, TW, t, tw);
+    if (!X4_DBG(1)) reg::fft<N, E, +1>(v, (q == 0 ? buf0 : buf1) + l, TW, t, tw);
 #pragma unroll 1
     for (int j = q; j < (q == 0 ? 1 : 3); ++j) {
       const double f = j == 0 ? 1.0 : (j == 1 ? xiy : xiz);
+      if (X4_DBG(2)) continue;
       if constexpr (!RT) {
 #pragma unroll
         for (int m = 0; m < E; ++m)
@@ -1323,6 +1334,13 @@ void x4_rt(fm_ctx* ctx, const Geo& g, double2* spec) {
   constexpr int T = N / E;
   const size_t smem = size_t(2) * N * TW * 16;
   allow(k_x_fast4<N, TW, E, RT>, smem);
+#ifdef FM_X4_DEBUG
+  {
+    const char* e = getenv("FM_X4_DBG");
+    const int bits = e ? atoi(e) : 0;
+    cudaMemcpyToSymbolAsync(x4_dbg_bits, &bits, sizeof(bits), 0, cudaMemcpyHostToDevice, ctx->stream);
+  }
+#endif
   const dim3 grid(ctx->nzh / TW, g.Ny, 3);
   k_x_fast4<N, TW, E, RT><<<grid, TW * T, smem, ctx->stream>>>(g, ctx->px.tw, spec);
 }
