@@ -1508,6 +1508,7 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
   }
   if (done) {
   } else if (zc && N >= 64 && ctx->nzh % X4TW == 0) {  // (8 elements/thread at 512: 6.5 vs 5.9 ms)
+    // (16-column tiles = 256-byte row segments at 256 points, one CTA per SM: 0.656 vs 0.479 ms in the debug build)
     x4_go<N, X4TW, e_line(N)>(ctx, g, spec);
     name = "k_x_fast4";
   } else if (N <= 512 && ctx->nzh % 8 == 0 && !(zc && N < 64)) {
