@@ -213,11 +213,11 @@ if __name__ == "__main__" and "config3_64_band" in sys.argv[1:]:
 
 # ---------------------------------------------------------------------------
 # Large-grid fixtures (BASELINE configs 2 and 3): too big to commit whole, so
-# the fixture holds the run record, full-field norms and checksums, and 2^20
+# the fixture holds the run record, full-field norms and checksums, and 2^18
 # fixed (component, node) samples of each field (tests/golden_util.py).
 # The oracle runs threaded here (bit-identical to one thread, see
 # oracle/fftmech_oracle.cpp par_for).
-NSAMP = 1 << 20
+NSAMP = 1 << 18
 
 
 def _record(reps):

@@ -4,7 +4,7 @@ solver.cpp:73-160, projection.cpp:123-194, hyperelastic.cpp:10-65):
 
 * one 256^3 matvec G(K4 : dF^T) in the reference operator form (K4
   materialised) and in the matrix-free form the bench times (the pipelined
-  SVK pass 1), against the oracle's K4 + apply_projected_tangent: 2^20 fixed
+  SVK pass 1), against the oracle's K4 + apply_projected_tangent: 2^18 fixed
   samples, the full-field norm and per-component checksums, 1e-12;
 * the full config-2 Newton solve (256^3 SVK, Bernoulli(0.3) seed 2, contrast
   10, one increment to F_bar = I + 0.1 e_x e_y) through fm_solve_increment,

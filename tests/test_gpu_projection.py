@@ -228,7 +228,7 @@ def test_warp_per_line_x_pass_is_bit_identical_to_the_lockstep_one(pts):
 
 def test_projection_256_matches_oracle_golden():
     """BASELINE config 4 at 256^3 against the CPU oracle (tests/golden/make_golden.py
-    proj256 -> proj256.npz: 2^20 fixed samples, norm and per-component checksums of
+    proj256 -> proj256.npz: 2^18 fixed samples, norm and per-component checksums of
     G applied to the seeded U(-1,1) field), 1e-12; the 512^3 run of the oracle does
     not fit the CPU container, where the analytic known-answer test
     (test_gpu_config4_known_answer.py) and the idempotence check take over."""
