@@ -331,7 +331,9 @@ bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double
              int* st);
 // Cached CUtensorMap (written to out_map) of a spectral buffer viewed as
 // [rows][Ny][2 nzh] doubles with a (2 TW, 1, box_rows) box (projection_fast.cu).
-bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, int box_rows, void* out_map);
+// split2: rows viewed as [rows / 2][2]: the even and the odd rows are separate boxes (4-D map).
+bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, int box_rows, void* out_map,
+                  bool split2 = false);
 // 512-point x pass, one warp per line, TMA in and out (projection_xw.cu).
 bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg);
 

@@ -1367,13 +1367,15 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 }  // namespace
-bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, int box_rows, void* out_map) {
+bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, int box_rows, void* out_map,
+                  bool split2) {
   CUtensorMap* out = static_cast<CUtensorMap*>(out_map);
   struct Entry {
     const void* base;
     int rows, Ny, nzh, TW;
     bool swz;
     int box_rows;
+    bool split2;
     CUtensorMap map;
   };
   static std::mutex mx;
@@ -1390,11 +1392,11 @@ bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz1
   if (!enc) return false;
   std::lock_guard<std::mutex> lk(mx);
   for (const Entry& e : cache)
-    if (e.base == base && e.rows == rows && e.Ny == Ny && e.nzh == nzh && e.TW == TW && e.swz == swz128 && e.box_rows == box_rows) {
+    if (e.base == base && e.rows == rows && e.Ny == Ny && e.nzh == nzh && e.TW == TW && e.swz == swz128 && e.box_rows == box_rows && e.split2 == split2) {
       *out = e.map;
       return true;
     }
-  Entry e{base, rows, Ny, nzh, TW, swz128, box_rows, {}};
+  Entry e{base, rows, Ny, nzh, TW, swz128, box_rows, split2, {}};
   const cuuint64_t dims[3] = {cuuint64_t(2 * nzh), cuuint64_t(Ny), cuuint64_t(rows)};
   const cuuint64_t strides[2] = {cuuint64_t(nzh) * 16, cuuint64_t(Ny) * nzh * 16};
   const cuuint32_t box[3] = {cuuint32_t(2 * TW), 1, cuuint32_t(box_rows)};
@@ -1410,10 +1412,22 @@ bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz1
                                     : pm == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                                     : pm == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                               : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  if (enc(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, pr,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
+  CUresult rc;
+  if (!split2) {
+    rc = enc(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, pr,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    // rows split by parity: [rows / 2][2][Ny][2 nzh] -- even and odd x-rows of every component are separate boxes
+    const cuuint64_t d4[4] = {cuuint64_t(2 * nzh), cuuint64_t(Ny), 2, cuuint64_t(rows / 2)};
+    const cuuint64_t s4[3] = {cuuint64_t(nzh) * 16, cuuint64_t(Ny) * nzh * 16, cuuint64_t(2) * Ny * nzh * 16};
+    const cuuint32_t b4[4] = {cuuint32_t(2 * TW), 1, 1, cuuint32_t(box_rows)};
+    const cuuint32_t e4[4] = {1, 1, 1, 1};
+    rc = enc(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), d4, s4, b4, e4,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, pr,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (rc != CUDA_SUCCESS) return false;
   if (cache.size() > 256) cache.clear();
   cache.push_back(e);
   *out = e.map;
@@ -1504,6 +1518,25 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
       g.P > 1 ? xd_rt<N, 8, true>(ctx, g, spec) : xd_rt<N, 8, false>(ctx, g, spec);
       done = true;
       name = "k_x_direct";
+    }
+  }
+  if constexpr (N == 1024) {
+    // FM_XW1024=1: the cluster form of k_x_warp (projection_xw.cu); default k_x_fast4 on 4-column tiles
+    static const bool xw1024 = [] {
+      const char* e = getenv("FM_XW1024");
+      return e && atoi(e) != 0;
+    }();
+    if (zc && xw1024 && g.P == 1) {
+      static const int xdbg1024 = [] {
+        const char* e = getenv("FM_X_DBG");
+        return e ? atoi(e) : 0;
+      }();
+      if (xw_launch(ctx, g, spec, xdbg1024)) {
+        done = true;
+        name = "k_x_warp";
+      } else {
+        cudaGetLastError();
+      }
     }
   }
   if (done) {

@@ -57,7 +57,7 @@ constexpr int XSCR = 4096;                    // exchange scratch per warp
 // sub-partition would cap every thread at 168 registers, so the copy group
 // hands its registers back (setmaxnreg) and the transform groups take 232
 constexpr int XTHREADS = 384;
-constexpr size_t XSMEM = 1024 + 3 * size_t(XTILE) + XTW * size_t(XSCR) + 64;
+constexpr size_t XSMEM = 1024 + 3 * size_t(XTILE) + XTW * size_t(XSCR) + 256;
 
 // Transposing exchange of the two half-lines of a warp: lane (t, h) hands its
 // a[k] to lane (k, h), slot t.  One double per element and round; element p of
@@ -89,13 +89,14 @@ __device__ __forceinline__ void exchange(double2 (&v)[XE], unsigned wr0, unsigne
 // 256-point transform of a half-line held as v[m] = x[t + 16 m] by its 16
 // lanes: the two Stockham radix-16 stages of reg::fft<256, 16, SIGN, 2> (same
 // butterflies, same twiddles W_512^(2 t r)), exchanged as above.
-template <int SIGN>
+// TS: tw is the W_512 table (TS = 1) or the W_1024 table read at stride 2.
+template <int SIGN, int TS>
 __device__ __forceinline__ void fft256(double2 (&v)[XE], int t, unsigned wr0, unsigned rd0,
                                        const double2* __restrict__ tw) {
   reg::Dft<16, SIGN>::run(v);
   exchange(v, wr0, rd0);
 #pragma unroll
-  for (int r = 1; r < 16; ++r) v[r] = reg::tw_mul(v[r], __ldg(&tw[2 * t * r]), SIGN);
+  for (int r = 1; r < 16; ++r) v[r] = reg::tw_mul(v[r], __ldg(&tw[2 * TS * t * r]), SIGN);
   reg::Dft<16, SIGN>::run(v);
 }
 
@@ -121,9 +122,24 @@ struct XwMaps {
 // parking the idle register array in the free column of R during two of the
 // four transforms (20 700 vs 20 100 cycles per tile: register pressure is not
 // what limits the transform warps).
-template <bool RT>
+// CL (1024-point lines): a tile of 8 columns is 128 KB per component -- neither
+// three buffers in one SM's shared memory nor two 16-element arrays per lane
+// hold it -- so the line is split over a cluster of two CTAs: CTA r takes the
+// rows of parity r (a 4-D tensor map makes them a box), runs the same 512-point
+// machinery on its half-line, and the outermost radix-2 step X[k] = E[k] +
+// W^k O[k], X[k + 512] = E[k] - W^k O[k] crosses the CTA pair through
+// distributed shared memory: each warp leaves the eight values per lane its
+// partner needs in its own scratch, signals the partner warp's mbarrier
+// (release at cluster scope) and reads the partner's eight with
+// ld.shared::cluster; a second mbarrier tells it when its scratch may be
+// written again.  The warps stay independent of everything but their partner
+// warp in the other CTA.
+template <bool RT, bool CL>
 __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, int tiles,
                                                         const __grid_constant__ XwMaps maps, int dbg) {
+  static_assert(!(RT && CL), "the cluster form is single-device only");
+  constexpr int TS = CL ? 2 : 1;        // table stride: tw is W_1024 for the cluster form
+  constexpr int NLINE = CL ? 2 * XN : XN;  // points of a whole x-line
   extern __shared__ unsigned char smraw[];
   // 1024-byte alignment: the swizzle pattern is a function of the address
   unsigned char* const sm0 =
@@ -135,6 +151,8 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
   uint64_t* const full_r = bars + 2;     // A_0
   uint64_t* const staged_pq = bars + 3;  // all 8 warps are done with P and Q (count 8)
   uint64_t* const staged_r = bars + 4;   // all 8 warps have written output 0 into R
+  uint64_t* const ready = bars + 8;      // CL, per warp: the partner warp's eight values are in its scratch
+  uint64_t* const consumed = bars + 16;  // CL, per warp: the partner warp has read this warp's scratch
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     bulk::mbar_init(full_p, 1);
@@ -142,13 +160,22 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     bulk::mbar_init(full_r, 1);
     bulk::mbar_init(staged_pq, XTW);
     bulk::mbar_init(staged_r, XTW);
+    if constexpr (CL)
+      for (int i = 0; i < XTW; ++i) {
+        bulk::mbar_init(ready + i, 1);
+        bulk::mbar_init(consumed + i, 1);
+      }
   }
   __syncthreads();
+  const unsigned crank = CL ? bulk::cluster_ctarank() : 0u;  // parity of this CTA's rows
+  if constexpr (CL) bulk::cluster_sync();  // the partner's barriers exist before anything arrives on them
   const int kzb = g.nzh / XTW;
-  const int K = blockIdx.x < tiles ? (tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+  // the unit that walks the tiles: this CTA, or the CTA pair
+  const int unit = CL ? int(blockIdx.x >> 1) : int(blockIdx.x), units = CL ? int(gridDim.x >> 1) : int(gridDim.x);
+  const int K = unit < tiles ? (tiles - 1 - unit) / units + 1 : 0;
   // tile -> (kz block fastest, y, row i)
   auto tile_of = [&](int k, int& kz0, int& y, int& i) {
-    const int T_ = blockIdx.x + k * gridDim.x;
+    const int T_ = unit + k * units;
     kz0 = (T_ % kzb) * XTW;
     const int r = T_ / kzb;
     y = r % g.Ny;
@@ -159,7 +186,10 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::);
     // warp 8: P (component 1), warp 9: Q (component 2), warp 10: R (component 0)
     const int buf = w - XTW;
-    if (buf > 2 || K == 0) return;
+    if (buf > 2 || K == 0) {
+      if constexpr (CL) bulk::cluster_sync();
+      return;
+    }
     const int q = buf == 2 ? 0 : buf + 1;
     const bool late = buf < 2;  // P, Q: phase k stages the outputs of tile k - 1
     uint64_t* const full = buf == 0 ? full_p : (buf == 1 ? full_q : full_r);
@@ -170,13 +200,19 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
       tile_of(k, kz0, y, i);
       bulk::mbar_expect_tx(full, XTILE);
 #pragma unroll
-      for (int r0 = 0; r0 < XN; r0 += 256)
-        bulk::tma3d(tile + r0 * 128, &maps.in, 2 * kz0, y, (i * 3 + q) * XN + r0, full);
+      for (int r0 = 0; r0 < XN; r0 += 256) {
+        if constexpr (CL) bulk::tma4d(tile + r0 * 128, &maps.in, 2 * kz0, y, int(crank), (i * 3 + q) * XN + r0, full);
+        else bulk::tma3d(tile + r0 * 128, &maps.in, 2 * kz0, y, (i * 3 + q) * XN + r0, full);
+      }
     };
     auto store = [&](int k) {  // lane 0
       int kz0, y, i;
       tile_of(k, kz0, y, i);
-      if constexpr (!RT) {
+      if constexpr (CL) {
+#pragma unroll
+        for (int r0 = 0; r0 < XN; r0 += 256)
+          bulk::tma4d_store(&maps.out[0], 2 * kz0, y, int(crank), (i * 3 + q) * XN + r0, tile + r0 * 128);
+      } else if constexpr (!RT) {
 #pragma unroll
         for (int r0 = 0; r0 < XN; r0 += 256)
           bulk::tma3d_store(&maps.out[0], 2 * kz0, y, (i * 3 + q) * XN + r0, tile + r0 * 128);
@@ -215,6 +251,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     if (prof) atomicAdd(&xw_prof[2 + (buf == 2)], (unsigned long long)t_drain),
         atomicAdd(&xw_prof[4 + (buf == 2)], (unsigned long long)t_idle);
     if (lane == 0) bulk::bulk_wait_all();  // the stores are performed before the CTA retires
+    if constexpr (CL) bulk::cluster_sync();
     return;
   }
 
@@ -239,15 +276,97 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     asm volatile("mov.b64 %0, %1;\n" : "=l"(p) : "l"(tw));
     return p;
   };
+  // CL: the radix-2 step across the CTA pair (see the kernel comment).  Cross c
+  // uses phase c of ready[w] and consumed[w]; the scratch may be written again
+  // (by the next half-line exchange or the next cross) once the partner has
+  // confirmed cross c.
+  const unsigned peer = crank ^ 1u;
+  const unsigned scr_peer = CL ? bulk::cluster_map(scr, peer) : 0u;
+  const unsigned ready_peer = CL ? bulk::cluster_map(bulk::smem_addr(ready + w), peer) : 0u;
+  const unsigned consumed_peer = CL ? bulk::cluster_map(bulk::smem_addr(consumed + w), peer) : 0u;
+  unsigned crosses = 0;
+  bool lent = false;  // the partner may still be reading this warp's scratch
+  auto scratch_acquire = [&]() {
+    if constexpr (CL) {
+      if (lent) bulk::mbar_wait_cluster(consumed + w, (crosses - 1) & 1);
+      lent = false;
+    }
+  };
+  auto cross_exchange = [&](const double2(&out8)[8], double2(&in8)[8]) {
+    scratch_acquire();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned a = scr + unsigned(((j << 5) + lane) << 4);
+      asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(out8[j].x), "d"(out8[j].y) : "memory");
+    }
+    __syncwarp();
+    if (lane == 0) bulk::mbar_arrive_remote(ready_peer);
+    bulk::mbar_wait_cluster(ready + w, crosses & 1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) in8[j] = bulk::ld_cluster(scr_peer + unsigned(((j << 5) + lane) << 4));
+    __syncwarp();
+    if (lane == 0) bulk::mbar_arrive_remote(consumed_peer);
+    ++crosses;
+    lent = true;
+  };
+  // frequency held in slot s once the forward transform is complete
+  auto kx_of = [&](int s) {
+    if constexpr (CL) return kslot<XTH, XH>(t, h, (s & 7) + 8 * int(crank)) + XN * (s >> 3);
+    else return kslot<XTH, XH>(t, h, s);
+  };
   auto fwd = [&](double2(&v)[XE]) {
     if (dbg & 1) return;
-    fft256<-1>(v, t, wr0, rd0, twp());
-    pair_dit<XTH, 1>(v, t, h, twp());
+    scratch_acquire();
+    fft256<-1, TS>(v, t, wr0, rd0, twp());
+    pair_dit<XTH, 1, TS>(v, t, h, twp());
+    if constexpr (CL) {
+      // this CTA holds the half-line transform S_r[k] in kslot order; CTA 0 forms the outputs of the
+      // frequencies in its slots 0..7, CTA 1 those in its slots 8..15
+      double2 out8[8], in8[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out8[j] = crank == 0 ? v[j + 8] : v[j];
+      cross_exchange(out8, in8);
+      const double2* tp = twp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = kslot<XTH, XH>(t, h, j + 8 * int(crank));
+        const double2 e = crank == 0 ? v[j] : in8[j], o = crank == 0 ? in8[j] : v[j + 8];
+        const double2 wo = reg::tw_mul(o, __ldg(&tp[k]), -1);
+        v[j] = make_double2(e.x + wo.x, e.y + wo.y);
+        v[j + 8] = make_double2(e.x - wo.x, e.y - wo.y);
+      }
+    }
   };
   auto inv = [&](double2(&v)[XE]) {
     if (dbg & 33) return;  // (bit 5: only the inverse transforms skipped -- how far the TMA pipeline can follow)
-    pair_dif<XTH, 1>(v, t, h, twp());
-    fft256<+1>(v, t, wr0, rd0, twp());
+    if constexpr (CL) {
+      // the mirror image: sums go to the even-row half-line (CTA 0), twiddled differences to the odd one
+      double2 out8[8], in8[8];
+      const double2* tp = twp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = kslot<XTH, XH>(t, h, j + 8 * int(crank));
+        const double2 xa = v[j], xb = v[j + 8];
+        const double2 u = make_double2(xa.x + xb.x, xa.y + xb.y);
+        const double2 d = reg::tw_mul(make_double2(xa.x - xb.x, xa.y - xb.y), __ldg(&tp[k]), +1);
+        if (crank == 0) {
+          v[j] = u;
+          out8[j] = d;
+        } else {
+          v[j + 8] = d;
+          out8[j] = u;
+        }
+      }
+      cross_exchange(out8, in8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (crank == 0) v[j + 8] = in8[j];
+        else v[j] = in8[j];
+      }
+    }
+    pair_dif<XTH, 1, TS>(v, t, h, twp());
+    scratch_acquire();
+    fft256<+1, TS>(v, t, wr0, rd0, twp());
   };
   double2 X[XE], v[XE];
   double xiy_p = 0.0, xiz_p = 0.0;
@@ -298,17 +417,17 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
 #pragma unroll
     for (int m = 0; m < XE; ++m) {
-      const int kx = kslot<XTH, XH>(t, h, m);
-      const double xix = freq_of(kx, XN) * g.invL[0];
+      const int kx = kx_of(m);
+      const double xix = freq_of(kx, NLINE) * g.invL[0];
       const double norm2 = xix * xix + xiy * xiy + xiz * xiz;
-      const bool zero = norm2 == 0.0 || nyq_yz || kx == XN / 2;
+      const bool zero = norm2 == 0.0 || nyq_yz || kx == NLINE / 2;
       const double iv = zero ? 0.0 : 1.0 / norm2;
       X[m] = make_double2((v[m].x * xix + X[m].x) * iv, (v[m].y * xix + X[m].y) * iv);
     }
     // Bhat_i0 = IFFT(s xi_x) -> back into R
 #pragma unroll
     for (int m = 0; m < XE; ++m) {
-      const double f = freq_of(kslot<XTH, XH>(t, h, m), XN) * g.invL[0];
+      const double f = freq_of(kx_of(m), NLINE) * g.invL[0];
       v[m] = make_double2(X[m].x * f, X[m].y * f);
     }
     inv(v);
@@ -343,13 +462,16 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     atomicAdd(&xw_prof[6], (unsigned long long)(clock64() - t_begin));
     atomicAdd(&xw_prof[7], (unsigned long long)K);
   }
+  if constexpr (CL) bulk::cluster_sync();  // neither CTA retires while its partner may still read its scratch
 }
 
 }  // namespace
 
 bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
-  if (g.Nx != XN || g.nzh % XTW != 0) return false;
+  const bool cluster = g.Nx == 2 * XN;  // 1024-point lines: a CTA pair per tile
+  if ((g.Nx != XN && !cluster) || g.nzh % XTW != 0) return false;
   const bool routed = g.P > 1;
+  if (cluster && routed) return false;
   if (routed) {
     // The routed TMA stores are the default where they have been validated --
     // virtual ranks, all buffers on this device (bit-equal to P = 1).  Across
@@ -362,7 +484,7 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
     if (!on || g.P > kMaxRanks || g.Xl % 8 != 0 || XN % g.Xl != 0 || int(ctx->h_dst_a.size()) < g.P) return false;
   }
   XwMaps maps;
-  if (!x_tensor_map(spec, 9 * XN, g.Ny, g.nzh, XTW, true, 256, &maps.in)) return false;
+  if (!x_tensor_map(spec, 9 * g.Nx, g.Ny, g.nzh, XTW, true, 256, &maps.in, cluster)) return false;
   if (!routed) {
     maps.out[0] = maps.in;
   } else {
@@ -372,14 +494,38 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
         return false;
   }
   using Kern = void (*)(Geo, const double2*, int, const XwMaps, int);
-  const Kern kern = routed ? k_x_warp<true> : k_x_warp<false>;
+  const Kern kern = cluster ? k_x_warp<false, true> : (routed ? k_x_warp<true, false> : k_x_warp<false, false>);
   set_smem_limit(reinterpret_cast<const void*>(kern), int(XSMEM));
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = (g.nzh / XTW) * g.Ny * 3;
-  const int grid = std::min(tiles, std::max(sms, 1));
-  kern<<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, tiles, maps, dbg);
+  if (!cluster) {
+    const int grid = std::min(tiles, std::max(sms, 1));
+    kern<<<grid, XTHREADS, XSMEM, ctx->stream>>>(g, ctx->px.tw, tiles, maps, dbg);
+  } else {
+    // persistent CTA pairs: as many clusters as the device can hold at once
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(XTHREADS);
+    cfg.dynamicSmemBytes = XSMEM;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(2 * std::max(sms / 2, 1));
+    int pairs = 0;
+    if (cudaOccupancyMaxActiveClusters(&pairs, kern, &cfg) != cudaSuccess || pairs < 1) {
+      cudaGetLastError();
+      return false;
+    }
+    cfg.gridDim = dim3(2 * std::min(tiles, pairs));
+    if (cudaLaunchKernelEx(&cfg, kern, g, static_cast<const double2*>(ctx->px.tw), tiles, maps, dbg) != cudaSuccess)
+      return false;  // (the caller falls back to the staged pass; the error is cleared there)
+  }
   if (dbg & 16) {  // timing experiments only: per-tile averages to stderr
     unsigned long long h[8] = {}, z[8] = {};
     cudaStreamSynchronize(ctx->stream);

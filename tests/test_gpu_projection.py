@@ -250,3 +250,37 @@ def test_projection_256_matches_oracle_golden():
     assert np.all(np.abs(cs[1] - ref[1]) <= 1e-12 * ref[1])
     assert np.all(np.abs(cs[0] - ref[0]) <= 1e-12 * np.sqrt(ref[1] * 256 ** 3))
     assert np.linalg.norm(again - x) <= 1e-13 * np.linalg.norm(x)
+
+
+def _sample_child(pts, env, path):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np\n"
+        "from paper_1603_08893_b200 import abi, microstructure as M\n"
+        "pts = %r\n"
+        "A = M.uniform_field(pts, 9, seed=23)\n"
+        "with abi.Context(pts, 3) as ctx:\n"
+        "    out = ctx.projection(ctx.field(9, A)).download()\n"
+        "    np.save(%r, out)\n"
+        "    print(','.join(ctx.kernel_names))\n" % (root, pts, path))
+    r = subprocess.run(["timeout", "300", sys.executable, "-c", code], env=dict(os.environ, **env),
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return r.stdout.strip()
+
+
+@pytest.mark.parametrize("pts", [(1024, 8, 16), (1024, 48, 32)])
+def test_cluster_x_pass_1024_matches_default(pts, tmp_path):
+    """The opt-in cluster form of k_x_warp for 1024-point lines (FM_XW1024=1: the
+    line split over a 2-CTA cluster, the outermost radix-2 step through
+    distributed shared memory) against the default k_x_fast4: another
+    factorisation of the same transform, so equal to round-off, not bit for bit."""
+    a, b = str(tmp_path / "a.npy"), str(tmp_path / "b.npy")
+    names_def = _sample_child(pts, {}, a)
+    names_cl = _sample_child(pts, {"FM_XW1024": "1"}, b)
+    assert "k_x_fast4" in names_def and "k_x_warp" in names_cl, (names_def, names_cl)
+    x, y = np.load(a), np.load(b)
+    assert np.linalg.norm(x - y) <= 1e-14 * np.linalg.norm(x)
