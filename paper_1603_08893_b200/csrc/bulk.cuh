@@ -124,22 +124,33 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-// Arrival on an mbarrier of another CTA of the cluster: this thread's earlier
-// accesses become visible to whoever acquires that barrier's phase.
+// Arrival on an mbarrier of another CTA of the cluster, relaxed: a pure "go
+// ahead" signal (no data rides on it).  A release at cluster scope would cost a
+// MEMBAR.ALL.GPU per arrival and its acquire a CCTL.IVALL (L1 invalidation) per
+// wait -- measured: they doubled the tile time of the cluster x pass.
 __device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
-// Wait on a local mbarrier that CTAs of the cluster arrive on.
+// Wait (relaxed) on a local mbarrier that a CTA of the cluster arrives on.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "FM_WAITC_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra FM_WAITC_%=;\n"
       "}\n" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+}
+// 16-byte store into another CTA's shared memory that completes on that CTA's
+// mbarrier (complete_tx): the receiver's ordinary wait on the barrier makes the
+// data visible, no fence on either side.
+__device__ __forceinline__ void st_async_remote(unsigned cluster_addr, double2 v, unsigned cluster_bar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
+                   cluster_addr),
+               "d"(v.x), "d"(v.y), "r"(cluster_bar)
+               : "memory");
 }
 __device__ __forceinline__ double2 ld_cluster(unsigned cluster_addr) {
   double2 v;

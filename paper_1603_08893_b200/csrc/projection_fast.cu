@@ -1521,10 +1521,11 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
     }
   }
   if constexpr (N == 1024) {
-    // FM_XW1024=1: the cluster form of k_x_warp (projection_xw.cu); default k_x_fast4 on 4-column tiles
+    // the cluster form of k_x_warp (projection_xw.cu): 40.4 vs 58.6 ms at 1024^3; FM_XW1024=0: k_x_fast4 on
+    // 4-column tiles (also the routed P > 1 pass)
     static const bool xw1024 = [] {
       const char* e = getenv("FM_XW1024");
-      return e && atoi(e) != 0;
+      return !e || atoi(e) != 0;
     }();
     if (zc && xw1024 && g.P == 1) {
       static const int xdbg1024 = [] {

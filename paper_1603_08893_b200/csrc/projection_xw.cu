@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
   uint64_t* const full_r = bars + 2;     // A_0
   uint64_t* const staged_pq = bars + 3;  // all 8 warps are done with P and Q (count 8)
   uint64_t* const staged_r = bars + 4;   // all 8 warps have written output 0 into R
-  uint64_t* const ready = bars + 8;      // CL, per warp: the partner warp's eight values are in its scratch
-  uint64_t* const consumed = bars + 16;  // CL, per warp: the partner warp has read this warp's scratch
+  uint64_t* const ready = bars + 8;      // CL, per warp: the partner warp has pushed its eight values per lane into this warp's scratch
+  uint64_t* const consumed = bars + 16;  // CL, per warp: the partner warp's scratch is free for this warp's push
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     bulk::mbar_init(full_p, 1);
@@ -276,48 +276,57 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     asm volatile("mov.b64 %0, %1;\n" : "=l"(p) : "l"(tw));
     return p;
   };
-  // CL: the radix-2 step across the CTA pair (see the kernel comment).  Cross c
-  // uses phase c of ready[w] and consumed[w]; the scratch may be written again
-  // (by the next half-line exchange or the next cross) once the partner has
-  // confirmed cross c.
+  // CL: the radix-2 step across the CTA pair (see the kernel comment).  Each warp
+  // PUSHES the eight values per lane its partner needs into the partner's
+  // scratch with st.async, which completes on the partner's ready[w] (armed with
+  // the byte count); the partner then reads its own shared memory after an
+  // ordinary mbarrier wait -- no fence on either side.  free[w] is the reverse
+  // "go ahead": it is signalled (relaxed, no data rides on it) after a half-line
+  // exchange that is followed by a cross, and after a cross that is followed
+  // directly by another cross (fwd, fwd | inv, inv: after F1, after F2, after the
+  // read of cross 2, after F3) -- once per cross, so both barriers advance one
+  // phase per cross.  (First form: the partner's values pulled with
+  // ld.shared::cluster between release / acquire handshakes at cluster scope --
+  // every release a MEMBAR.ALL.GPU, every acquire an L1 invalidation that threw
+  // the twiddles out: 42 900 cycles per tile against 20 100 at 512 points.)
   const unsigned peer = crank ^ 1u;
   const unsigned scr_peer = CL ? bulk::cluster_map(scr, peer) : 0u;
   const unsigned ready_peer = CL ? bulk::cluster_map(bulk::smem_addr(ready + w), peer) : 0u;
-  const unsigned consumed_peer = CL ? bulk::cluster_map(bulk::smem_addr(consumed + w), peer) : 0u;
+  const unsigned free_peer = CL ? bulk::cluster_map(bulk::smem_addr(consumed + w), peer) : 0u;
+  uint64_t* const free_mine = consumed + w;  // the partner arrives here: ITS scratch is free for my push
   unsigned crosses = 0;
-  bool lent = false;  // the partner may still be reading this warp's scratch
-  auto scratch_acquire = [&]() {
+  auto signal_free = [&]() {  // after this warp's last use of its scratch before the partner's next push
     if constexpr (CL) {
-      if (lent) bulk::mbar_wait_cluster(consumed + w, (crosses - 1) & 1);
-      lent = false;
+      __syncwarp();
+      if (lane == 0) {
+        bulk::mbar_expect_tx(ready + w, 32 * 8 * 16);  // arm the inbox barrier before the partner may push
+        bulk::mbar_arrive_remote(free_peer);
+      }
     }
   };
   auto cross_exchange = [&](const double2(&out8)[8], double2(&in8)[8]) {
-    scratch_acquire();
+    bulk::mbar_wait_cluster(free_mine, crosses & 1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      bulk::st_async_remote(scr_peer + unsigned(((j << 5) + lane) << 4), out8[j], ready_peer);
+    bulk::mbar_wait(ready + w, crosses & 1);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const unsigned a = scr + unsigned(((j << 5) + lane) << 4);
-      asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(out8[j].x), "d"(out8[j].y) : "memory");
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(in8[j].x), "=d"(in8[j].y) : "r"(a) : "memory");
     }
-    __syncwarp();
-    if (lane == 0) bulk::mbar_arrive_remote(ready_peer);
-    bulk::mbar_wait_cluster(ready + w, crosses & 1);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) in8[j] = bulk::ld_cluster(scr_peer + unsigned(((j << 5) + lane) << 4));
-    __syncwarp();
-    if (lane == 0) bulk::mbar_arrive_remote(consumed_peer);
     ++crosses;
-    lent = true;
   };
   // frequency held in slot s once the forward transform is complete
   auto kx_of = [&](int s) {
     if constexpr (CL) return kslot<XTH, XH>(t, h, (s & 7) + 8 * int(crank)) + XN * (s >> 3);
     else return kslot<XTH, XH>(t, h, s);
   };
-  auto fwd = [&](double2(&v)[XE]) {
+  // then_cross: the next transform starts with its cross step (an inverse follows)
+  auto fwd = [&](double2(&v)[XE], bool then_cross) {
     if (dbg & 1) return;
-    scratch_acquire();
     fft256<-1, TS>(v, t, wr0, rd0, twp());
+    signal_free();
     pair_dit<XTH, 1, TS>(v, t, h, twp());
     if constexpr (CL) {
       // this CTA holds the half-line transform S_r[k] in kslot order; CTA 0 forms the outputs of the
@@ -335,9 +344,11 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
         v[j] = make_double2(e.x + wo.x, e.y + wo.y);
         v[j + 8] = make_double2(e.x - wo.x, e.y - wo.y);
       }
+      // the inbox has been read and no half-line exchange comes before the next cross
+      if (then_cross && !(dbg & 32)) signal_free();
     }
   };
-  auto inv = [&](double2(&v)[XE]) {
+  auto inv = [&](double2(&v)[XE], bool then_cross) {
     if (dbg & 33) return;  // (bit 5: only the inverse transforms skipped -- how far the TMA pipeline can follow)
     if constexpr (CL) {
       // the mirror image: sums go to the even-row half-line (CTA 0), twiddled differences to the odd one
@@ -365,8 +376,8 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
       }
     }
     pair_dif<XTH, 1, TS>(v, t, h, twp());
-    scratch_acquire();
     fft256<+1, TS>(v, t, wr0, rd0, twp());
+    if (then_cross) signal_free();
   };
   double2 X[XE], v[XE];
   double xiy_p = 0.0, xiz_p = 0.0;
@@ -404,7 +415,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     bulk::fence_async_smem();
     __syncwarp();
     if (lane == 0) bulk::mbar_arrive(staged_pq);
-    fwd(X);
+    fwd(X, false);
     // forward transform of A_0
     {
       const long long c0 = prof ? clock64() : 0;
@@ -413,7 +424,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     }
 #pragma unroll
     for (int m = 0; m < XE; ++m) v[m] = *at(R, m);
-    fwd(v);
+    fwd(v, true);
     // s = (xi_x FFT(A_0) + FFT(B)) / |xi|^2, zero at xi = 0 and on Nyquist planes
 #pragma unroll
     for (int m = 0; m < XE; ++m) {
@@ -430,7 +441,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
       const double f = freq_of(kx_of(m), NLINE) * g.invL[0];
       v[m] = make_double2(X[m].x * f, X[m].y * f);
     }
-    inv(v);
+    inv(v, true);
 #pragma unroll
     for (int m = 0; m < XE; ++m) *at(R, m) = v[m];
     bulk::fence_async_smem();
@@ -440,7 +451,7 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     // start of the next tile (or below, after the last one)
 #pragma unroll
     for (int m = 0; m < XE; ++m) v[m] = make_double2(X[m].x * 1.0, X[m].y * 1.0);
-    inv(v);
+    inv(v, false);
     xiy_p = xiy;
     xiz_p = xiz;
   }

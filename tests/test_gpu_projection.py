@@ -274,13 +274,13 @@ def _sample_child(pts, env, path):
 
 @pytest.mark.parametrize("pts", [(1024, 8, 16), (1024, 48, 32)])
 def test_cluster_x_pass_1024_matches_default(pts, tmp_path):
-    """The opt-in cluster form of k_x_warp for 1024-point lines (FM_XW1024=1: the
-    line split over a 2-CTA cluster, the outermost radix-2 step through
-    distributed shared memory) against the default k_x_fast4: another
-    factorisation of the same transform, so equal to round-off, not bit for bit."""
+    """The cluster form of k_x_warp for 1024-point lines (the line split over a
+    2-CTA cluster, the outermost radix-2 step through distributed shared
+    memory) against k_x_fast4 (FM_XW1024=0): another factorisation of the same
+    transform, so equal to round-off, not bit for bit."""
     a, b = str(tmp_path / "a.npy"), str(tmp_path / "b.npy")
-    names_def = _sample_child(pts, {}, a)
-    names_cl = _sample_child(pts, {"FM_XW1024": "1"}, b)
+    names_def = _sample_child(pts, {"FM_XW1024": "0"}, a)
+    names_cl = _sample_child(pts, {}, b)
     assert "k_x_fast4" in names_def and "k_x_warp" in names_cl, (names_def, names_cl)
     x, y = np.load(a), np.load(b)
     assert np.linalg.norm(x - y) <= 1e-14 * np.linalg.norm(x)
