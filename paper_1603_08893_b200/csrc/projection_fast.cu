@@ -1527,7 +1527,7 @@ bool x_launch(fm_ctx* ctx, const Geo& g, double2* spec, int* st) {
       const char* e = getenv("FM_XW1024");
       return !e || atoi(e) != 0;
     }();
-    if (zc && xw1024 && g.P == 1) {
+    if (zc && xw1024) {  // (P > 1: routed TMA stores, where xw_launch allows them)
       static const int xdbg1024 = [] {
         const char* e = getenv("FM_X_DBG");
         return e ? atoi(e) : 0;

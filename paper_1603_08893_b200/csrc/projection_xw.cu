@@ -137,7 +137,6 @@ struct XwMaps {
 template <bool RT, bool CL>
 __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, int tiles,
                                                         const __grid_constant__ XwMaps maps, int dbg) {
-  static_assert(!(RT && CL), "the cluster form is single-device only");
   constexpr int TS = CL ? 2 : 1;        // table stride: tw is W_1024 for the cluster form
   constexpr int NLINE = CL ? 2 * XN : XN;  // points of a whole x-line
   extern __shared__ unsigned char smraw[];
@@ -208,7 +207,15 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
     auto store = [&](int k) {  // lane 0
       int kz0, y, i;
       tile_of(k, kz0, y, i);
-      if constexpr (CL) {
+      if constexpr (CL && RT) {
+        // this CTA's rows j (x = 2 j + parity) belong to rank s = j / (Xl / 2): boxes of at most Xl / 2 rows
+        const int xh = g.Xl >> 1, box = xh < 256 ? xh : 256;
+        for (int r0 = 0; r0 < XN; r0 += box) {
+          const int s = r0 / xh;
+          bulk::tma4d_store(&maps.out[s], 2 * kz0, g.y0 + y, int(crank), (i * 3 + q) * xh + (r0 - s * xh),
+                            tile + r0 * 128);
+        }
+      } else if constexpr (CL) {
 #pragma unroll
         for (int r0 = 0; r0 < XN; r0 += 256)
           bulk::tma4d_store(&maps.out[0], 2 * kz0, y, int(crank), (i * 3 + q) * XN + r0, tile + r0 * 128);
@@ -482,7 +489,6 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
   const bool cluster = g.Nx == 2 * XN;  // 1024-point lines: a CTA pair per tile
   if ((g.Nx != XN && !cluster) || g.nzh % XTW != 0) return false;
   const bool routed = g.P > 1;
-  if (cluster && routed) return false;
   if (routed) {
     // The routed TMA stores are the default where they have been validated --
     // virtual ranks, all buffers on this device (bit-equal to P = 1).  Across
@@ -492,20 +498,26 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
     // path off everywhere.
     const char* e = getenv("FM_XW_ROUTED");
     const bool on = e ? atoi(e) != 0 : ctx->virt;
-    if (!on || g.P > kMaxRanks || g.Xl % 8 != 0 || XN % g.Xl != 0 || int(ctx->h_dst_a.size()) < g.P) return false;
+    const int rows_per_rank = cluster ? g.Xl / 2 : g.Xl;  // of one CTA's XN rows
+    if (!on || g.P > kMaxRanks || g.Xl % 16 != 0 || rows_per_rank % 8 != 0 || XN % rows_per_rank != 0 ||
+        int(ctx->h_dst_a.size()) < g.P)
+      return false;
   }
   XwMaps maps;
   if (!x_tensor_map(spec, 9 * g.Nx, g.Ny, g.nzh, XTW, true, 256, &maps.in, cluster)) return false;
   if (!routed) {
     maps.out[0] = maps.in;
   } else {
-    const int box = g.Xl < 256 ? g.Xl : 256;
-    for (int s = 0; s < g.P; ++s)  // A_s viewed as [9 Xl][Ny global][2 nzh]
-      if (!ctx->h_dst_a[s] || !x_tensor_map(ctx->h_dst_a[s], 9 * g.Xl, g.Nyg, g.nzh, XTW, true, box, &maps.out[s]))
+    const int rows_per_rank = cluster ? g.Xl / 2 : g.Xl;
+    const int box = rows_per_rank < 256 ? rows_per_rank : 256;
+    for (int s = 0; s < g.P; ++s)  // A_s viewed as [9 Xl][Ny global][2 nzh] (cluster form: rows split by parity)
+      if (!ctx->h_dst_a[s] ||
+          !x_tensor_map(ctx->h_dst_a[s], 9 * g.Xl, g.Nyg, g.nzh, XTW, true, box, &maps.out[s], cluster))
         return false;
   }
   using Kern = void (*)(Geo, const double2*, int, const XwMaps, int);
-  const Kern kern = cluster ? k_x_warp<false, true> : (routed ? k_x_warp<true, false> : k_x_warp<false, false>);
+  const Kern kern = cluster ? (routed ? k_x_warp<true, true> : k_x_warp<false, true>)
+                            : (routed ? k_x_warp<true, false> : k_x_warp<false, false>);
   set_smem_limit(reinterpret_cast<const void*>(kern), int(XSMEM));
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
                                    # long routed x lines (512: direct lane-pair pass, 1024: 4-column tiles) and y lines
                                    # (P = 1 at 512: the warp-per-line TMA pass k_x_warp, one tile per CTA and,
                                    # at 64 x 32, two to three tiles per CTA, against the routed k_x_stream)
-                                   ((512, 32, 16), 4), ((512, 64, 32), 2), ((1024, 16, 32), 2), ((32, 512, 16), 2),
+                                   ((512, 32, 16), 4), ((512, 64, 32), 2), ((1024, 16, 32), 2), ((1024, 32, 32), 8), ((32, 512, 16), 2),
                                    ((16, 1024, 32), 4)])
 def test_virtual_ranks_bitwise_equal(pts, P):
     A = M.uniform_field(pts, 9, seed=3)
@@ -33,12 +33,6 @@ def test_virtual_ranks_bitwise_equal(pts, P):
         assert ctx.ranks() == (P, 0, True)
         gp = ctx.projection(fa).download()
         mp = ctx.projected_tangent(fk, fa).download()
-    if pts[0] == 1024:
-        # P = 1 runs the 2-CTA-cluster x pass (1024 = 2 x 512 across the CTA pair), the routed pass the
-        # 16 x 16 x 4 k_x_fast4: two factorisations of the same transform, equal to round-off
-        assert np.linalg.norm(g1 - gp) <= 1e-14 * np.linalg.norm(g1)
-        assert np.linalg.norm(m1 - mp) <= 1e-14 * np.linalg.norm(m1)
-        return
     assert np.array_equal(g1, gp)
     assert np.array_equal(m1, mp)
 
