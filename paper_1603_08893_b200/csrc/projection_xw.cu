@@ -42,6 +42,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "bulk.cuh"
 #include "fft_pair.cuh"
@@ -540,11 +543,23 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(2 * std::max(sms / 2, 1));
+    // (co-resident CTA pairs: queried once per device and kernel, the query is not cheap)
+    static std::mutex mx;
+    static std::map<std::pair<int, const void*>, int> cache;
     int pairs = 0;
-    if (cudaOccupancyMaxActiveClusters(&pairs, kern, &cfg) != cudaSuccess || pairs < 1) {
-      cudaGetLastError();
-      return false;
+    {
+      std::lock_guard<std::mutex> lk(mx);
+      const auto key = std::make_pair(dev, reinterpret_cast<const void*>(kern));
+      auto it = cache.find(key);
+      if (it == cache.end()) {
+        int q = 0;
+        if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) != cudaSuccess) q = 0;
+        cudaGetLastError();
+        it = cache.emplace(key, q).first;
+      }
+      pairs = it->second;
     }
+    if (pairs < 1) return false;
     cfg.gridDim = dim3(2 * std::min(tiles, pairs));
     if (cudaLaunchKernelEx(&cfg, kern, g, static_cast<const double2*>(ctx->px.tw), tiles, maps, dbg) != cudaSuccess)
       return false;  // (the caller falls back to the staged pass; the error is cleared there)
