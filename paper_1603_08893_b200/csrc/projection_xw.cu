@@ -1,5 +1,6 @@
-// 512-point x pass (projection.cpp:137-155: x FFT, ghat, inverse x FFT), one
-// warp per x-line, all HBM traffic by TMA in both directions.
+// x pass for long lines (projection.cpp:137-155: x FFT, ghat, inverse x FFT):
+// 512 points with one warp per x-line, 1024 points with the line split over a
+// 2-CTA cluster; all HBM traffic by TMA in both directions.
 //
 // Why (profiles/r2_x512_dbg.md): the streamed pass k_x_stream (one CTA per SM,
 // 8 warps walking its tiles in lock-step) took 4.5 ms at 512^3 whatever was
@@ -131,12 +132,9 @@ struct XwMaps {
 // rows of parity r (a 4-D tensor map makes them a box), runs the same 512-point
 // machinery on its half-line, and the outermost radix-2 step X[k] = E[k] +
 // W^k O[k], X[k + 512] = E[k] - W^k O[k] crosses the CTA pair through
-// distributed shared memory: each warp leaves the eight values per lane its
-// partner needs in its own scratch, signals the partner warp's mbarrier
-// (release at cluster scope) and reads the partner's eight with
-// ld.shared::cluster; a second mbarrier tells it when its scratch may be
-// written again.  The warps stay independent of everything but their partner
-// warp in the other CTA.
+// distributed shared memory, warp to partner warp (cross_exchange below), so
+// the warps stay independent of everything but their partner in the other CTA.
+// 1024^3: 40.4 ms against 58.6 ms for k_x_fast4<1024> (profiles/r2_x1024_cluster.md).
 template <bool RT, bool CL>
 __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, int tiles,
                                                         const __grid_constant__ XwMaps maps, int dbg) {
@@ -153,8 +151,8 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
   uint64_t* const full_r = bars + 2;     // A_0
   uint64_t* const staged_pq = bars + 3;  // all 8 warps are done with P and Q (count 8)
   uint64_t* const staged_r = bars + 4;   // all 8 warps have written output 0 into R
-  uint64_t* const ready = bars + 8;      // CL, per warp: the partner warp has pushed its eight values per lane into this warp's scratch
-  uint64_t* const consumed = bars + 16;  // CL, per warp: the partner warp's scratch is free for this warp's push
+  uint64_t* const ready = bars + 8;      // CL, per warp: the partner's pushed values have landed in this warp's scratch
+  uint64_t* const consumed = bars + 16;  // CL, per warp: the partner's scratch is free for this warp's push
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     bulk::mbar_init(full_p, 1);
