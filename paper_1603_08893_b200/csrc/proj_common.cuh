@@ -334,6 +334,10 @@ bool zi_fast(fm_ctx* ctx, const Geo& g, const double2* spec, double* out, double
 // split2: rows viewed as [rows / 2][2]: the even and the odd rows are separate boxes (4-D map).
 bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz128, int box_rows, void* out_map,
                   bool split2 = false);
+bool tensor_map_encode(const void* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                       bool swz128, void* out_map);
+// 1024-point y pass in place, the line split over a 2-CTA cluster (projection_xw.cu).
+bool yw_launch(fm_ctx* ctx, const Geo& g, int sign, double2* spec);
 // 512-point x pass, one warp per line, TMA in and out (projection_xw.cu).
 bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg);
 

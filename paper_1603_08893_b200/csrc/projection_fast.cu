@@ -1308,6 +1308,19 @@ bool y_launch(fm_ctx* ctx, const Geo& g, int sign, const double2* in, double2* o
       const char* e = getenv("FM_Y1024_TW");
       return e ? atoi(e) : 4;
     }();
+    // the cluster form (k_y_warp, projection_xw.cu), in place on one device: 31.3 / 32.0 ms against 34.9 / 35.0 ms
+    // at 1024^3; FM_YW1024=0 restores k_y_fast (which the routed P > 1 passes use)
+    static const bool yw = [] {
+      const char* e = getenv("FM_YW1024");
+      return !e || atoi(e) != 0;
+    }();
+    if (yw && N == 1024 && g.P == 1 && in == out) {
+      if (yw_launch(ctx, g, sign, out)) {
+        *st = launched(ctx, "k_y_warp");
+        return true;
+      }
+      cudaGetLastError();
+    }
     if (tw == 8 && ctx->nzh % 8 == 0) return y_launch_tw<N, 8>(ctx, g, sign, in, out, st);
     return y_launch_tw<N, 4>(ctx, g, sign, in, out, st);
   } else {
@@ -1432,6 +1445,33 @@ bool x_tensor_map(const void* base, int rows, int Ny, int nzh, int TW, bool swz1
   cache.push_back(e);
   *out = e.map;
   return true;
+}
+// Uncached encode of a tiled fp64 tensor map of any rank (dims innermost first,
+// strides in bytes for dims 1.., box in elements), 128-byte swizzle optional.
+bool tensor_map_encode(const void* base, int rank, const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                       bool swz128, void* out_map) {
+  static EncodeTiledFn enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  if (!enc || rank < 1 || rank > 5) return false;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i > 0) st[i - 1] = strides[i - 1];
+  }
+  return enc(static_cast<CUtensorMap*>(out_map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank),
+             const_cast<void*>(base), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 namespace {
 

@@ -104,6 +104,148 @@ __device__ __forceinline__ void fft256(double2 (&v)[XE], int t, unsigned wr0, un
   reg::Dft<16, SIGN>::run(v);
 }
 
+// The transforms of one warp's line -- a 512-point line, or (CL) the half-line
+// of a 1024-point line whose other half lives in the partner CTA of a 2-CTA
+// cluster -- and, CL, the link to the partner warp.
+//
+// CL: the outermost radix-2 step crosses the CTA pair (X[k] = E[k] + W^k O[k],
+// X[k + 512] = E[k] - W^k O[k]).  Each warp PUSHES the eight values per lane its
+// partner needs into the partner's scratch with st.async, which completes on the
+// partner's ready barrier (armed with the byte count); the partner then reads
+// its own shared memory after an ordinary mbarrier wait -- no fence on either
+// side.  The free barrier is the reverse "go ahead": signalled (relaxed, no data
+// rides on it) after a half-line exchange that is followed by a cross, and after
+// a cross that is followed directly by another cross -- once per cross, so both
+// barriers advance one phase per cross.  (First form: the partner's values
+// pulled with ld.shared::cluster between release / acquire handshakes at cluster
+// scope -- every release a MEMBAR.ALL.GPU, every acquire an L1 invalidation that
+// threw the twiddles out: 42 900 cycles per x-pass tile against 26 800.)
+template <bool CL>
+struct WarpLine {
+  static constexpr int TS = CL ? 2 : 1;  // table stride: tw is W_1024 for the cluster form
+  int lane, t, h;
+  unsigned crank;                // CL: parity of this CTA's rows
+  unsigned scr, wr0, rd0;        // this warp's exchange scratch (shared-space addresses)
+  unsigned scr_peer, ready_peer, free_peer;
+  uint64_t* ready_mine;          // the partner's pushed values have landed in this warp's scratch
+  uint64_t* free_mine;           // the partner's scratch is free for this warp's push
+  unsigned crosses;
+  const double2* tw;
+
+  __device__ __forceinline__ void init(int lane_, int w, unsigned crank_, unsigned char* scr0, uint64_t* ready,
+                                       uint64_t* freeb, const double2* tw_) {
+    lane = lane_;
+    h = lane & 1;
+    t = lane >> 1;
+    crank = crank_;
+    scr = bulk::smem_addr(scr0) + w * XSCR;
+    wr0 = scr + (t << 8) + (h << 3) + ((t & 7) << 4);  // exchange addresses of slot 0 (see exchange())
+    rd0 = scr + (t << 4) + (h << 3);
+    ready_mine = ready + w;
+    free_mine = freeb + w;
+    scr_peer = ready_peer = free_peer = 0u;
+    if constexpr (CL) {
+      const unsigned peer = crank ^ 1u;
+      scr_peer = bulk::cluster_map(scr, peer);
+      ready_peer = bulk::cluster_map(bulk::smem_addr(ready_mine), peer);
+      free_peer = bulk::cluster_map(bulk::smem_addr(free_mine), peer);
+    }
+    crosses = 0;
+    tw = tw_;
+  }
+  // The twiddles only depend on the lane: through an opaque copy of the table
+  // pointer each transform reloads them instead of keeping ~90 registers live
+  // across the tile loop.
+  __device__ __forceinline__ const double2* twp() const {
+    const double2* p;
+    asm volatile("mov.b64 %0, %1;\n" : "=l"(p) : "l"(tw));
+    return p;
+  }
+  // after this warp's last use of its scratch before the partner's next push
+  __device__ __forceinline__ void signal_free() {
+    if constexpr (CL) {
+      __syncwarp();
+      if (lane == 0) {
+        bulk::mbar_expect_tx(ready_mine, 32 * 8 * 16);  // arm the inbox barrier before the partner may push
+        bulk::mbar_arrive_remote(free_peer);
+      }
+    }
+  }
+  __device__ __forceinline__ void cross_exchange(const double2 (&out8)[8], double2 (&in8)[8]) {
+    bulk::mbar_wait_cluster(free_mine, crosses & 1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      bulk::st_async_remote(scr_peer + unsigned(((j << 5) + lane) << 4), out8[j], ready_peer);
+    bulk::mbar_wait(ready_mine, crosses & 1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned a = scr + unsigned(((j << 5) + lane) << 4);
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(in8[j].x), "=d"(in8[j].y) : "r"(a) : "memory");
+    }
+    ++crosses;
+  }
+  // frequency held in slot s once the forward transform is complete
+  __device__ __forceinline__ int kx_of(int s) const {
+    if constexpr (CL) return kslot<XTH, XH>(t, h, (s & 7) + 8 * int(crank)) + XN * (s >> 3);
+    else return kslot<XTH, XH>(t, h, s);
+  }
+  // then_cross: the next transform starts with its cross step (an inverse follows)
+  __device__ __forceinline__ void fwd(double2 (&v)[XE], bool then_cross) {
+    fft256<-1, TS>(v, t, wr0, rd0, twp());
+    signal_free();
+    pair_dit<XTH, 1, TS>(v, t, h, twp());
+    if constexpr (CL) {
+      // this CTA holds the half-line transform S_r[k] in kslot order; CTA 0 forms the outputs of the
+      // frequencies in its slots 0..7, CTA 1 those in its slots 8..15
+      double2 out8[8], in8[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out8[j] = crank == 0 ? v[j + 8] : v[j];
+      cross_exchange(out8, in8);
+      const double2* tp = twp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = kslot<XTH, XH>(t, h, j + 8 * int(crank));
+        const double2 e = crank == 0 ? v[j] : in8[j], o = crank == 0 ? in8[j] : v[j + 8];
+        const double2 wo = reg::tw_mul(o, __ldg(&tp[k]), -1);
+        v[j] = make_double2(e.x + wo.x, e.y + wo.y);
+        v[j + 8] = make_double2(e.x - wo.x, e.y - wo.y);
+      }
+      // the inbox has been read and no half-line exchange comes before the next cross
+      if (then_cross) signal_free();
+    }
+  }
+  __device__ __forceinline__ void inv(double2 (&v)[XE], bool then_cross) {
+    if constexpr (CL) {
+      // the mirror image: sums go to the even-row half-line (CTA 0), twiddled differences to the odd one
+      double2 out8[8], in8[8];
+      const double2* tp = twp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = kslot<XTH, XH>(t, h, j + 8 * int(crank));
+        const double2 xa = v[j], xb = v[j + 8];
+        const double2 u = make_double2(xa.x + xb.x, xa.y + xb.y);
+        const double2 d = reg::tw_mul(make_double2(xa.x - xb.x, xa.y - xb.y), __ldg(&tp[k]), +1);
+        if (crank == 0) {
+          v[j] = u;
+          out8[j] = d;
+        } else {
+          v[j + 8] = d;
+          out8[j] = u;
+        }
+      }
+      cross_exchange(out8, in8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (crank == 0) v[j + 8] = in8[j];
+        else v[j] = in8[j];
+      }
+    }
+    pair_dif<XTH, 1, TS>(v, t, h, twp());
+    fft256<+1, TS>(v, t, wr0, rd0, twp());
+    if (then_cross) signal_free();
+  }
+};
+
 // FM_X_DBG bit 4: cycle counts summed over the CTAs -- [0], [1] transform warp
 // 0 waiting for A_1/A_2 and A_0; [2], [3] store drain (issue -> shared memory
 // read) of P/Q and R; [4], [5] the copy threads waiting for staged buffers;
@@ -138,7 +280,6 @@ struct XwMaps {
 template <bool RT, bool CL>
 __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __restrict__ tw, int tiles,
                                                         const __grid_constant__ XwMaps maps, int dbg) {
-  constexpr int TS = CL ? 2 : 1;        // table stride: tw is W_1024 for the cluster form
   constexpr int NLINE = CL ? 2 * XN : XN;  // points of a whole x-line
   extern __shared__ unsigned char smraw[];
   // 1024-byte alignment: the swizzle pattern is a function of the address
@@ -272,120 +413,16 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
   unsigned char* const Q = sm0 + XTILE + col;
   unsigned char* const R = sm0 + 2 * XTILE + col;
   auto at = [](unsigned char* b, int m) { return reinterpret_cast<double2*>(b + (m << 12)); };
-  // exchange addresses of slot 0 (see exchange())
-  const unsigned scr = bulk::smem_addr(scr0) + w * XSCR;
-  const unsigned wr0 = scr + (t << 8) + (h << 3) + ((t & 7) << 4);
-  const unsigned rd0 = scr + (t << 4) + (h << 3);
-  // The twiddles only depend on the lane: through an opaque copy of the table
-  // pointer each transform reloads them instead of keeping ~90 registers live
-  // across the tile loop.
-  auto twp = [&]() {
-    const double2* p;
-    asm volatile("mov.b64 %0, %1;\n" : "=l"(p) : "l"(tw));
-    return p;
-  };
-  // CL: the radix-2 step across the CTA pair (see the kernel comment).  Each warp
-  // PUSHES the eight values per lane its partner needs into the partner's
-  // scratch with st.async, which completes on the partner's ready[w] (armed with
-  // the byte count); the partner then reads its own shared memory after an
-  // ordinary mbarrier wait -- no fence on either side.  free[w] is the reverse
-  // "go ahead": it is signalled (relaxed, no data rides on it) after a half-line
-  // exchange that is followed by a cross, and after a cross that is followed
-  // directly by another cross (fwd, fwd | inv, inv: after F1, after F2, after the
-  // read of cross 2, after F3) -- once per cross, so both barriers advance one
-  // phase per cross.  (First form: the partner's values pulled with
-  // ld.shared::cluster between release / acquire handshakes at cluster scope --
-  // every release a MEMBAR.ALL.GPU, every acquire an L1 invalidation that threw
-  // the twiddles out: 42 900 cycles per tile against 20 100 at 512 points.)
-  const unsigned peer = crank ^ 1u;
-  const unsigned scr_peer = CL ? bulk::cluster_map(scr, peer) : 0u;
-  const unsigned ready_peer = CL ? bulk::cluster_map(bulk::smem_addr(ready + w), peer) : 0u;
-  const unsigned free_peer = CL ? bulk::cluster_map(bulk::smem_addr(consumed + w), peer) : 0u;
-  uint64_t* const free_mine = consumed + w;  // the partner arrives here: ITS scratch is free for my push
-  unsigned crosses = 0;
-  auto signal_free = [&]() {  // after this warp's last use of its scratch before the partner's next push
-    if constexpr (CL) {
-      __syncwarp();
-      if (lane == 0) {
-        bulk::mbar_expect_tx(ready + w, 32 * 8 * 16);  // arm the inbox barrier before the partner may push
-        bulk::mbar_arrive_remote(free_peer);
-      }
-    }
-  };
-  auto cross_exchange = [&](const double2(&out8)[8], double2(&in8)[8]) {
-    bulk::mbar_wait_cluster(free_mine, crosses & 1);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      bulk::st_async_remote(scr_peer + unsigned(((j << 5) + lane) << 4), out8[j], ready_peer);
-    bulk::mbar_wait(ready + w, crosses & 1);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const unsigned a = scr + unsigned(((j << 5) + lane) << 4);
-      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(in8[j].x), "=d"(in8[j].y) : "r"(a) : "memory");
-    }
-    ++crosses;
-  };
-  // frequency held in slot s once the forward transform is complete
-  auto kx_of = [&](int s) {
-    if constexpr (CL) return kslot<XTH, XH>(t, h, (s & 7) + 8 * int(crank)) + XN * (s >> 3);
-    else return kslot<XTH, XH>(t, h, s);
-  };
-  // then_cross: the next transform starts with its cross step (an inverse follows)
+  WarpLine<CL> L;
+  L.init(lane, w, crank, scr0, ready, consumed, tw);
+  auto kx_of = [&](int s) { return L.kx_of(s); };
   auto fwd = [&](double2(&v)[XE], bool then_cross) {
     if (dbg & 1) return;
-    fft256<-1, TS>(v, t, wr0, rd0, twp());
-    signal_free();
-    pair_dit<XTH, 1, TS>(v, t, h, twp());
-    if constexpr (CL) {
-      // this CTA holds the half-line transform S_r[k] in kslot order; CTA 0 forms the outputs of the
-      // frequencies in its slots 0..7, CTA 1 those in its slots 8..15
-      double2 out8[8], in8[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) out8[j] = crank == 0 ? v[j + 8] : v[j];
-      cross_exchange(out8, in8);
-      const double2* tp = twp();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int k = kslot<XTH, XH>(t, h, j + 8 * int(crank));
-        const double2 e = crank == 0 ? v[j] : in8[j], o = crank == 0 ? in8[j] : v[j + 8];
-        const double2 wo = reg::tw_mul(o, __ldg(&tp[k]), -1);
-        v[j] = make_double2(e.x + wo.x, e.y + wo.y);
-        v[j + 8] = make_double2(e.x - wo.x, e.y - wo.y);
-      }
-      // the inbox has been read and no half-line exchange comes before the next cross
-      if (then_cross && !(dbg & 32)) signal_free();
-    }
+    L.fwd(v, then_cross && !(dbg & 32));
   };
   auto inv = [&](double2(&v)[XE], bool then_cross) {
     if (dbg & 33) return;  // (bit 5: only the inverse transforms skipped -- how far the TMA pipeline can follow)
-    if constexpr (CL) {
-      // the mirror image: sums go to the even-row half-line (CTA 0), twiddled differences to the odd one
-      double2 out8[8], in8[8];
-      const double2* tp = twp();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int k = kslot<XTH, XH>(t, h, j + 8 * int(crank));
-        const double2 xa = v[j], xb = v[j + 8];
-        const double2 u = make_double2(xa.x + xb.x, xa.y + xb.y);
-        const double2 d = reg::tw_mul(make_double2(xa.x - xb.x, xa.y - xb.y), __ldg(&tp[k]), +1);
-        if (crank == 0) {
-          v[j] = u;
-          out8[j] = d;
-        } else {
-          v[j + 8] = d;
-          out8[j] = u;
-        }
-      }
-      cross_exchange(out8, in8);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (crank == 0) v[j + 8] = in8[j];
-        else v[j] = in8[j];
-      }
-    }
-    pair_dif<XTH, 1, TS>(v, t, h, twp());
-    fft256<+1, TS>(v, t, wr0, rd0, twp());
-    if (then_cross) signal_free();
+    L.inv(v, then_cross);
   };
   double2 X[XE], v[XE];
   double xiy_p = 0.0, xiz_p = 0.0;
@@ -484,6 +521,143 @@ __global__ void __launch_bounds__(XTHREADS, 1) k_x_warp(Geo g, const double2* __
   if constexpr (CL) bulk::cluster_sync();  // neither CTA retires while its partner may still read its scratch
 }
 
+// ---------------------------------------------------------------- y pass, 1024
+// The 1024-point y pass on the same machinery: a tile is (component, x, 8 kz
+// columns) x 1024 y-rows, split over the CTA pair by row parity.  One transform
+// per tile, three tiles in flight per CTA (a ring of three 64 KB buffers, each
+// with its copy warp).  Forward: the tile arrives as this CTA's parity rows
+// (4-D tensor map), the result -- frequencies in kslot order, which for CTA r
+// are four blocks of 128 consecutive frequencies -- is written block-wise into
+// the same buffer and stored with the natural-order map; the inverse pass runs
+// the mirror image.
+struct YwMaps {
+  CUtensorMap split;  // [C Nx][Ny / 2][2][2 nzh]: box = 256 rows of one parity
+  CUtensorMap nat;    // [C Nx][Ny][2 nzh]: box = 128 consecutive rows
+};
+// CTA r holds the frequencies of blocks {0, 3, 4, 7} (r = 0) or {1, 2, 5, 6} (r = 1) of 128; its buffer
+// keeps them in that order.
+__device__ __forceinline__ int yw_local_row(int f, unsigned r) {
+  const int blk = f >> 7, hi = blk >> 2, lo = blk & 3;
+  const int idx = r == 0 ? (lo ? 1 : 0) : lo - 1;
+  return ((2 * hi + idx) << 7) + (f & 127);
+}
+__device__ __forceinline__ int yw_block_row0(int lb, unsigned r) {  // first global row of local block lb
+  const int hi = lb >> 1, idx = lb & 1;
+  const int lo = r == 0 ? (idx ? 3 : 0) : idx + 1;
+  return (4 * hi + lo) << 7;
+}
+
+template <int SIGN>
+__global__ void __launch_bounds__(XTHREADS, 1) k_y_warp(int nzh, const double2* __restrict__ tw, int tiles,
+                                                        const __grid_constant__ YwMaps maps) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* const sm0 = smraw + ((1024u - (bulk::smem_addr(smraw) & 1023u)) & 1023u);
+  unsigned char* const scr0 = sm0 + 3 * XTILE;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(scr0 + XTW * XSCR);
+  uint64_t* const full = bars + 0;    // [3] the buffer's tile has arrived
+  uint64_t* const staged = bars + 3;  // [3] all 8 warps have written their results into the buffer
+  uint64_t* const ready = bars + 8;
+  uint64_t* const freeb = bars + 16;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 3; ++b) {
+      bulk::mbar_init(full + b, 1);
+      bulk::mbar_init(staged + b, XTW);
+    }
+    for (int i = 0; i < XTW; ++i) {
+      bulk::mbar_init(ready + i, 1);
+      bulk::mbar_init(freeb + i, 1);
+    }
+  }
+  __syncthreads();
+  const unsigned crank = bulk::cluster_ctarank();
+  bulk::cluster_sync();
+  const int kzb = nzh / XTW;
+  const int unit = int(blockIdx.x >> 1), units = int(gridDim.x >> 1);
+  const int K = unit < tiles ? (tiles - 1 - unit) / units + 1 : 0;
+  auto tile_of = [&](int k, int& kz0, int& cx) {
+    const int T_ = unit + k * units;
+    kz0 = (T_ % kzb) * XTW;
+    cx = T_ / kzb;
+  };
+
+  if (w >= XTW) {  // --------------------------------------------- copy warps
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::);
+    const int buf = w - XTW;
+    if (buf <= 2 && lane == 0) {
+      unsigned char* const tile = sm0 + buf * XTILE;
+      // SIGN < 0 reads parity rows and writes frequency blocks; SIGN > 0 the other way round
+      auto move = [&](int k, bool in) {
+        int kz0, cx;
+        tile_of(k, kz0, cx);
+        if (in) bulk::mbar_expect_tx(full + buf, XTILE);
+        if ((SIGN < 0) == in) {
+#pragma unroll
+          for (int r0 = 0; r0 < XN; r0 += 256) {
+            if (in) bulk::tma4d(tile + r0 * 128, &maps.split, 2 * kz0, int(crank), r0, cx, full + buf);
+            else bulk::tma4d_store(&maps.split, 2 * kz0, int(crank), r0, cx, tile + r0 * 128);
+          }
+        } else {
+#pragma unroll
+          for (int lb = 0; lb < 4; ++lb) {
+            if (in) bulk::tma3d(tile + lb * 128 * 128, &maps.nat, 2 * kz0, yw_block_row0(lb, crank), cx, full + buf);
+            else bulk::tma3d_store(&maps.nat, 2 * kz0, yw_block_row0(lb, crank), cx, tile + lb * 128 * 128);
+          }
+        }
+        if (!in) bulk::bulk_commit();
+      };
+      if (buf < K) move(buf, true);
+      for (int k = buf; k < K; k += 3) {
+        while (!bulk::mbar_test(staged + buf, (k / 3) & 1)) __nanosleep(128);
+        move(k, false);
+        if (k + 3 < K) {
+          bulk::bulk_wait_read();
+          move(k + 3, true);
+        }
+      }
+      bulk::bulk_wait_all();
+    }
+    bulk::cluster_sync();
+    return;
+  }
+
+  // --------------------------------------------------------- transform warps
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::);
+  WarpLine<true> L;
+  L.init(lane, w, crank, scr0, ready, freeb, tw);
+  if (SIGN > 0) L.signal_free();  // an inverse transform starts with its cross step
+  const int col = (lane << 7) + ((w ^ (lane & 7)) << 4);  // row lane + 32 m, column w, swizzled
+  double2 v[XE];
+  for (int k = 0; k < K; ++k) {
+    const int b = k % 3;
+    unsigned char* const base = sm0 + b * XTILE;
+    bulk::mbar_wait(full + b, (k / 3) & 1);
+    if (SIGN < 0) {
+#pragma unroll
+      for (int m = 0; m < XE; ++m) v[m] = *reinterpret_cast<const double2*>(base + col + (m << 12));
+      L.fwd(v, false);
+#pragma unroll
+      for (int s = 0; s < XE; ++s) {
+        const int lr = yw_local_row(L.kx_of(s), crank);
+        *reinterpret_cast<double2*>(base + (lr << 7) + ((w ^ (lr & 7)) << 4)) = v[s];
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < XE; ++s) {
+        const int lr = yw_local_row(L.kx_of(s), crank);
+        v[s] = *reinterpret_cast<const double2*>(base + (lr << 7) + ((w ^ (lr & 7)) << 4));
+      }
+      L.inv(v, true);
+#pragma unroll
+      for (int m = 0; m < XE; ++m) *reinterpret_cast<double2*>(base + col + (m << 12)) = v[m];
+    }
+    bulk::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) bulk::mbar_arrive(staged + b);
+  }
+  bulk::cluster_sync();
+}
+
 }  // namespace
 
 bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
@@ -574,6 +748,42 @@ bool xw_launch(fm_ctx* ctx, const Geo& g, double2* spec, int dbg) {
             h[6] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, h[5] / n);
   }
   return true;
+}
+
+bool yw_launch(fm_ctx* ctx, const Geo& g, int sign, double2* spec) {
+  if (g.Ny != 2 * XN || g.P != 1 || g.nzh % XTW != 0) return false;
+  const uint64_t ncx = uint64_t(ctx->ncomp) * g.Nx, nzh = uint64_t(g.nzh), Ny = uint64_t(g.Ny);
+  YwMaps maps;
+  {
+    const uint64_t d[4] = {2 * nzh, 2, Ny / 2, ncx}, st[3] = {nzh * 16, 2 * nzh * 16, Ny * nzh * 16};
+    const uint32_t b[4] = {2 * XTW, 1, 256, 1};
+    if (!tensor_map_encode(spec, 4, d, st, b, true, &maps.split)) return false;
+  }
+  {
+    const uint64_t d[3] = {2 * nzh, Ny, ncx}, st[2] = {nzh * 16, Ny * nzh * 16};
+    const uint32_t b[3] = {2 * XTW, 128, 1};
+    if (!tensor_map_encode(spec, 3, d, st, b, true, &maps.nat)) return false;
+  }
+  using Kern = void (*)(int, const double2*, int, const YwMaps);
+  const Kern kern = sign < 0 ? k_y_warp<-1> : k_y_warp<+1>;
+  set_smem_limit(reinterpret_cast<const void*>(kern), int(XSMEM));
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = int(nzh / XTW) * int(ncx);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(XTHREADS);
+  cfg.dynamicSmemBytes = XSMEM;
+  cfg.stream = ctx->stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(2 * std::min(tiles, std::max(sms / 2, 1)));
+  return cudaLaunchKernelEx(&cfg, kern, g.nzh, static_cast<const double2*>(ctx->py.tw), tiles, maps) == cudaSuccess;
 }
 
 }  // namespace fm

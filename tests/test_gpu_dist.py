@@ -33,6 +33,12 @@ def test_virtual_ranks_bitwise_equal(pts, P):
         assert ctx.ranks() == (P, 0, True)
         gp = ctx.projection(fa).download()
         mp = ctx.projected_tangent(fk, fa).download()
+    if pts[1] == 1024:
+        # P = 1 runs the 2-CTA-cluster y pass (1024 = 2 x 512 across the CTA pair), the slab ranks the
+        # 16 x 16 x 4 k_y_fast: two factorisations of the same transform, equal to round-off
+        assert np.linalg.norm(g1 - gp) <= 1e-14 * np.linalg.norm(g1)
+        assert np.linalg.norm(m1 - mp) <= 1e-14 * np.linalg.norm(m1)
+        return
     assert np.array_equal(g1, gp)
     assert np.array_equal(m1, mp)
 

@@ -284,3 +284,15 @@ def test_cluster_x_pass_1024_matches_default(pts, tmp_path):
     assert "k_x_fast4" in names_def and "k_x_warp" in names_cl, (names_def, names_cl)
     x, y = np.load(a), np.load(b)
     assert np.linalg.norm(x - y) <= 1e-14 * np.linalg.norm(x)
+
+
+@pytest.mark.parametrize("pts", [(8, 1024, 16), (24, 1024, 64)])
+def test_cluster_y_pass_1024_matches_k_y_fast(pts, tmp_path):
+    """The cluster form of the 1024-point y pass (k_y_warp) against k_y_fast
+    (FM_YW1024=0): equal to round-off."""
+    a, b = str(tmp_path / "a.npy"), str(tmp_path / "b.npy")
+    names_def = _sample_child(pts, {"FM_YW1024": "0"}, a)
+    names_cl = _sample_child(pts, {}, b)
+    assert "k_y_fast" in names_def and "k_y_warp" in names_cl, (names_def, names_cl)
+    x, y = np.load(a), np.load(b)
+    assert np.linalg.norm(x - y) <= 1e-14 * np.linalg.norm(x)
