@@ -1744,7 +1744,10 @@ struct ZReg {
   static constexpr int T = M / E;
   static constexpr int LPC = 128 / T;
   static constexpr int THREADS = LPC * T;
-  static constexpr int MINB = 4;
+#ifndef FM_ZREG_MINB256
+#define FM_ZREG_MINB256 4  // CTAs/SM of the 256-point (Nz = 512) z passes; 3 (no spills, 168 registers): 3.22 vs 3.09 ms forward, 3.37 vs 3.35 ms inverse at 512^3
+#endif
+  static constexpr int MINB = M == 256 ? FM_ZREG_MINB256 : 4;
   static constexpr size_t SMEM = size_t(LPC) * M * 16;
   static constexpr bool OK = M >= 16 && 32 % T == 0;
 };
